@@ -1,0 +1,353 @@
+#!/usr/bin/env python
+"""Benchmark of the CSR-k SpMV hot path on B200 (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config C2] [--fp32]
+
+Workload (N = 1): BASELINE.json configs[1], the 3D 7-point Laplacian on a
+256^3 grid (16.8 M rows, 117 M nonzeros), fp64, CSR-k with k = 3 built by
+native Band-k with the model's (SSRS, SRS).  One "step" = one SpMV of the
+whole matrix.  Inputs (1.74 GB per SpMV) are larger than the 126 MB L2, so
+no flush is needed between steps.
+
+  value      kernel-only GFLOP/s, x / y resident in HBM, CUDA events over K
+             back-to-back launches on the launching stream (max over ranks)
+  e2e        same metric through the public drop-in call spmv_csr3(m, x)
+             with pinned host x / y: H2D of x, kernel, D2H of y every step
+  roofline   algorithmic bytes (vals + col_idx + row_ptr + x + y, SURVEY.md
+             §8(d)) per launch / measured launch time, against the measured
+             HBM copy bandwidth (MEASURED_PEAKS.json)
+  cpu_baseline  the reference's CSR-3 algorithm restated in C + OpenMP
+             (oracle/, kind "port"), all host cores, bounded sample
+
+N > 1 (torchrun, one process per GPU): the matrix's super-super-rows are
+split across ranks by nonzeros (paper_2203_05096_b200.dist) and each step
+exchanges the x halo over NCCL before the local SpMV (strong scaling).
+
+``--impl reference`` times the reference's CPU CSR-3 algorithm (the oracle
+port; the Python reference cannot be shipped to the GPU box) on the host
+cores for the same config and prints the same JSON line.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+CONFIG_TEXT = {
+    "C1": "2D 5-point Laplacian 1000x1000 fp64 CSR-k k=3",
+    "C2": "3D 7-point Laplacian 256^3 fp64 CSR-k k=3 on 1 B200",
+    "C3": "3D 27-point stencil 192^3 fp64 CSR-k k=3",
+    "C5": "irregular random-row-length matrix, 5M rows, fp64 CSR-k k=3",
+}
+METRIC = "SpMV GFLOP/s and achieved HBM GB/s (% of peak) at 1/2/4/8 B200 vs host CPU"
+
+
+def measured_peak():
+    path = os.path.join(REPO, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(key):
+    path = os.path.join(REPO, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as fh:
+            return json.load(fh).get(key)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi SM clock / throttle-reason samples during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._thread = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                    timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([s.strip() for s in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._thread = threading.Thread(target=self._run, daemon=True)
+        self._thread.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._thread.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
+                 "sw_power_cap")
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > i + 2 and s[i + 2].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def build_matrix(cfg: str, log):
+    """Host CSR of the config, tuned sizes, native Band-k, device pack."""
+    import paper_2203_05096_b200 as ck
+    from paper_2203_05096_b200 import synthetic
+
+    t0 = time.perf_counter()
+    n, rp, ci, va = synthetic.config_arrays(cfg)
+    a = ck.CsrMatrix(n, n, rp, ci, va, _trusted=True)
+    t_gen = time.perf_counter() - t0
+    stats = ck.compute_stats(a)
+    params = ck.tune_gpu(stats, ck.b200_profile())
+    t0 = time.perf_counter()
+    res = ck.band_k(a, 3, [params.srs, params.ssrs])
+    t_band = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    m = ck.pack_csrk(a, res.perm, res.level_group_sizes)
+    t_pack = time.perf_counter() - t0
+    log(f"[bench] {cfg}: n={n} nnz={a.nnz} gen {t_gen:.1f}s band_k {t_band:.1f}s "
+        f"pack {t_pack:.1f}s sizes ssrs={params.ssrs} srs={params.srs} "
+        f"n_sr={m.num_super_rows} n_ssr={m.num_ssr} variant={params.kernel_variant.value}")
+    x = synthetic.config_x(n)
+    xp = ck.permute_vector(res.perm, x)
+    return a, m, xp, params, {"gen_s": t_gen, "band_k_s": t_band, "pack_s": t_pack}
+
+
+def cpu_baseline(m, xp, budget_s=10.0, threads=None):
+    """Time the oracle's CSR-3 (C + OpenMP restatement of kernels.py:209-221)
+    on the host cores: repeat whole-matrix SpMVs for ~budget_s seconds."""
+    from oracle import oracle as O
+
+    threads = threads or (os.cpu_count() or 1)
+    rows = O.csr3_group_rows(m.sr_ptr, m.ssr_ptr)
+    b = m.base
+    O.spmv_grouped(rows, b.row_ptr, b.col_idx, b.vals, xp, threads)  # warm-up
+    times = []
+    t_start = time.perf_counter()
+    while True:
+        t0 = time.perf_counter()
+        y = O.spmv_grouped(rows, b.row_ptr, b.col_idx, b.vals, xp, threads)
+        times.append(time.perf_counter() - t0)
+        if time.perf_counter() - t_start > budget_s or len(times) >= 50:
+            break
+    mean = sum(times) / len(times)
+    return {"value": round(2.0 * b.nnz / mean / 1e9, 3), "unit": "GFLOP/s",
+            "cores": int(threads), "kind": "port",
+            "sample": f"{len(times)} full SpMVs of the same CSR-k matrix "
+                      f"(oracle/csrk_oracle.c oracle_spmv_grouped, OpenMP static chunks "
+                      f"over super-super-rows), mean {mean * 1e3:.1f} ms"}, y
+
+
+def run_ours(args, log):
+    import torch
+
+    import paper_2203_05096_b200 as ck
+    from paper_2203_05096_b200.bench import spmv_bytes
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1:
+        from paper_2203_05096_b200 import dist
+        return dist.bench_main(args, log)
+    torch.cuda.set_device(0)
+    a, m, xp, params, build_t = build_matrix(args.config, log)
+    n, nnz = a.n_rows, a.nnz
+    f32 = args.fp32
+    dtype = torch.float32 if f32 else torch.float64
+    vbytes = 4 if f32 else 8
+    dims = params.block_dims
+    variant = "strided" if params.kernel_variant.value == "cuda35" else "serial"
+    xd = torch.from_numpy(xp).to("cuda", dtype)
+    yd = torch.empty(n, dtype=dtype, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def step():
+        ck.spmv_device(m, xd, yd, dims=dims, variant=variant, stream=stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    gflops = 2.0 * nnz / (ms * 1e-3) / 1e9
+    algo_bytes = spmv_bytes(n, n, nnz, vbytes)
+    gbs = algo_bytes / (ms * 1e-3) / 1e9
+    peak, peak_src = measured_peak()
+
+    # correctness of the timed output against the drop-in host path
+    y_dev = yd.double().cpu().numpy()
+
+    # e2e: the public drop-in call with pinned host buffers
+    x_pin = torch.empty(n, dtype=torch.float64, pin_memory=True).numpy()
+    x_pin[:] = xp
+    y_pin = torch.empty(n, dtype=torch.float64, pin_memory=True).numpy()
+    for _ in range(max(1, args.warmup)):
+        ck.spmv_csr3(m, x_pin, out=y_pin)
+    e2e_times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        ck.spmv_csr3(m, x_pin, out=y_pin)
+        e2e_times.append(time.perf_counter() - t0)
+    e2e_s = sum(e2e_times) / len(e2e_times)
+    if not f32:
+        assert np.array_equal(y_dev, y_pin), "device-resident and host-path y differ"
+
+    base, _ = cpu_baseline(m, xp, budget_s=args.cpu_budget)
+    key = f"{args.config}_{'f32' if f32 else 'f64'}"
+    line = {
+        "metric": METRIC,
+        "value": round(gflops, 2),
+        "unit": "GFLOP/s",
+        "n_gpus": 1,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms, 4),
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f32" if f32 else "f64",
+        "data": "synthetic (deterministic grid Laplacian, x ~ U[-1,1) seed 0)",
+        "config": {"workload": CONFIG_TEXT.get(args.config, args.config),
+                   "config_id": args.config, "n_rows": n, "nnz": nnz,
+                   "ssrs_target": params.ssrs, "srs_target": params.srs,
+                   "n_sr": m.num_super_rows, "n_ssr": m.num_ssr,
+                   "kernel": f"csrk_stream_kernel ({variant})",
+                   "parallelism": "1 GPU",
+                   "l2": "inputs larger than L2 (algorithmic %.2f GB per step vs 126 MB L2); "
+                         "no flush" % (algo_bytes / 1e9)},
+        "hbm_gbs": round(gbs, 1),
+        "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": peak,
+                     "unit": "GB/s", "frac": round(gbs / peak, 4),
+                     "peak_source": peak_src,
+                     "frac_of_8tbs_nominal": round(gbs / 8000.0, 4),
+                     "traffic": ncu_traffic(key),
+                     "algorithmic_bytes_per_launch": algo_bytes},
+        "e2e": {"value": round(2.0 * nnz / e2e_s / 1e9, 2), "unit": "GFLOP/s",
+                "h2d_bytes_per_step": int(x_pin.nbytes),
+                "d2h_bytes_per_step": int(y_pin.nbytes),
+                "ms_per_step": round(e2e_s * 1e3, 3),
+                "call": "paper_2203_05096_b200.spmv_csr3(m, x_pinned, out=y_pinned)"},
+        "cpu_baseline": base,
+        "gpu_launches": args.steps,
+        "clocks": clk.summary(),
+        "build_seconds": {k: round(v, 2) for k, v in build_t.items()},
+    }
+    return line
+
+
+def run_reference(args, log):
+    """--impl reference: the reference's CPU CSR-3 algorithm (oracle port),
+    all host cores, same config / metric."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return None
+    import paper_2203_05096_b200 as ck  # noqa: F401  (matrix construction only)
+
+    a, m, xp, params, _ = build_matrix(args.config, log)
+    from oracle import oracle as O
+
+    threads = os.cpu_count() or 1
+    rows = O.csr3_group_rows(m.sr_ptr, m.ssr_ptr)
+    b = m.base
+    for _ in range(args.warmup):
+        O.spmv_grouped(rows, b.row_ptr, b.col_idx, b.vals, xp, threads)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        O.spmv_grouped(rows, b.row_ptr, b.col_idx, b.vals, xp, threads)
+        times.append(time.perf_counter() - t0)
+    mean = sum(times) / len(times)
+    val = round(2.0 * a.nnz / mean / 1e9, 3)
+    return {
+        "impl": "reference",
+        "metric": METRIC,
+        "value": val,
+        "unit": "GFLOP/s",
+        "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(mean * 1e3, 3),
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (deterministic grid Laplacian, x ~ U[-1,1) seed 0)",
+        "config": {"workload": CONFIG_TEXT.get(args.config, args.config),
+                   "config_id": args.config, "n_rows": a.n_rows, "nnz": a.nnz},
+        "cpu_baseline": {"value": val, "unit": "GFLOP/s", "cores": threads,
+                         "kind": "port",
+                         "sample": f"{args.steps} whole-matrix SpMVs of the same CSR-k "
+                                   "matrix; the reference's spmv_csr3 algorithm "
+                                   "(kernels.py:209-221) restated in C + OpenMP "
+                                   "(oracle/csrk_oracle.c); the pure-Python reference "
+                                   "cannot travel to the GPU box"},
+        "e2e": {"value": val, "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser(description=__doc__.split("\n")[1])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--config", default="C2", choices=("C1", "C2", "C3", "C5"))
+    ap.add_argument("--fp32", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=10.0)
+    args = ap.parse_args(argv)
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    rank = int(os.environ.get("RANK", "0"))
+
+    def log(msg):
+        if rank == 0:
+            print(msg, file=sys.stderr, flush=True)
+
+    line = run_reference(args, log) if args.impl == "reference" else run_ours(args, log)
+    if rank == 0 and line is not None:
+        print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,198 @@
+/*
+ * csrk.h -- C-ABI of libcsrk_cuda.so, the B200-native CSR-k SpMV.
+ *
+ * The reference (arxiv 2203.05096's `csrk` package, /root/reference/pkg) is
+ * pure Python; its "FFI" for this path is the Python call surface listed in
+ * SURVEY.md §8(b).  Every entry point below names the reference function it
+ * replaces (file:line under pkg/src/csrk/).  The Python package
+ * `paper_2203_05096_b200` binds these through ctypes.
+ *
+ * Conventions
+ *   - plain pointers and sizes only; no torch or CUDA types in signatures
+ *     (streams are passed as `void*` holding a cudaStream_t, NULL = default);
+ *   - indices are uint32 (reference format.py:32 INDEX_DTYPE), values f64
+ *     (format.py:33 VALUE_DTYPE), permutations int64 (format.py:130);
+ *   - every function returns CSRK_OK (0) or an error code; the message of
+ *     the last failure on the calling thread is csrk_last_error();
+ *   - CSRK_EINVAL messages reuse the reference's ValueError wording.
+ */
+#ifndef CSRK_H
+#define CSRK_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CSRK_ABI_VERSION 1
+
+#define CSRK_OK 0
+#define CSRK_EINVAL 1 /* maps to ValueError */
+#define CSRK_ECUDA 2  /* maps to RuntimeError */
+#define CSRK_ENOMEM 3 /* maps to MemoryError */
+
+/* value storage types for csrk_matrix_upload(value_types) bitmask and for
+ * the `value_type` argument of the SpMV entry points */
+#define CSRK_F64 1
+#define CSRK_F32 2
+
+/* summation order of a row (bitwise contract):
+ *   SERIAL  -- strict left-to-right sum, no FMA: kernels.py:117-147 and
+ *              kernels.py:224-228 (spmv_csr_ref / spmv_csr2 / spmv_csr3 /
+ *              emulate_gpu_spmv3 all share it)
+ *   STRIDED -- nonzero p of a row goes to lane p mod nx, lanes summed
+ *              serially, then a zero-padded halving tree:
+ *              kernels.py:264-324 (emulate_gpu_spmv35) */
+#define CSRK_SERIAL 0
+#define CSRK_STRIDED 1
+
+typedef struct csrk_matrix csrk_matrix;
+
+int csrk_abi_version(void);
+const char *csrk_last_error(void);
+int csrk_device_count(int *count);
+
+/* ---- raw device buffers (for callers without another CUDA allocator) ---- */
+int csrk_buffer_alloc(int device, int64_t bytes, void **out);
+int csrk_buffer_free(int device, void *p);
+/* kind: 0 host->device, 1 device->host, 2 device->device; stream may be
+ * NULL (legacy default stream); the copy is complete on return when stream
+ * is NULL, otherwise stream-ordered */
+int csrk_memcpy(void *dst, const void *src, int64_t bytes, int kind,
+                void *stream);
+int csrk_memset(void *dst, int value, int64_t bytes, void *stream);
+int csrk_stream_sync(void *stream);
+int csrk_device_sync(int device);
+
+/* ---- device matrix handle ------------------------------------------------
+ * Replaces the host-resident CsrMatrix / CsrKMatrix (format.py:45-230) on the
+ * device.  k = 1 is plain CSR (group pointers ignored), k = 2 uses sr_ptr
+ * (n_sr + 1 entries), k = 3 uses sr_ptr and ssr_ptr (n_ssr + 1 entries).
+ * Host arrays are only read during the call.  value_types: CSRK_F64 and/or
+ * CSRK_F32 storage to keep resident. */
+int csrk_matrix_upload(int device, int64_t n_rows, int64_t n_cols, int64_t nnz,
+                       const uint32_t *row_ptr, const uint32_t *col_idx,
+                       const double *vals, int k, int64_t n_sr,
+                       const uint32_t *sr_ptr, int64_t n_ssr,
+                       const uint32_t *ssr_ptr, int value_types,
+                       csrk_matrix **out);
+int csrk_matrix_free(csrk_matrix *m);
+/* out[0..6] = n_rows, n_cols, nnz, k, n_sr, n_ssr, device */
+int csrk_matrix_shape(const csrk_matrix *m, int64_t out[7]);
+/* copy the device arrays back; any output pointer may be NULL */
+int csrk_matrix_download(const csrk_matrix *m, uint32_t *row_ptr,
+                         uint32_t *col_idx, double *vals, uint32_t *sr_ptr,
+                         uint32_t *ssr_ptr);
+/* add an f32 copy of the values (for CSRK_F32 SpMV) if not present */
+int csrk_matrix_add_f32(csrk_matrix *m);
+/* Tile plan of the streaming kernel: whole groups (SSRs for k=3, SRs for
+ * k=2, rows for k=1) are packed into CTA tiles of about tile_nnz nonzeros;
+ * cap is the shared-memory stage size in nonzeros.  0 = defaults. */
+int csrk_matrix_set_plan(csrk_matrix *m, int64_t tile_nnz, int64_t cap);
+
+/* ---- SpMV ------------------------------------------------------------------
+ * y = A x on device-resident x / y (already in the permuted index space, as
+ * spmv_csr3 expects, kernels.py:209-221).  Replaces spmv_csr_ref
+ * (kernels.py:97-114, k=1), spmv_csr2 (kernels.py:185-206, k=2),
+ * spmv_csr3 (kernels.py:209-221, k=3) with variant CSRK_SERIAL, and the
+ * arithmetic of emulate_gpu_spmv35 (kernels.py:284-324) with CSRK_STRIDED
+ * and nx = dims.x (1..32).  value_type selects f64 x/y/vals or f32
+ * x/y/vals (f32 products are accumulated in f64 and rounded once).
+ * Asynchronous on `stream`. */
+int csrk_spmv(const csrk_matrix *m, int value_type, int variant, int nx,
+              const void *x, void *y, void *stream);
+/* Same, from host x to host y (H2D, kernel, D2H on an internal stream;
+ * returns when y is written).  The drop-in call shape of spmv_csr3(m, x). */
+int csrk_spmv_host(csrk_matrix *m, int value_type, int variant, int nx,
+                   const void *x_host, void *y_host);
+/* CUDA-event device time of the last csrk_spmv_host kernel, milliseconds */
+int csrk_last_kernel_ms(const csrk_matrix *m, float *ms);
+
+/* Literal paper mappings, with the reference's per-row lane trace
+ * (EmulationTrace, kernels.py:55-87; 7 int64 columns of n_rows entries:
+ * row, block, z_lane, y_lane, x_first, x_count, reduction_depth; may be
+ * NULL).  listing3 = emulate_gpu_spmv3 (kernels.py:231-261, PAPER Listing
+ * 3); listing4 = emulate_gpu_spmv35 (kernels.py:284-324, PAPER Listing 4).
+ * Require k = 3, f64. */
+int csrk_spmv_listing3(const csrk_matrix *m, int dx, int dy, const double *x,
+                       double *y, int64_t *trace, void *stream);
+int csrk_spmv_listing4(const csrk_matrix *m, int dx, int dy, int dz,
+                       const double *x, double *y, int64_t *trace,
+                       void *stream);
+
+/* ---- construction on device ------------------------------------------------
+ * csrk_pack: replaces pack_csrk (format.py:347-393) + _permute_symmetric
+ * (format.py:318-344).  Uploads A (original order) and the permutation,
+ * builds P.A.P^T with per-row column sort and the group pointer arrays
+ * (prefix sums of sizes1 / sizes2) on the device, and returns the packed
+ * handle.  n_levels = 1 (k=2) or 2 (k=3); sizes2 may be NULL for k=2.
+ * Validation (square, sizes positive and summing to the level below) uses
+ * the reference's messages ("level N ..."). */
+int csrk_pack(int device, int64_t n, int64_t nnz, const uint32_t *row_ptr,
+              const uint32_t *col_idx, const double *vals, const int64_t *fwd,
+              const int64_t *inv, int n_levels, int64_t n_sizes1,
+              const int64_t *sizes1, int64_t n_sizes2, const int64_t *sizes2,
+              csrk_matrix **out);
+/* permute_vector / unpermute_vector (format.py:396-409) on device:
+ * out[i] = in[idx[i]] with idx = perm.inv (permute) or perm.fwd (unpermute);
+ * f64, device pointers, asynchronous. */
+int csrk_gather_f64(int64_t n, const double *in, const int64_t *idx,
+                    double *out, void *stream);
+/* compute_stats (tuning.py:108-134) integer parts on the device:
+ * out[0] = sum(row_nnz), out[1] = sum(row_nnz^2), out[2] = max row_nnz,
+ * out[3] = off-diagonal count, out[4] = off-diagonal entries whose
+ * transpose is present.  Works on any handle (uses its current arrays). */
+int csrk_stats(const csrk_matrix *m, int64_t out[5]);
+/* float(np.var(row_nnz)) bit for bit (tuning.py:130): numpy's pairwise
+ * summation of (row_nnz - mean)^2 divided by n_rows; `mean` must be
+ * float(nnz) / n_rows as numpy computes it. */
+int csrk_row_variance(const csrk_matrix *m, double mean, double *out);
+
+/* Synthetic stencil generator writing canonical CSR on the device
+ * (SURVEY.md §8(d)); shape = {nz, ny, nx} (nz = 1 for 2D), points = 5, 7, 27.
+ * Produces a k = 1 handle (natural order). */
+int csrk_stencil(int device, int64_t nz, int64_t ny, int64_t nx, int points,
+                 csrk_matrix **out);
+
+/* ---- Band-k reordering (native) -------------------------------------------
+ * Bit-exact native restatement of reorder.py (band_k 415-469 and its
+ * helpers).  Results are held in an opaque object and read back with
+ * csrk_bandk_result_get. */
+typedef struct csrk_bandk_result csrk_bandk_result;
+int csrk_band_k(int64_t n, const uint32_t *row_ptr, const uint32_t *col_idx,
+                int k, const double *targets, csrk_bandk_result **out);
+/* sizes: out[0] = n, out[1] = len(level 1 sizes), out[2] = len(level 2) */
+int csrk_bandk_result_sizes(const csrk_bandk_result *r, int64_t out[3]);
+int csrk_bandk_result_get(const csrk_bandk_result *r, int64_t *fwd,
+                          int64_t *sizes1, int64_t *sizes2);
+int csrk_bandk_result_free(csrk_bandk_result *r);
+
+/* Graph-level pieces of reorder.py on the reference's AdjacencyGraph arrays
+ * (int64 CSR adjacency, reorder.py:35-58). */
+/* heavy_edge_matching (reorder.py:138-173): match[n] */
+int csrk_heavy_edge_matching(int64_t n, const int64_t *adj_ptr,
+                             const int64_t *adj_idx,
+                             const int64_t *edge_weight, int64_t *match);
+/* weighted_bandwidth_order (reorder.py:281-336): fwd[n] */
+int csrk_weighted_bandwidth_order(int64_t n, const int64_t *adj_ptr,
+                                  const int64_t *adj_idx,
+                                  const int64_t *node_weight, int64_t *fwd);
+/* build_graph (reorder.py:115-135) and coarsen (reorder.py:199-237) return
+ * an opaque graph (plus the fine-to-coarse map for coarsen) read back with
+ * csrk_graph_sizes (out = n, adjacency length, f2c length) / csrk_graph_get. */
+typedef struct csrk_graph csrk_graph;
+int csrk_build_graph(int64_t n, const uint32_t *row_ptr,
+                     const uint32_t *col_idx, csrk_graph **out);
+int csrk_coarsen(int64_t n, const int64_t *adj_ptr, const int64_t *adj_idx,
+                 const int64_t *edge_weight, const int64_t *node_weight,
+                 double target, csrk_graph **out);
+int csrk_graph_sizes(const csrk_graph *g, int64_t out[3]);
+int csrk_graph_get(const csrk_graph *g, int64_t *adj_ptr, int64_t *adj_idx,
+                   int64_t *edge_weight, int64_t *node_weight, int64_t *f2c);
+int csrk_graph_free(csrk_graph *g);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CSRK_H */

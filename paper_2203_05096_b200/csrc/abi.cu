@@ -1,0 +1,431 @@
+// extern "C" entry points of libcsrk_cuda.so (declared in include/csrk.h).
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "internal.h"
+
+namespace csrk {
+
+static thread_local std::string g_last_error;
+
+void set_error(const char *fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+}
+
+int alloc_matrix_arrays(csrk_matrix *m, bool want64, bool want32) {
+  const int64_t pn = padded_nnz(m->nnz);
+  CSRK_CUDA_TRY(cudaMalloc(&m->row_ptr, (m->n_rows + 1) * sizeof(uint32_t)));
+  CSRK_CUDA_TRY(cudaMalloc(&m->col_idx, pn * sizeof(uint32_t)));
+  CSRK_CUDA_TRY(cudaMemset(m->col_idx, 0, pn * sizeof(uint32_t)));
+  if (want64) {
+    CSRK_CUDA_TRY(cudaMalloc(&m->vals64, pn * sizeof(double)));
+    CSRK_CUDA_TRY(cudaMemset(m->vals64, 0, pn * sizeof(double)));
+  }
+  if (want32) {
+    CSRK_CUDA_TRY(cudaMalloc(&m->vals32, pn * sizeof(float)));
+    CSRK_CUDA_TRY(cudaMemset(m->vals32, 0, pn * sizeof(float)));
+  }
+  if (m->k >= 2)
+    CSRK_CUDA_TRY(cudaMalloc(&m->sr_ptr, (m->n_sr + 1) * sizeof(uint32_t)));
+  if (m->k == 3)
+    CSRK_CUDA_TRY(cudaMalloc(&m->ssr_ptr, (m->n_ssr + 1) * sizeof(uint32_t)));
+  CSRK_CUDA_TRY(cudaStreamCreateWithFlags(&m->stream, cudaStreamNonBlocking));
+  CSRK_CUDA_TRY(cudaEventCreate(&m->ev0));
+  CSRK_CUDA_TRY(cudaEventCreate(&m->ev1));
+  return CSRK_OK;
+}
+
+static void release(csrk_matrix *m) {
+  if (!m) return;
+  int cur = 0;
+  cudaGetDevice(&cur);
+  cudaSetDevice(m->device);
+  cudaFree(m->row_ptr);
+  cudaFree(m->col_idx);
+  cudaFree(m->vals64);
+  cudaFree(m->vals32);
+  cudaFree(m->sr_ptr);
+  cudaFree(m->ssr_ptr);
+  cudaFree(m->plan.tile_row);
+  cudaFree(m->x_stage);
+  cudaFree(m->y_stage);
+  if (m->ev0) cudaEventDestroy(m->ev0);
+  if (m->ev1) cudaEventDestroy(m->ev1);
+  if (m->stream) cudaStreamDestroy(m->stream);
+  delete m;
+  cudaSetDevice(cur);
+}
+
+// Validation of a packed layout, with the reference's messages
+// (format.py:71-98 CsrMatrix, format.py:180-202 CsrKMatrix).
+static int validate_host(int64_t n_rows, int64_t n_cols, int64_t nnz,
+                         const uint32_t *row_ptr, int k, int64_t n_sr,
+                         const uint32_t *sr_ptr, int64_t n_ssr,
+                         const uint32_t *ssr_ptr) {
+  if (n_rows < 0 || n_cols < 0) {
+    set_error("matrix dimensions must be non-negative");
+    return CSRK_EINVAL;
+  }
+  if (nnz > 2147483647LL) {
+    set_error("nnz %lld exceeds the 32-bit index limit 2147483647",
+              static_cast<long long>(nnz));
+    return CSRK_EINVAL;
+  }
+  if (row_ptr[0] != 0) {
+    set_error("row_ptr[0] must be 0");
+    return CSRK_EINVAL;
+  }
+  if (static_cast<int64_t>(row_ptr[n_rows]) != nnz) {
+    set_error("col_idx and vals must have length row_ptr[-1]");
+    return CSRK_EINVAL;
+  }
+  if (k < 1 || k > 3) {
+    set_error("k must be 2 or 3");
+    return CSRK_EINVAL;
+  }
+  const uint32_t *ptrs[2] = {sr_ptr, ssr_ptr};
+  const int64_t lens[2] = {n_sr, n_ssr};
+  int64_t below = n_rows;
+  for (int level = 1; level < k; ++level) {
+    const uint32_t *p = ptrs[level - 1];
+    const int64_t len = lens[level - 1];
+    if (!p || len < 0 || p[0] != 0) {
+      set_error("level %d pointer array must start at 0", level);
+      return CSRK_EINVAL;
+    }
+    for (int64_t i = 0; i < len; ++i)
+      if (p[i + 1] <= p[i]) {
+        set_error("level %d pointer array must be strictly increasing", level);
+        return CSRK_EINVAL;
+      }
+    if (static_cast<int64_t>(p[len]) != below) {
+      set_error("level %d pointer array must end at %lld, got %lld", level,
+                static_cast<long long>(below), static_cast<long long>(p[len]));
+      return CSRK_EINVAL;
+    }
+    below = len;
+  }
+  return CSRK_OK;
+}
+
+}  // namespace csrk
+
+using namespace csrk;
+
+extern "C" {
+
+int csrk_abi_version(void) { return CSRK_ABI_VERSION; }
+
+const char *csrk_last_error(void) { return g_last_error.c_str(); }
+
+int csrk_device_count(int *count) {
+  CSRK_CUDA_TRY(cudaGetDeviceCount(count));
+  return CSRK_OK;
+}
+
+int csrk_buffer_alloc(int device, int64_t bytes, void **out) {
+  if (!out || bytes < 0) {
+    set_error("invalid buffer request");
+    return CSRK_EINVAL;
+  }
+  CSRK_CUDA_TRY(cudaSetDevice(device));
+  CSRK_CUDA_TRY(cudaMalloc(out, bytes > 0 ? static_cast<size_t>(bytes) : 16));
+  return CSRK_OK;
+}
+
+int csrk_buffer_free(int device, void *p) {
+  if (!p) return CSRK_OK;
+  CSRK_CUDA_TRY(cudaSetDevice(device));
+  CSRK_CUDA_TRY(cudaFree(p));
+  return CSRK_OK;
+}
+
+int csrk_memcpy(void *dst, const void *src, int64_t bytes, int kind,
+                void *stream) {
+  if (bytes <= 0) return CSRK_OK;
+  const cudaMemcpyKind k = kind == 0   ? cudaMemcpyHostToDevice
+                           : kind == 1 ? cudaMemcpyDeviceToHost
+                                       : cudaMemcpyDeviceToDevice;
+  if (stream) {
+    CSRK_CUDA_TRY(cudaMemcpyAsync(dst, src, static_cast<size_t>(bytes), k,
+                                  static_cast<cudaStream_t>(stream)));
+  } else {
+    CSRK_CUDA_TRY(cudaMemcpy(dst, src, static_cast<size_t>(bytes), k));
+  }
+  return CSRK_OK;
+}
+
+int csrk_memset(void *dst, int value, int64_t bytes, void *stream) {
+  if (bytes <= 0) return CSRK_OK;
+  CSRK_CUDA_TRY(cudaMemsetAsync(dst, value, static_cast<size_t>(bytes),
+                                static_cast<cudaStream_t>(stream)));
+  if (!stream) CSRK_CUDA_TRY(cudaStreamSynchronize(nullptr));
+  return CSRK_OK;
+}
+
+int csrk_stream_sync(void *stream) {
+  CSRK_CUDA_TRY(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+  return CSRK_OK;
+}
+
+int csrk_device_sync(int device) {
+  CSRK_CUDA_TRY(cudaSetDevice(device));
+  CSRK_CUDA_TRY(cudaDeviceSynchronize());
+  return CSRK_OK;
+}
+
+int csrk_matrix_upload(int device, int64_t n_rows, int64_t n_cols, int64_t nnz,
+                       const uint32_t *row_ptr, const uint32_t *col_idx,
+                       const double *vals, int k, int64_t n_sr,
+                       const uint32_t *sr_ptr, int64_t n_ssr,
+                       const uint32_t *ssr_ptr, int value_types,
+                       csrk_matrix **out) {
+  if (!out || !row_ptr || (nnz > 0 && (!col_idx || !vals))) {
+    set_error("null argument");
+    return CSRK_EINVAL;
+  }
+  *out = nullptr;
+  CSRK_TRY(validate_host(n_rows, n_cols, nnz, row_ptr, k, n_sr, sr_ptr, n_ssr,
+                         ssr_ptr));
+  if ((value_types & (CSRK_F64 | CSRK_F32)) == 0) value_types = CSRK_F64;
+  // a column >= n_cols would read outside x
+  for (int64_t p = 0; p < nnz; ++p)
+    if (static_cast<int64_t>(col_idx[p]) >= n_cols) {
+      set_error("column index out of range");
+      return CSRK_EINVAL;
+    }
+  CSRK_CUDA_TRY(cudaSetDevice(device));
+  csrk_matrix *m = new csrk_matrix();
+  m->device = device;
+  m->n_rows = n_rows;
+  m->n_cols = n_cols;
+  m->nnz = nnz;
+  m->k = k;
+  m->n_sr = k >= 2 ? n_sr : 0;
+  m->n_ssr = k == 3 ? n_ssr : 0;
+  int rc = alloc_matrix_arrays(m, true, (value_types & CSRK_F32) != 0);
+  if (rc != CSRK_OK) {
+    release(m);
+    return rc;
+  }
+  auto fail = [&](cudaError_t e) {
+    set_error("CUDA error %s during upload: %s", cudaGetErrorName(e),
+              cudaGetErrorString(e));
+    release(m);
+    return CSRK_ECUDA;
+  };
+  cudaError_t e;
+  if ((e = cudaMemcpy(m->row_ptr, row_ptr, (n_rows + 1) * sizeof(uint32_t),
+                      cudaMemcpyHostToDevice)) != cudaSuccess)
+    return fail(e);
+  if (nnz > 0) {
+    if ((e = cudaMemcpy(m->col_idx, col_idx, nnz * sizeof(uint32_t),
+                        cudaMemcpyHostToDevice)) != cudaSuccess)
+      return fail(e);
+    if ((e = cudaMemcpy(m->vals64, vals, nnz * sizeof(double),
+                        cudaMemcpyHostToDevice)) != cudaSuccess)
+      return fail(e);
+  }
+  if (k >= 2 && (e = cudaMemcpy(m->sr_ptr, sr_ptr, (n_sr + 1) * sizeof(uint32_t),
+                                cudaMemcpyHostToDevice)) != cudaSuccess)
+    return fail(e);
+  if (k == 3 &&
+      (e = cudaMemcpy(m->ssr_ptr, ssr_ptr, (n_ssr + 1) * sizeof(uint32_t),
+                      cudaMemcpyHostToDevice)) != cudaSuccess)
+    return fail(e);
+  if (m->vals32) {
+    rc = launch_f64_to_f32(m->vals64, m->vals32, nnz, m->stream);
+    if (rc != CSRK_OK) {
+      release(m);
+      return rc;
+    }
+  }
+  rc = ensure_plan(m, 0, 0, m->stream);
+  if (rc == CSRK_OK && (e = cudaStreamSynchronize(m->stream)) != cudaSuccess)
+    return fail(e);
+  if (rc != CSRK_OK) {
+    release(m);
+    return rc;
+  }
+  *out = m;
+  return CSRK_OK;
+}
+
+int csrk_matrix_free(csrk_matrix *m) {
+  release(m);
+  return CSRK_OK;
+}
+
+int csrk_matrix_shape(const csrk_matrix *m, int64_t out[7]) {
+  if (!m || !out) {
+    set_error("null argument");
+    return CSRK_EINVAL;
+  }
+  out[0] = m->n_rows;
+  out[1] = m->n_cols;
+  out[2] = m->nnz;
+  out[3] = m->k;
+  out[4] = m->n_sr;
+  out[5] = m->n_ssr;
+  out[6] = m->device;
+  return CSRK_OK;
+}
+
+int csrk_matrix_download(const csrk_matrix *m, uint32_t *row_ptr,
+                         uint32_t *col_idx, double *vals, uint32_t *sr_ptr,
+                         uint32_t *ssr_ptr) {
+  if (!m) {
+    set_error("null argument");
+    return CSRK_EINVAL;
+  }
+  CSRK_CUDA_TRY(cudaSetDevice(m->device));
+  CSRK_CUDA_TRY(cudaStreamSynchronize(m->stream));
+  if (row_ptr)
+    CSRK_CUDA_TRY(cudaMemcpy(row_ptr, m->row_ptr,
+                             (m->n_rows + 1) * sizeof(uint32_t),
+                             cudaMemcpyDeviceToHost));
+  if (col_idx && m->nnz)
+    CSRK_CUDA_TRY(cudaMemcpy(col_idx, m->col_idx, m->nnz * sizeof(uint32_t),
+                             cudaMemcpyDeviceToHost));
+  if (vals && m->nnz)
+    CSRK_CUDA_TRY(cudaMemcpy(vals, m->vals64, m->nnz * sizeof(double),
+                             cudaMemcpyDeviceToHost));
+  if (sr_ptr && m->k >= 2)
+    CSRK_CUDA_TRY(cudaMemcpy(sr_ptr, m->sr_ptr, (m->n_sr + 1) * sizeof(uint32_t),
+                             cudaMemcpyDeviceToHost));
+  if (ssr_ptr && m->k == 3)
+    CSRK_CUDA_TRY(cudaMemcpy(ssr_ptr, m->ssr_ptr,
+                             (m->n_ssr + 1) * sizeof(uint32_t),
+                             cudaMemcpyDeviceToHost));
+  return CSRK_OK;
+}
+
+int csrk_matrix_add_f32(csrk_matrix *m) {
+  if (!m) {
+    set_error("null argument");
+    return CSRK_EINVAL;
+  }
+  if (m->vals32) return CSRK_OK;
+  CSRK_CUDA_TRY(cudaSetDevice(m->device));
+  const int64_t pn = padded_nnz(m->nnz);
+  CSRK_CUDA_TRY(cudaMalloc(&m->vals32, pn * sizeof(float)));
+  CSRK_CUDA_TRY(cudaMemsetAsync(m->vals32, 0, pn * sizeof(float), m->stream));
+  CSRK_TRY(launch_f64_to_f32(m->vals64, m->vals32, m->nnz, m->stream));
+  CSRK_CUDA_TRY(cudaStreamSynchronize(m->stream));
+  return CSRK_OK;
+}
+
+int csrk_matrix_set_plan(csrk_matrix *m, int64_t tile_nnz, int64_t cap) {
+  if (!m) {
+    set_error("null argument");
+    return CSRK_EINVAL;
+  }
+  CSRK_CUDA_TRY(cudaSetDevice(m->device));
+  CSRK_TRY(ensure_plan(m, tile_nnz, cap, m->stream));
+  CSRK_CUDA_TRY(cudaStreamSynchronize(m->stream));
+  return CSRK_OK;
+}
+
+int csrk_spmv(const csrk_matrix *m, int value_type, int variant, int nx,
+              const void *x, void *y, void *stream) {
+  if (!m || (m->n_rows > 0 && (!x || !y))) {
+    set_error("null argument");
+    return CSRK_EINVAL;
+  }
+  CSRK_CUDA_TRY(cudaSetDevice(m->device));
+  return launch_spmv(m, value_type, variant, nx, x, y,
+                     static_cast<cudaStream_t>(stream));
+}
+
+int csrk_spmv_host(csrk_matrix *m, int value_type, int variant, int nx,
+                   const void *x_host, void *y_host) {
+  if (!m || (m->n_rows > 0 && (!x_host || !y_host))) {
+    set_error("null argument");
+    return CSRK_EINVAL;
+  }
+  const size_t es = value_type == CSRK_F32 ? sizeof(float) : sizeof(double);
+  CSRK_CUDA_TRY(cudaSetDevice(m->device));
+  const size_t xb = static_cast<size_t>(m->n_cols) * es + 16;
+  const size_t yb = static_cast<size_t>(m->n_rows) * es + 16;
+  if (m->x_stage_bytes < xb) {
+    cudaFree(m->x_stage);
+    m->x_stage = nullptr;
+    CSRK_CUDA_TRY(cudaMalloc(&m->x_stage, xb));
+    m->x_stage_bytes = xb;
+  }
+  if (m->y_stage_bytes < yb) {
+    cudaFree(m->y_stage);
+    m->y_stage = nullptr;
+    CSRK_CUDA_TRY(cudaMalloc(&m->y_stage, yb));
+    m->y_stage_bytes = yb;
+  }
+  if (m->n_cols)
+    CSRK_CUDA_TRY(cudaMemcpyAsync(m->x_stage, x_host, m->n_cols * es,
+                                  cudaMemcpyHostToDevice, m->stream));
+  CSRK_CUDA_TRY(cudaEventRecord(m->ev0, m->stream));
+  CSRK_TRY(launch_spmv(m, value_type, variant, nx, m->x_stage, m->y_stage,
+                       m->stream));
+  CSRK_CUDA_TRY(cudaEventRecord(m->ev1, m->stream));
+  if (m->n_rows)
+    CSRK_CUDA_TRY(cudaMemcpyAsync(y_host, m->y_stage, m->n_rows * es,
+                                  cudaMemcpyDeviceToHost, m->stream));
+  CSRK_CUDA_TRY(cudaStreamSynchronize(m->stream));
+  return CSRK_OK;
+}
+
+int csrk_last_kernel_ms(const csrk_matrix *m, float *ms) {
+  if (!m || !ms) {
+    set_error("null argument");
+    return CSRK_EINVAL;
+  }
+  CSRK_CUDA_TRY(cudaEventElapsedTime(ms, m->ev0, m->ev1));
+  return CSRK_OK;
+}
+
+int csrk_spmv_listing3(const csrk_matrix *m, int dx, int dy, const double *x,
+                       double *y, int64_t *trace, void *stream) {
+  if (!m) {
+    set_error("null argument");
+    return CSRK_EINVAL;
+  }
+  if (m->k != 3) {
+    set_error("emulate_gpu_spmv3 requires k = 3");
+    return CSRK_EINVAL;
+  }
+  if (dx < 1 || dy < 1 || dx * dy > 1024) {
+    set_error("block holds %d threads, limit is 1024", dx * dy);
+    return CSRK_EINVAL;
+  }
+  CSRK_CUDA_TRY(cudaSetDevice(m->device));
+  return launch_listing3(m, dx, dy, x, y, trace,
+                         static_cast<cudaStream_t>(stream));
+}
+
+int csrk_spmv_listing4(const csrk_matrix *m, int dx, int dy, int dz,
+                       const double *x, double *y, int64_t *trace,
+                       void *stream) {
+  if (!m) {
+    set_error("null argument");
+    return CSRK_EINVAL;
+  }
+  if (m->k != 3) {
+    set_error("emulate_gpu_spmv35 requires k = 3");
+    return CSRK_EINVAL;
+  }
+  if (dx < 1 || dy < 1 || dz < 1 || dx * dy * dz > 1024) {
+    set_error("block holds %d threads, limit is 1024", dx * dy * dz);
+    return CSRK_EINVAL;
+  }
+  CSRK_CUDA_TRY(cudaSetDevice(m->device));
+  return launch_listing4(m, dx, dy, dz, x, y, trace,
+                         static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

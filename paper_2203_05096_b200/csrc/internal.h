@@ -1,0 +1,80 @@
+// Internal declarations shared by the translation units of libcsrk_cuda.so.
+#pragma once
+
+#include <cstdarg>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+
+#include <cuda_runtime.h>
+
+#include "../../include/csrk.h"
+
+namespace csrk {
+
+void set_error(const char *fmt, ...);
+
+// A tile plan of the streaming kernel: tile t covers rows
+// [tile_row[t], tile_row[t+1]) made of whole groups.
+struct TilePlan {
+  int64_t tile_nnz = 0;  // requested nonzeros per tile
+  int64_t cap = 0;       // shared-memory stage, nonzeros
+  int64_t n_tiles = 0;
+  uint32_t *tile_row = nullptr;  // device, n_tiles + 1
+};
+
+}  // namespace csrk
+
+struct csrk_matrix {
+  int device = 0;
+  int64_t n_rows = 0, n_cols = 0, nnz = 0;
+  int k = 1;
+  int64_t n_sr = 0, n_ssr = 0;
+  uint32_t *row_ptr = nullptr;  // n_rows + 1
+  uint32_t *col_idx = nullptr;  // nnz, padded to a multiple of 4 (+4)
+  double *vals64 = nullptr;     // nnz, padded
+  float *vals32 = nullptr;      // optional
+  uint32_t *sr_ptr = nullptr;   // n_sr + 1 (k >= 2)
+  uint32_t *ssr_ptr = nullptr;  // n_ssr + 1 (k == 3)
+  csrk::TilePlan plan;          // current streaming plan
+  // host-API staging
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  void *x_stage = nullptr, *y_stage = nullptr;
+  size_t x_stage_bytes = 0, y_stage_bytes = 0;
+};
+
+namespace csrk {
+
+// padded element count for col_idx / vals allocations: room for the 16-byte
+// aligned over-read of the TMA bulk copies at both ends of a span.
+inline int64_t padded_nnz(int64_t nnz) { return ((nnz + 3) / 4) * 4 + 8; }
+
+int alloc_matrix_arrays(csrk_matrix *m, bool want64, bool want32);
+int ensure_plan(csrk_matrix *m, int64_t tile_nnz, int64_t cap, cudaStream_t s);
+int launch_spmv(const csrk_matrix *m, int value_type, int variant, int nx,
+                const void *x, void *y, cudaStream_t stream);
+int launch_listing3(const csrk_matrix *m, int dx, int dy, const double *x,
+                    double *y, int64_t *trace, cudaStream_t stream);
+int launch_listing4(const csrk_matrix *m, int dx, int dy, int dz,
+                    const double *x, double *y, int64_t *trace,
+                    cudaStream_t stream);
+int launch_f64_to_f32(const double *in, float *out, int64_t n, cudaStream_t s);
+
+}  // namespace csrk
+
+#define CSRK_CUDA_TRY(expr)                                                 \
+  do {                                                                      \
+    cudaError_t e_ = (expr);                                                \
+    if (e_ != cudaSuccess) {                                                \
+      csrk::set_error("CUDA error %s at %s:%d: %s", cudaGetErrorName(e_),   \
+                      __FILE__, __LINE__, cudaGetErrorString(e_));          \
+      return e_ == cudaErrorMemoryAllocation ? CSRK_ENOMEM : CSRK_ECUDA;    \
+    }                                                                       \
+  } while (0)
+
+#define CSRK_TRY(expr)            \
+  do {                            \
+    int rc_ = (expr);             \
+    if (rc_ != CSRK_OK) return rc_; \
+  } while (0)
