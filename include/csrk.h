@@ -86,10 +86,15 @@ int csrk_matrix_download(const csrk_matrix *m, uint32_t *row_ptr,
                          uint32_t *ssr_ptr);
 /* add an f32 copy of the values (for CSRK_F32 SpMV) if not present */
 int csrk_matrix_add_f32(csrk_matrix *m);
-/* Tile plan of the streaming kernel: whole groups (SSRs for k=3, SRs for
- * k=2, rows for k=1) are packed into CTA tiles of about tile_nnz nonzeros;
- * cap is the shared-memory stage size in nonzeros.  0 = defaults. */
-int csrk_matrix_set_plan(csrk_matrix *m, int64_t tile_nnz, int64_t cap);
+/* Tile plan of the streaming kernel: contiguous row ranges balanced by
+ * cost = nonzeros + rows (tile_cost per tile), cut only on group boundaries
+ * (SSRs for k=3, SRs for k=2) when every group costs at most tile_cost / 2;
+ * cap = stage capacity in nonzeros (larger tiles run in direct mode);
+ * stages = TMA ring depth per CTA.  0 = defaults. */
+int csrk_matrix_set_plan(csrk_matrix *m, int64_t tile_cost, int64_t cap,
+                         int64_t stages);
+/* out = tile_cost, cap, rcap, stages, n_tiles, group_aligned */
+int csrk_matrix_plan(const csrk_matrix *m, int64_t out[6]);
 
 /* ---- SpMV ------------------------------------------------------------------
  * y = A x on device-resident x / y (already in the permuted index space, as

@@ -45,7 +45,8 @@ _SIGNATURES = {
     "csrk_matrix_shape": ([P, I64P], C.c_int),
     "csrk_matrix_download": ([P, U32P, U32P, F64P, U32P, U32P], C.c_int),
     "csrk_matrix_add_f32": ([P], C.c_int),
-    "csrk_matrix_set_plan": ([P, I64, I64], C.c_int),
+    "csrk_matrix_set_plan": ([P, I64, I64, I64], C.c_int),
+    "csrk_matrix_plan": ([P, I64P], C.c_int),
     "csrk_spmv": ([P, C.c_int, C.c_int, C.c_int, P, P, P], C.c_int),
     "csrk_spmv_host": ([P, C.c_int, C.c_int, C.c_int, P, P], C.c_int),
     "csrk_last_kernel_ms": ([P, C.POINTER(C.c_float)], C.c_int),
@@ -232,8 +233,15 @@ class DeviceMatrix:
     def ensure_f32(self):
         call("csrk_matrix_add_f32", self.ptr)
 
-    def set_plan(self, tile_nnz=0, cap=0):
-        call("csrk_matrix_set_plan", self.ptr, int(tile_nnz), int(cap))
+    def set_plan(self, tile_cost=0, cap=0, stages=0):
+        """Streaming-kernel tile plan (0 = defaults); see include/csrk.h."""
+        call("csrk_matrix_set_plan", self.ptr, int(tile_cost), int(cap), int(stages))
+
+    def plan(self) -> dict:
+        out = np.zeros(6, dtype=np.int64)
+        call("csrk_matrix_plan", self.ptr, i64p(out))
+        keys = ("tile_cost", "cap", "rcap", "stages", "n_tiles", "group_aligned")
+        return {k: int(v) for k, v in zip(keys, out)}
 
     def stats(self):
         out = np.zeros(5, dtype=np.int64)

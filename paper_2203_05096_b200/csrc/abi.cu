@@ -21,7 +21,8 @@ void set_error(const char *fmt, ...) {
 
 int alloc_matrix_arrays(csrk_matrix *m, bool want64, bool want32) {
   const int64_t pn = padded_nnz(m->nnz);
-  CSRK_CUDA_TRY(cudaMalloc(&m->row_ptr, (m->n_rows + 1) * sizeof(uint32_t)));
+  CSRK_CUDA_TRY(cudaMalloc(&m->row_ptr, padded_rows(m->n_rows) * sizeof(uint32_t)));
+  CSRK_CUDA_TRY(cudaMemset(m->row_ptr, 0, padded_rows(m->n_rows) * sizeof(uint32_t)));
   CSRK_CUDA_TRY(cudaMalloc(&m->col_idx, pn * sizeof(uint32_t)));
   CSRK_CUDA_TRY(cudaMemset(m->col_idx, 0, pn * sizeof(uint32_t)));
   if (want64) {
@@ -247,7 +248,7 @@ int csrk_matrix_upload(int device, int64_t n_rows, int64_t n_cols, int64_t nnz,
       return rc;
     }
   }
-  rc = ensure_plan(m, 0, 0, m->stream);
+  rc = ensure_plan(m, 0, 0, 0, m->stream);
   if (rc == CSRK_OK && (e = cudaStreamSynchronize(m->stream)) != cudaSuccess)
     return fail(e);
   if (rc != CSRK_OK) {
@@ -322,13 +323,14 @@ int csrk_matrix_add_f32(csrk_matrix *m) {
   return CSRK_OK;
 }
 
-int csrk_matrix_set_plan(csrk_matrix *m, int64_t tile_nnz, int64_t cap) {
+int csrk_matrix_set_plan(csrk_matrix *m, int64_t tile_cost, int64_t cap,
+                         int64_t stages) {
   if (!m) {
     set_error("null argument");
     return CSRK_EINVAL;
   }
   CSRK_CUDA_TRY(cudaSetDevice(m->device));
-  CSRK_TRY(ensure_plan(m, tile_nnz, cap, m->stream));
+  CSRK_TRY(ensure_plan(m, tile_cost, cap, stages, m->stream));
   CSRK_CUDA_TRY(cudaStreamSynchronize(m->stream));
   return CSRK_OK;
 }
@@ -377,6 +379,20 @@ int csrk_spmv_host(csrk_matrix *m, int value_type, int variant, int nx,
     CSRK_CUDA_TRY(cudaMemcpyAsync(y_host, m->y_stage, m->n_rows * es,
                                   cudaMemcpyDeviceToHost, m->stream));
   CSRK_CUDA_TRY(cudaStreamSynchronize(m->stream));
+  return CSRK_OK;
+}
+
+int csrk_matrix_plan(const csrk_matrix *m, int64_t out[6]) {
+  if (!m || !out) {
+    set_error("null argument");
+    return CSRK_EINVAL;
+  }
+  out[0] = m->plan.tile_cost;
+  out[1] = m->plan.cap;
+  out[2] = m->plan.rcap;
+  out[3] = m->plan.stages;
+  out[4] = m->plan.n_tiles;
+  out[5] = m->plan.group_aligned ? 1 : 0;
   return CSRK_OK;
 }
 

@@ -582,7 +582,7 @@ int pack_device(int device, int64_t n, int64_t nnz, const uint32_t *row_ptr_h,
     gsz.p = nullptr;
     gptr.p = nullptr;
   }
-  rc = ensure_plan(m, 0, 0, s);
+  rc = ensure_plan(m, 0, 0, 0, s);
   if (rc != CSRK_OK) return bail(rc);
   PACK_CUDA(cudaStreamSynchronize(s));
 #undef PACK_CUDA
@@ -704,7 +704,7 @@ int stencil_device(int device, int64_t nz, int64_t ny, int64_t nx, int points,
         st, nz, ny, nx, ptr.p, m->row_ptr, m->col_idx, m->vals64);
     if (cudaGetLastError() != cudaSuccess) rc = CSRK_ECUDA;
   }
-  if (rc == CSRK_OK) rc = ensure_plan(m, 0, 0, m->stream);
+  if (rc == CSRK_OK) rc = ensure_plan(m, 0, 0, 0, m->stream);
   if (rc == CSRK_OK && cudaStreamSynchronize(m->stream) != cudaSuccess) {
     set_error("stencil generator failed");
     rc = CSRK_ECUDA;

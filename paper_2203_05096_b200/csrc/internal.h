@@ -16,10 +16,16 @@ void set_error(const char *fmt, ...);
 
 // A tile plan of the streaming kernel: tile t covers rows
 // [tile_row[t], tile_row[t+1]) made of whole groups.
+constexpr int64_t kDefaultTileCost = 2048;  // nonzeros + rows per tile
+constexpr int64_t kDefaultStages = 3;       // TMA ring depth per CTA
+
 struct TilePlan {
-  int64_t tile_nnz = 0;  // requested nonzeros per tile
-  int64_t cap = 0;       // shared-memory stage, nonzeros
+  int64_t tile_cost = 0;  // requested nonzeros + rows per tile
+  int64_t cap = 0;        // stage capacity, nonzeros
+  int64_t rcap = 0;       // stage capacity, rows
+  int64_t stages = 0;     // ring depth
   int64_t n_tiles = 0;
+  bool group_aligned = false;    // tile cuts only on SSR / SR boundaries
   uint32_t *tile_row = nullptr;  // device, n_tiles + 1
 };
 
@@ -30,13 +36,14 @@ struct csrk_matrix {
   int64_t n_rows = 0, n_cols = 0, nnz = 0;
   int k = 1;
   int64_t n_sr = 0, n_ssr = 0;
-  uint32_t *row_ptr = nullptr;  // n_rows + 1
+  uint32_t *row_ptr = nullptr;  // n_rows + 1, padded (padded_rows)
   uint32_t *col_idx = nullptr;  // nnz, padded to a multiple of 4 (+4)
   double *vals64 = nullptr;     // nnz, padded
   float *vals32 = nullptr;      // optional
   uint32_t *sr_ptr = nullptr;   // n_sr + 1 (k >= 2)
   uint32_t *ssr_ptr = nullptr;  // n_ssr + 1 (k == 3)
   csrk::TilePlan plan;          // current streaming plan
+  int sm_count = 0;
   // host-API staging
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -49,9 +56,11 @@ namespace csrk {
 // padded element count for col_idx / vals allocations: room for the 16-byte
 // aligned over-read of the TMA bulk copies at both ends of a span.
 inline int64_t padded_nnz(int64_t nnz) { return ((nnz + 3) / 4) * 4 + 8; }
+inline int64_t padded_rows(int64_t n_rows) { return ((n_rows + 1 + 3) / 4) * 4 + 8; }
 
 int alloc_matrix_arrays(csrk_matrix *m, bool want64, bool want32);
-int ensure_plan(csrk_matrix *m, int64_t tile_nnz, int64_t cap, cudaStream_t s);
+int ensure_plan(csrk_matrix *m, int64_t tile_cost, int64_t cap, int64_t stages,
+                cudaStream_t s);
 int launch_spmv(const csrk_matrix *m, int value_type, int variant, int nx,
                 const void *x, void *y, cudaStream_t stream);
 int launch_listing3(const csrk_matrix *m, int dx, int dy, const double *x,

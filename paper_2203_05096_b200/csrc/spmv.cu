@@ -1,26 +1,29 @@
-// CSR-k SpMV kernels for sm_100a.
+// CSR-k streaming SpMV for sm_100a -- the hot path.
 //
 // Bitwise contract: every reference kernel sums a row
 // strictly left to right with the multiply and the add rounded separately
-// (reference kernels.py:117-147, 224-228), so the products and sums below use
-// __dmul_rn / __dadd_rn, which the compiler never contracts into DFMA.  The
-// STRIDED order reproduces emulate_gpu_spmv35 (kernels.py:284-324): nonzero p
-// of a row feeds lane p mod nx, each lane sums serially from 0.0, and the
-// lanes are combined by the zero-padded halving tree of _tree_reduce
+// (reference kernels.py:117-147, 224-228), so products and sums use
+// __dmul_rn / __dadd_rn, which are never contracted into DFMA.  The STRIDED
+// order reproduces emulate_gpu_spmv35 (kernels.py:284-324): nonzero p of a
+// row feeds lane p mod nx, each lane sums serially from 0.0, and the lanes
+// are combined by the zero-padded halving tree of _tree_reduce
 // (kernels.py:268-281), here a __shfl_down_sync tree.
 //
-// The streaming kernel (csrk_stream_kernel) is the B200 hot path:
-//   * one CTA per tile; a tile is a run of whole super-super-rows (k=3),
-//     super-rows (k=2) or rows (k=1) holding about `tile_nnz` nonzeros
-//     (the paper's block <-> SSR mapping, Listing 3, coarsened so a
-//     CTA moves enough bytes to keep HBM3e busy);
-//   * the tile's contiguous vals / col_idx span is moved HBM -> shared memory
-//     by one TMA bulk copy each (cp.async.bulk + mbarrier complete_tx) with an
-//     L2 evict-first policy, so the streamed matrix does not push x out of L2;
-//   * rows go to threads (SERIAL) or to nx-lane sub-warps (STRIDED); x is
-//     gathered through the read-only path; y is stored coalesced.
-// Tiles larger than the stage are walked in row-aligned chunks; a single row
-// larger than the stage is summed straight from global memory by one warp.
+// Design (B200):
+//   * tiles: contiguous row ranges balanced by cost = nonzeros + rows (merge
+//     path).  When every group (super-super-row for k=3, super-row for k=2)
+//     is small against the tile, tile cuts fall only on group boundaries, so
+//     a CTA always owns whole super-super-rows (the paper's block <-> SSR
+//     mapping, Listing 3, coarsened to a B200-sized unit of work);
+//   * persistent, warp-specialised CTAs: warp 0 is the producer and moves
+//     each tile's vals / col_idx / row_ptr spans HBM -> shared memory with
+//     TMA bulk copies (cp.async.bulk + mbarrier complete_tx, L2 evict-first
+//     so the streamed matrix does not push x out of L2) into an S-stage ring;
+//     warps 1..8 consume: rows to threads (SERIAL) or to nx-lane sub-warps
+//     (STRIDED), x gathered through the read-only path, y stored coalesced,
+//     and release the stage through an `empty` mbarrier;
+//   * a tile that does not fit a stage (a very long row) is computed from
+//     global memory by the consumers ("direct" mode).
 
 #include <cstdint>
 
@@ -29,7 +32,10 @@
 namespace csrk {
 namespace {
 
-constexpr int kThreads = 256;
+constexpr int kConsumerWarps = 8;
+constexpr int kConsumers = 32 * kConsumerWarps;
+constexpr int kThreads = kConsumers + 32;
+constexpr uint32_t kStaged = 0, kDirect = 1;
 
 __device__ __forceinline__ uint32_t smem_addr(const void *p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -39,7 +45,10 @@ __device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)),
                "r"(count)
                : "memory");
-  // make the initialised barrier visible to the async (TMA) proxy
+}
+
+__device__ __forceinline__ void fence_barrier_init() {
+  // make initialised barriers visible to the async (TMA) proxy
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
@@ -50,6 +59,11 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar,
           smem_addr(bar)),
       "r"(bytes)
       : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar))
+               : "memory");
 }
 
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
@@ -108,36 +122,71 @@ __host__ __device__ constexpr int pow2_ceil(int v) {
   return p;
 }
 
-// Serial left-to-right sum of one row from (possibly shared) arrays.
-// `vb` / `cb` are the element offsets of the staged spans.
+__host__ __device__ constexpr uint32_t round_up(uint32_t v, uint32_t a) {
+  return (v + a - 1) / a * a;
+}
+
+// Shared-memory geometry of one pipeline stage (host and device agree).
+struct Geometry {
+  uint32_t cap, rcap, stages;
+  uint32_t v_elems, c_elems, r_elems;  // allocated elements per stage
+  uint32_t v_off, c_off, r_off, stage_bytes, header_bytes;
+
+  __host__ __device__ Geometry(uint32_t cap_, uint32_t rcap_, uint32_t stages_,
+                               uint32_t vsize)
+      : cap(cap_), rcap(rcap_), stages(stages_) {
+    v_elems = cap + 8;       // alignment slack at both ends
+    c_elems = cap + 8;
+    r_elems = rcap + 1 + 8;  // rows + 1 pointers
+    v_off = 0;
+    c_off = round_up(v_elems * vsize, 128);
+    r_off = c_off + round_up(c_elems * 4, 128);
+    stage_bytes = r_off + round_up(r_elems * 4, 128);
+    header_bytes = round_up(stages * (8 + 8 + 32), 128);
+  }
+  __host__ __device__ uint32_t total_bytes() const {
+    return header_bytes + stages * stage_bytes;
+  }
+};
+
+struct StageMeta {
+  uint32_t r0, r1;  // row range of the tile
+  uint32_t va0;     // first staged vals element (16-byte aligned)
+  uint32_t ca0;     // first staged col_idx element
+  uint32_t ra0;     // first staged row_ptr element
+  uint32_t mode;    // kStaged or kDirect
+  uint32_t pad0, pad1;
+};
+
+// ---- per-row arithmetic ---------------------------------------------------
+
+// serial left-to-right row sum; all gathers of an 8-wide batch are issued
+// before its ordered adds
 template <typename V>
-__device__ __forceinline__ double row_sum_serial(const V *__restrict__ sv,
-                                                 const uint32_t *__restrict__ sc,
-                                                 uint32_t s, uint32_t e,
-                                                 const V *__restrict__ x) {
+__device__ __forceinline__ double row_serial(const V *__restrict__ sv,
+                                             const uint32_t *__restrict__ sc,
+                                             uint32_t s, uint32_t e,
+                                             const V *__restrict__ x) {
   double acc = 0.0;
-  uint32_t p = s;
-  // 8-wide batches: issue the x gathers of a batch before the ordered adds
-  for (; p + 8 <= e; p += 8) {
-    double pv[8];
+  for (uint32_t p = s; p < e; p += 8) {
+    double prod[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j)
-      pv[j] = __dmul_rn(static_cast<double>(sv[p + j]),
-                        Elem<V>::load_x(x, sc[p + j]));
+      if (p + j < e)
+        prod[j] = __dmul_rn(static_cast<double>(sv[p + j]),
+                            Elem<V>::load_x(x, sc[p + j]));
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc = __dadd_rn(acc, pv[j]);
+    for (int j = 0; j < 8; ++j)
+      if (p + j < e) acc = __dadd_rn(acc, prod[j]);
   }
-  for (; p < e; ++p)
-    acc = __dadd_rn(acc, __dmul_rn(static_cast<double>(sv[p]),
-                                   Elem<V>::load_x(x, sc[p])));
   return acc;
 }
 
-// Lane partial of the STRIDED order: lane l sums nonzeros l, l+nx, ...
 template <typename V, int NX>
-__device__ __forceinline__ double row_partial_strided(
-    const V *__restrict__ sv, const uint32_t *__restrict__ sc, uint32_t s,
-    uint32_t e, int lane, const V *__restrict__ x) {
+__device__ __forceinline__ double lane_partial(const V *__restrict__ sv,
+                                               const uint32_t *__restrict__ sc,
+                                               uint32_t s, uint32_t e, int lane,
+                                               const V *__restrict__ x) {
   double acc = 0.0;
   if (lane < NX) {
     for (uint32_t p = s + lane; p < e; p += NX)
@@ -157,35 +206,62 @@ __device__ __forceinline__ double subwarp_tree(double acc) {
   return acc;
 }
 
-// A row longer than the shared stage: summed from global memory by warp 0.
-template <typename V, int NX>
-__device__ void long_row(const uint32_t *__restrict__ row_ptr,
-                         const uint32_t *__restrict__ col_idx,
-                         const V *__restrict__ vals, const V *__restrict__ x,
-                         V *__restrict__ y, uint32_t r) {
-  const int tid = threadIdx.x;
-  if (tid >= 32) return;
-  const uint32_t s = row_ptr[r], e = row_ptr[r + 1];
+// rows [r0, r1) with staged (or global) arrays; `srp(r)` yields row_ptr[r]
+template <typename V, int NX, typename RowPtr>
+__device__ __forceinline__ void compute_rows(uint32_t r0, uint32_t r1,
+                                             const V *__restrict__ sv,
+                                             const uint32_t *__restrict__ sc,
+                                             RowPtr srp, const V *__restrict__ x,
+                                             V *__restrict__ y, int ct) {
   if constexpr (NX == 0) {
-    // products in parallel, the ordered sum broadcast through shuffles
-    double acc = 0.0;
-    for (uint32_t p0 = s; p0 < e; p0 += 32) {
-      const uint32_t p = p0 + tid;
-      double prod = 0.0;
-      if (p < e)
-        prod = __dmul_rn(static_cast<double>(vals[p]),
-                         Elem<V>::load_x(x, col_idx[p]));
-      const uint32_t cnt = (e - p0) < 32u ? (e - p0) : 32u;
-      for (uint32_t j = 0; j < cnt; ++j)
-        acc = __dadd_rn(acc, __shfl_sync(0xffffffffu, prod, j));
-    }
-    if (tid == 0) y[r] = Elem<V>::out(acc);
+    for (uint32_t r = r0 + ct; r < r1; r += kConsumers)
+      y[r] = Elem<V>::out(row_serial<V>(sv, sc, srp(r), srp(r + 1), x));
   } else {
     constexpr int P = pow2_ceil(NX);
-    double acc = 0.0;
-    if (tid < P) acc = row_partial_strided<V, NX>(vals, col_idx, s, e, tid, x);
-    acc = subwarp_tree<P>(acc);
-    if (tid == 0) y[r] = Elem<V>::out(acc);
+    constexpr int kSubPerWarp = 32 / P;
+    constexpr int kSubs = kConsumers / P;
+    const int lane = ct % P;
+    const int sub = ct / P;
+    const int warp_first = (ct / 32) * kSubPerWarp;
+    for (uint32_t base = r0 + warp_first; base < r1; base += kSubs) {
+      const uint32_t r = base + (sub - warp_first);
+      double acc = 0.0;
+      if (r < r1) acc = lane_partial<V, NX>(sv, sc, srp(r), srp(r + 1), lane, x);
+      acc = subwarp_tree<P>(acc);
+      if (r < r1 && lane == 0) y[r] = Elem<V>::out(acc);
+    }
+  }
+}
+
+// a tile whose rows do not fit a stage: SERIAL rows are summed by whole
+// warps (products in parallel, ordered adds through shuffles)
+template <typename V, int NX>
+__device__ void compute_direct(uint32_t r0, uint32_t r1,
+                               const uint32_t *__restrict__ row_ptr,
+                               const uint32_t *__restrict__ col_idx,
+                               const V *__restrict__ vals,
+                               const V *__restrict__ x, V *__restrict__ y,
+                               int ct) {
+  if constexpr (NX == 0) {
+    const int lane = ct & 31, warp = ct >> 5;
+    for (uint32_t r = r0 + warp; r < r1; r += kConsumerWarps) {
+      const uint32_t s = row_ptr[r], e = row_ptr[r + 1];
+      double acc = 0.0;
+      for (uint32_t p0 = s; p0 < e; p0 += 32) {
+        const uint32_t p = p0 + lane;
+        double prod = 0.0;
+        if (p < e)
+          prod = __dmul_rn(static_cast<double>(vals[p]),
+                           Elem<V>::load_x(x, col_idx[p]));
+        const uint32_t cnt = (e - p0) < 32u ? (e - p0) : 32u;
+        for (uint32_t j = 0; j < cnt; ++j)
+          acc = __dadd_rn(acc, __shfl_sync(0xffffffffu, prod, j));
+      }
+      if (lane == 0) y[r] = Elem<V>::out(acc);
+    }
+  } else {
+    compute_rows<V, NX>(r0, r1, vals, col_idx,
+                        [&](uint32_t r) { return row_ptr[r]; }, x, y, ct);
   }
 }
 
@@ -195,244 +271,169 @@ __global__ void __launch_bounds__(kThreads)
                        const uint32_t *__restrict__ col_idx,
                        const V *__restrict__ vals, const V *__restrict__ x,
                        V *__restrict__ y, const uint32_t *__restrict__ tile_row,
-                       uint32_t cap) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  uint64_t *bar = reinterpret_cast<uint64_t *>(smem);
-  V *sv = reinterpret_cast<V *>(smem + 16);
-  uint32_t *sc = reinterpret_cast<uint32_t *>(
-      smem + 16 + ((static_cast<size_t>(cap) + 8) * sizeof(V) + 15) / 16 * 16);
+                       uint32_t n_tiles, uint32_t cap, uint32_t rcap,
+                       uint32_t stages) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const Geometry geo(cap, rcap, stages, sizeof(V));
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem);
+  uint64_t *empty = full + stages;
+  StageMeta *meta = reinterpret_cast<StageMeta *>(empty + stages);
+  unsigned char *stage0 = smem + geo.header_bytes;
 
-  constexpr uint32_t VPV = Elem<V>::kPerVec;
   const int tid = threadIdx.x;
-  const uint32_t r0 = tile_row[blockIdx.x];
-  const uint32_t r1 = tile_row[blockIdx.x + 1];
-  if (tid == 0) mbar_init(bar, 1);
+  if (tid == 0) {
+    for (uint32_t s = 0; s < stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumerWarps);
+    }
+    fence_barrier_init();
+  }
   __syncthreads();
-  const uint64_t policy = evict_first_policy();
 
-  uint32_t phase = 0;
-  uint32_t ra = r0;
-  while (ra < r1) {
-    const uint32_t pa = row_ptr[ra];
-    uint32_t rb = r1;
-    if (row_ptr[r1] - pa > cap) {
-      // largest rb in [ra, r1) with row_ptr[rb] - pa <= cap
-      uint32_t lo = ra, hi = r1;
-      while (hi - lo > 1) {
-        const uint32_t mid = lo + (hi - lo) / 2;
-        if (row_ptr[mid] - pa <= cap)
-          lo = mid;
-        else
-          hi = mid;
+  const uint32_t grid = gridDim.x;
+  if (tid < 32) {
+    // ---------------- producer warp ----------------
+    if (tid != 0) return;
+    constexpr uint32_t VPV = Elem<V>::kPerVec;
+    const uint64_t policy = evict_first_policy();
+    uint32_t i = 0;
+    for (uint32_t t = blockIdx.x; t < n_tiles; t += grid, ++i) {
+      const uint32_t s = i % stages;
+      const uint32_t r0 = tile_row[t], r1 = tile_row[t + 1];
+      const uint32_t p0 = row_ptr[r0], p1 = row_ptr[r1];
+      if (i >= stages) mbar_wait(&empty[s], ((i / stages) + 1) & 1);
+      StageMeta &md = meta[s];
+      md.r0 = r0;
+      md.r1 = r1;
+      if (p1 - p0 <= cap && r1 - r0 <= rcap) {
+        unsigned char *st = stage0 + s * geo.stage_bytes;
+        const uint32_t va0 = p0 & ~(VPV - 1), va1 = round_up(p1, VPV);
+        const uint32_t ca0 = p0 & ~3u, ca1 = round_up(p1, 4);
+        const uint32_t ra0 = r0 & ~3u, ra1 = round_up(r1 + 1, 4);
+        const uint32_t vb = (va1 - va0) * static_cast<uint32_t>(sizeof(V));
+        const uint32_t cb = (ca1 - ca0) * 4u, rb = (ra1 - ra0) * 4u;
+        md.va0 = va0;
+        md.ca0 = ca0;
+        md.ra0 = ra0;
+        md.mode = kStaged;
+        mbar_arrive_expect_tx(&full[s], vb + cb + rb);
+        if (vb) tma_bulk_load(st + geo.v_off, vals + va0, vb, &full[s], policy);
+        if (cb) tma_bulk_load(st + geo.c_off, col_idx + ca0, cb, &full[s], policy);
+        tma_bulk_load(st + geo.r_off, row_ptr + ra0, rb, &full[s], policy);
+      } else {
+        md.mode = kDirect;
+        mbar_arrive(&full[s]);
       }
-      rb = lo;
     }
-    if (rb == ra) {  // one row longer than the stage
-      long_row<V, NX>(row_ptr, col_idx, vals, x, y, ra);
-      ra += 1;
-      continue;
-    }
-    const uint32_t pb = row_ptr[rb];
-    const uint32_t va0 = pa & ~(VPV - 1), va1 = (pb + VPV - 1) & ~(VPV - 1);
-    const uint32_t ca0 = pa & ~3u, ca1 = (pb + 3u) & ~3u;
-    const bool staged = pb > pa;
-    if (staged && tid == 0) {
-      const uint32_t vbytes = (va1 - va0) * static_cast<uint32_t>(sizeof(V));
-      const uint32_t cbytes = (ca1 - ca0) * 4u;
-      mbar_arrive_expect_tx(bar, vbytes + cbytes);
-      tma_bulk_load(sv, vals + va0, vbytes, bar, policy);
-      tma_bulk_load(sc, col_idx + ca0, cbytes, bar, policy);
-    }
-    // shift so that sv_[p] / sc_[p] address global nonzero p
-    const V *sv_ = sv - va0;
-    const uint32_t *sc_ = sc - ca0;
+    return;
+  }
 
-    if constexpr (NX == 0) {
-      // row pointers of this thread's first row load while the copy runs
-      uint32_t r = ra + tid;
-      uint32_t s = 0, e = 0;
-      if (r < rb) {
-        s = row_ptr[r];
-        e = row_ptr[r + 1];
-      }
-      if (staged) mbar_wait(bar, phase);
-      for (; r < rb; r += kThreads) {
-        if (r != ra + tid) {
-          s = row_ptr[r];
-          e = row_ptr[r + 1];
-        }
-        y[r] = Elem<V>::out(row_sum_serial<V>(sv_, sc_, s, e, x));
-      }
+  // ---------------- consumer warps ----------------
+  const int ct = tid - 32;
+  uint32_t i = 0;
+  for (uint32_t t = blockIdx.x; t < n_tiles; t += grid, ++i) {
+    const uint32_t s = i % stages;
+    mbar_wait(&full[s], (i / stages) & 1);
+    const StageMeta md = meta[s];
+    if (md.mode == kStaged) {
+      const unsigned char *st = stage0 + s * geo.stage_bytes;
+      const V *sv = reinterpret_cast<const V *>(st + geo.v_off) - md.va0;
+      const uint32_t *sc = reinterpret_cast<const uint32_t *>(st + geo.c_off) - md.ca0;
+      const uint32_t *sr = reinterpret_cast<const uint32_t *>(st + geo.r_off) - md.ra0;
+      compute_rows<V, NX>(md.r0, md.r1, sv, sc, [&](uint32_t r) { return sr[r]; },
+                          x, y, ct);
     } else {
-      constexpr int P = pow2_ceil(NX);
-      constexpr int kSubPerWarp = 32 / P;
-      constexpr int kSubPerCta = kThreads / P;
-      const int lane = tid % P;
-      const int sub = tid / P;
-      const int warp_first = (tid / 32) * kSubPerWarp;
-      if (staged) mbar_wait(bar, phase);
-      for (uint32_t base = ra + warp_first; base < rb; base += kSubPerCta) {
-        const uint32_t r = base + (sub - warp_first);
-        double acc = 0.0;
-        if (r < rb)
-          acc = row_partial_strided<V, NX>(sv_, sc_, row_ptr[r], row_ptr[r + 1],
-                                           lane, x);
-        acc = subwarp_tree<P>(acc);
-        if (r < rb && lane == 0) y[r] = Elem<V>::out(acc);
-      }
+      compute_direct<V, NX>(md.r0, md.r1, row_ptr, col_idx, vals, x, y, ct);
     }
-    if (staged) phase ^= 1u;
-    __syncthreads();  // stage is rewritten by the next chunk
-    ra = rb;
+    __syncwarp();
+    if ((ct & 31) == 0) mbar_arrive(&empty[s]);
   }
 }
 
-// tile_row[t] = first row of group t*Q (k=3: SSR, k=2: SR, k=1: row)
-__global__ void build_tiles_kernel(const uint32_t *__restrict__ sr_ptr,
-                                   const uint32_t *__restrict__ ssr_ptr, int k,
-                                   int64_t n_groups, int64_t n_rows, int64_t q,
-                                   int64_t n_tiles, uint32_t *tile_row) {
-  const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+// ---- tile plan -------------------------------------------------------------
+
+__device__ __forceinline__ uint32_t group_start(const uint32_t *sr_ptr,
+                                                const uint32_t *ssr_ptr, int k,
+                                                int64_t g, int64_t n_groups,
+                                                int64_t n_rows) {
+  if (g >= n_groups) return static_cast<uint32_t>(n_rows);
+  if (k == 3) return sr_ptr[ssr_ptr[g]];
+  if (k == 2) return sr_ptr[g];
+  return static_cast<uint32_t>(g);
+}
+
+// largest group cost (nonzeros + rows)
+__global__ void max_group_cost_kernel(const uint32_t *__restrict__ row_ptr,
+                                      const uint32_t *__restrict__ sr_ptr,
+                                      const uint32_t *__restrict__ ssr_ptr,
+                                      int k, int64_t n_groups, int64_t n_rows,
+                                      unsigned long long *out) {
+  unsigned long long mx = 0;
+  for (int64_t g = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; g < n_groups;
+       g += int64_t(gridDim.x) * blockDim.x) {
+    const uint32_t a = group_start(sr_ptr, ssr_ptr, k, g, n_groups, n_rows);
+    const uint32_t b = group_start(sr_ptr, ssr_ptr, k, g + 1, n_groups, n_rows);
+    const unsigned long long c =
+        static_cast<unsigned long long>(row_ptr[b] - row_ptr[a]) + (b - a);
+    mx = c > mx ? c : mx;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long v = __shfl_down_sync(0xffffffffu, mx, o);
+    mx = v > mx ? v : mx;
+  }
+  if ((threadIdx.x & 31) == 0) atomicMax(out, mx);
+}
+
+// tile_row[t] = first cut point (group start, or row when cut_k == 1) whose
+// cost row_ptr[r] + r reaches t * tile_cost
+__global__ void tile_bounds_kernel(const uint32_t *__restrict__ row_ptr,
+                                   const uint32_t *__restrict__ sr_ptr,
+                                   const uint32_t *__restrict__ ssr_ptr,
+                                   int cut_k, int64_t n_groups, int64_t n_rows,
+                                   int64_t tile_cost, int64_t n_tiles,
+                                   uint32_t *__restrict__ tile_row) {
+  const int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   if (t > n_tiles) return;
-  const int64_t g = t * q < n_groups ? t * q : n_groups;
-  uint32_t r;
-  if (g == n_groups)
-    r = static_cast<uint32_t>(n_rows);
-  else if (k == 3)
-    r = sr_ptr[ssr_ptr[g]];
-  else if (k == 2)
-    r = sr_ptr[g];
-  else
-    r = static_cast<uint32_t>(g);
-  tile_row[t] = r;
-}
-
-// ---- literal paper mappings (with trace) -----------------------------------
-
-__device__ __forceinline__ void put_trace(int64_t *trace, int64_t n, uint32_t row,
-                                          int64_t block, int64_t z, int64_t y,
-                                          int64_t xf, int64_t xc, int64_t depth) {
-  trace[0 * n + row] = row;
-  trace[1 * n + row] = block;
-  trace[2 * n + row] = z;
-  trace[3 * n + row] = y;
-  trace[4 * n + row] = xf;
-  trace[5 * n + row] = xc;
-  trace[6 * n + row] = depth;
-}
-
-// PAPER Listing 3 / emulate_gpu_spmv3 (kernels.py:231-261): block = SSR,
-// threadIdx.y strides super-rows, threadIdx.x strides rows, serial rows.
-__global__ void listing3_kernel(const uint32_t *__restrict__ row_ptr,
-                                const uint32_t *__restrict__ col_idx,
-                                const double *__restrict__ vals,
-                                const uint32_t *__restrict__ sr_ptr,
-                                const uint32_t *__restrict__ ssr_ptr,
-                                const double *__restrict__ x,
-                                double *__restrict__ y, int64_t *trace,
-                                int64_t n) {
-  const int64_t b = blockIdx.x;
-  const uint32_t s0 = ssr_ptr[b], s1 = ssr_ptr[b + 1];
-  for (uint32_t sr = s0 + threadIdx.y; sr < s1; sr += blockDim.y) {
-    const uint32_t q0 = sr_ptr[sr], q1 = sr_ptr[sr + 1];
-    for (uint32_t row = q0 + threadIdx.x; row < q1; row += blockDim.x) {
-      double acc = 0.0;
-      for (uint32_t p = row_ptr[row]; p < row_ptr[row + 1]; ++p)
-        acc = __dadd_rn(acc, __dmul_rn(vals[p], __ldg(x + col_idx[p])));
-      y[row] = acc;
-      if (trace) put_trace(trace, n, row, b, 0, threadIdx.y, threadIdx.x, 1, 0);
-    }
+  if (t == n_tiles) {
+    tile_row[t] = static_cast<uint32_t>(n_rows);
+    return;
   }
-}
-
-// PAPER Listing 4 / emulate_gpu_spmv35 (kernels.py:284-324): block = SSR,
-// z strides super-rows, y strides rows, x strides the nonzeros of a row into
-// temp[x]; the x lanes are combined by the halving tree in shared memory.
-// Loop trip counts are made block-uniform so every __syncthreads is reached
-// by all threads.
-__global__ void listing4_kernel(const uint32_t *__restrict__ row_ptr,
-                                const uint32_t *__restrict__ col_idx,
-                                const double *__restrict__ vals,
-                                const uint32_t *__restrict__ sr_ptr,
-                                const uint32_t *__restrict__ ssr_ptr,
-                                const double *__restrict__ x,
-                                double *__restrict__ y, int64_t *trace,
-                                int64_t n, int pw, int depth) {
-  extern __shared__ double temp[];  // [dz][dy][pw]
-  __shared__ uint32_t max_rows;
-  const int dx = blockDim.x, dy = blockDim.y, dz = blockDim.z;
-  const int tx = threadIdx.x, ty = threadIdx.y, tz = threadIdx.z;
-  const int flat = (tz * dy + ty) * dx + tx;
-  const int nthreads = dx * dy * dz;
-  const int64_t b = blockIdx.x;
-  const uint32_t s0 = ssr_ptr[b], s1 = ssr_ptr[b + 1];
-  // zero the padding lanes [dx, pw) once; the tree never writes them
-  for (int i = flat; i < dz * dy * pw; i += nthreads) temp[i] = 0.0;
-  if (flat == 0) max_rows = 0;
-  __syncthreads();
-  uint32_t local_max = 0;
-  for (uint32_t sr = s0 + flat; sr < s1; sr += nthreads) {
-    const uint32_t len = sr_ptr[sr + 1] - sr_ptr[sr];
-    local_max = len > local_max ? len : local_max;
+  const int64_t target = t * tile_cost;
+  int64_t lo = 0, hi = n_groups;  // answer in [0, n_groups]
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) / 2;
+    const uint32_t r = group_start(sr_ptr, ssr_ptr, cut_k, mid, n_groups, n_rows);
+    if (static_cast<int64_t>(row_ptr[r]) + r >= target)
+      hi = mid;
+    else
+      lo = mid + 1;
   }
-  atomicMax(&max_rows, local_max);
-  __syncthreads();
-  const uint32_t iters_z = (s1 - s0 + dz - 1) / dz;
-  const uint32_t iters_y = (max_rows + dy - 1) / dy;
-  double *slot = temp + (tz * dy + ty) * pw;
-  for (uint32_t iz = 0; iz < iters_z; ++iz) {
-    const uint32_t sr = s0 + tz + iz * dz;
-    const bool vz = sr < s1;
-    const uint32_t q0 = vz ? sr_ptr[sr] : 0, q1 = vz ? sr_ptr[sr + 1] : 0;
-    for (uint32_t iy = 0; iy < iters_y; ++iy) {
-      const uint32_t row = q0 + ty + iy * dy;
-      const bool valid = vz && row < q1;
-      double part = 0.0;
-      if (valid) {
-        const uint32_t pe = row_ptr[row + 1];
-        for (uint32_t p = row_ptr[row] + tx; p < pe; p += dx)
-          part = __dadd_rn(part, __dmul_rn(vals[p], __ldg(x + col_idx[p])));
-      }
-      slot[tx] = part;
-      __syncthreads();
-      for (int stride = pw / 2; stride >= 1; stride >>= 1) {
-        if (tx < stride) slot[tx] = __dadd_rn(slot[tx], slot[tx + stride]);
-        __syncthreads();
-      }
-      if (valid && tx == 0) {
-        y[row] = slot[0];
-        if (trace)
-          put_trace(trace, n, row, b, (sr - s0) % dz, (row - q0) % dy, 0, dx,
-                    depth);
-      }
-      __syncthreads();
-    }
-  }
-}
-
-__global__ void f64_to_f32_kernel(const double *__restrict__ in,
-                                  float *__restrict__ out, int64_t n) {
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-       i < n; i += static_cast<int64_t>(gridDim.x) * blockDim.x)
-    out[i] = __double2float_rn(in[i]);
-}
-
-template <typename V>
-size_t stage_bytes(uint32_t cap) {
-  return 16 + ((static_cast<size_t>(cap) + 8) * sizeof(V) + 15) / 16 * 16 +
-         (static_cast<size_t>(cap) + 8) * 4;
+  tile_row[t] = group_start(sr_ptr, ssr_ptr, cut_k, lo, n_groups, n_rows);
 }
 
 template <typename V, int NX>
 int launch_stream(const csrk_matrix *m, const V *vals, const V *x, V *y,
                   cudaStream_t stream) {
-  const uint32_t cap = static_cast<uint32_t>(m->plan.cap);
-  const size_t smem = stage_bytes<V>(cap);
+  const TilePlan &pl = m->plan;
+  const Geometry geo(static_cast<uint32_t>(pl.cap), static_cast<uint32_t>(pl.rcap),
+                     static_cast<uint32_t>(pl.stages), sizeof(V));
+  const size_t smem = geo.total_bytes();
   auto kern = csrk_stream_kernel<V, NX>;
   CSRK_CUDA_TRY(cudaFuncSetAttribute(
       kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  kern<<<static_cast<unsigned>(m->plan.n_tiles), kThreads, smem, stream>>>(
-      m->row_ptr, m->col_idx, vals, x, y, m->plan.tile_row, cap);
+  int per_sm = 0;
+  CSRK_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads,
+                                                              smem));
+  if (per_sm < 1) {
+    set_error("stream kernel does not fit on an SM (%zu bytes of shared memory)", smem);
+    return CSRK_EINVAL;
+  }
+  int64_t grid = static_cast<int64_t>(per_sm) * m->sm_count;
+  if (grid > pl.n_tiles) grid = pl.n_tiles;
+  if (grid < 1) return CSRK_OK;
+  kern<<<static_cast<unsigned>(grid), kThreads, smem, stream>>>(
+      m->row_ptr, m->col_idx, vals, x, y, pl.tile_row,
+      static_cast<uint32_t>(pl.n_tiles), geo.cap, geo.rcap, geo.stages);
   CSRK_CUDA_TRY(cudaGetLastError());
   return CSRK_OK;
 }
@@ -476,25 +477,55 @@ int dispatch_nx(const csrk_matrix *m, int variant, int nx, const V *vals,
 
 }  // namespace
 
-bool strided_nx_supported(int nx) {
-  return (nx >= 1 && nx <= 16) || nx == 20 || nx == 24 || nx == 28 || nx == 32;
-}
-
-int ensure_plan(csrk_matrix *m, int64_t tile_nnz, int64_t cap, cudaStream_t s) {
-  if (tile_nnz <= 0) tile_nnz = 2048;
-  if (cap <= 0) cap = 4096;
+int ensure_plan(csrk_matrix *m, int64_t tile_cost, int64_t cap, int64_t stages,
+                cudaStream_t s) {
+  if (tile_cost <= 0) tile_cost = kDefaultTileCost;
+  if (tile_cost < 32) tile_cost = 32;
+  if (tile_cost > 65536) tile_cost = 65536;
+  if (cap <= 0) cap = tile_cost + 256;
   if (cap < 16) cap = 16;
-  if (cap > 16384) cap = 16384;
-  if (m->plan.tile_row && m->plan.tile_nnz == tile_nnz && m->plan.cap == cap)
-    return CSRK_OK;
-  int64_t n_groups = m->k == 3 ? m->n_ssr : (m->k == 2 ? m->n_sr : m->n_rows);
-  int64_t q = 1;
-  if (n_groups > 0 && m->nnz > 0) {
-    const double per_group = static_cast<double>(m->nnz) / n_groups;
-    q = static_cast<int64_t>(static_cast<double>(tile_nnz) / per_group + 0.5);
-    if (q < 1) q = 1;
+  if (stages <= 0) stages = kDefaultStages;
+  if (stages > 8) stages = 8;
+  const int64_t rcap = tile_cost;
+  const Geometry geo(static_cast<uint32_t>(cap), static_cast<uint32_t>(rcap),
+                     static_cast<uint32_t>(stages), sizeof(double));
+  if (geo.total_bytes() > 227 * 1024) {
+    set_error("tile plan needs %u bytes of shared memory (> 227 KB)",
+              geo.total_bytes());
+    return CSRK_EINVAL;
   }
-  const int64_t n_tiles = n_groups > 0 ? (n_groups + q - 1) / q : 0;
+  if (m->plan.tile_row && m->plan.tile_cost == tile_cost && m->plan.cap == cap &&
+      m->plan.stages == stages)
+    return CSRK_OK;
+  if (m->sm_count == 0) {
+    int dev = 0;
+    CSRK_CUDA_TRY(cudaGetDevice(&dev));
+    CSRK_CUDA_TRY(cudaDeviceGetAttribute(&m->sm_count, cudaDevAttrMultiProcessorCount,
+                                         dev));
+  }
+  const int64_t n_groups = m->k == 3 ? m->n_ssr : (m->k == 2 ? m->n_sr : m->n_rows);
+  // cut on group boundaries when every group is small against a tile
+  int cut_k = 1;
+  int64_t n_cuts = m->n_rows;
+  if (m->k >= 2 && n_groups > 0) {
+    unsigned long long *d = nullptr, h = 0;
+    CSRK_CUDA_TRY(cudaMallocAsync(&d, sizeof(h), s));
+    CSRK_CUDA_TRY(cudaMemsetAsync(d, 0, sizeof(h), s));
+    int64_t blocks = (n_groups + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    max_group_cost_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(
+        m->row_ptr, m->sr_ptr, m->ssr_ptr, m->k, n_groups, m->n_rows, d);
+    CSRK_CUDA_TRY(cudaGetLastError());
+    CSRK_CUDA_TRY(cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, s));
+    CSRK_CUDA_TRY(cudaStreamSynchronize(s));
+    cudaFreeAsync(d, s);
+    if (static_cast<int64_t>(h) * 2 <= tile_cost) {
+      cut_k = m->k;
+      n_cuts = n_groups;
+    }
+  }
+  const int64_t total_cost = m->nnz + m->n_rows;
+  const int64_t n_tiles = (total_cost + tile_cost - 1) / tile_cost;
   if (n_tiles > 0x7fffffffLL) {
     set_error("too many tiles (%lld)", static_cast<long long>(n_tiles));
     return CSRK_EINVAL;
@@ -504,15 +535,17 @@ int ensure_plan(csrk_matrix *m, int64_t tile_nnz, int64_t cap, cudaStream_t s) {
     m->plan.tile_row = nullptr;
   }
   CSRK_CUDA_TRY(cudaMalloc(&m->plan.tile_row, (n_tiles + 1) * sizeof(uint32_t)));
-  const int threads = 256;
-  const int64_t blocks = (n_tiles + 1 + threads - 1) / threads;
-  build_tiles_kernel<<<static_cast<unsigned>(blocks), threads, 0, s>>>(
-      m->sr_ptr, m->ssr_ptr, m->k, n_groups, m->n_rows, q, n_tiles,
-      m->plan.tile_row);
+  const int64_t blocks = (n_tiles + 1 + 255) / 256;
+  tile_bounds_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(
+      m->row_ptr, m->sr_ptr, m->ssr_ptr, cut_k, n_cuts, m->n_rows, tile_cost,
+      n_tiles, m->plan.tile_row);
   CSRK_CUDA_TRY(cudaGetLastError());
-  m->plan.tile_nnz = tile_nnz;
+  m->plan.tile_cost = tile_cost;
   m->plan.cap = cap;
+  m->plan.rcap = rcap;
+  m->plan.stages = stages;
   m->plan.n_tiles = n_tiles;
+  m->plan.group_aligned = cut_k != 1 || m->k == 1;
   return CSRK_OK;
 }
 
@@ -547,47 +580,6 @@ int launch_spmv(const csrk_matrix *m, int value_type, int variant, int nx,
   }
   set_error("unknown value type %d", value_type);
   return CSRK_EINVAL;
-}
-
-int launch_listing3(const csrk_matrix *m, int dx, int dy, const double *x,
-                    double *y, int64_t *trace, cudaStream_t stream) {
-  if (m->n_ssr == 0) return CSRK_OK;
-  dim3 block(dx, dy, 1);
-  listing3_kernel<<<static_cast<unsigned>(m->n_ssr), block, 0, stream>>>(
-      m->row_ptr, m->col_idx, m->vals64, m->sr_ptr, m->ssr_ptr, x, y, trace,
-      m->n_rows);
-  CSRK_CUDA_TRY(cudaGetLastError());
-  return CSRK_OK;
-}
-
-int launch_listing4(const csrk_matrix *m, int dx, int dy, int dz,
-                    const double *x, double *y, int64_t *trace,
-                    cudaStream_t stream) {
-  if (m->n_ssr == 0) return CSRK_OK;
-  int pw = 1, depth = 0;
-  while (pw < dx) {
-    pw <<= 1;
-    ++depth;
-  }
-  dim3 block(dx, dy, dz);
-  const size_t smem = static_cast<size_t>(dz) * dy * pw * sizeof(double);
-  if (smem > 48 * 1024) {
-    CSRK_CUDA_TRY(cudaFuncSetAttribute(
-        listing4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-        static_cast<int>(smem)));
-  }
-  listing4_kernel<<<static_cast<unsigned>(m->n_ssr), block, smem, stream>>>(
-      m->row_ptr, m->col_idx, m->vals64, m->sr_ptr, m->ssr_ptr, x, y, trace,
-      m->n_rows, pw, depth);
-  CSRK_CUDA_TRY(cudaGetLastError());
-  return CSRK_OK;
-}
-
-int launch_f64_to_f32(const double *in, float *out, int64_t n, cudaStream_t s) {
-  if (n == 0) return CSRK_OK;
-  f64_to_f32_kernel<<<148 * 8, 256, 0, s>>>(in, out, n);
-  CSRK_CUDA_TRY(cudaGetLastError());
-  return CSRK_OK;
 }
 
 }  // namespace csrk

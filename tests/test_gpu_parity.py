@@ -164,16 +164,18 @@ def test_long_rows_pack_and_spmv(long_len):
                                       O.spmv_strided(rp, ci, va, x, nx), err_msg=str(nx))
 
 
-@pytest.mark.parametrize("tile_nnz,cap", [(16, 16), (64, 40), (100000, 16384), (3, 17)])
-def test_tile_plans_do_not_change_bits(tile_nnz, cap):
-    rng = np.random.default_rng(tile_nnz + cap)
+@pytest.mark.parametrize("tile_cost,cap,stages", [(16, 16, 1), (64, 40, 2), (4096, 4400, 2),
+                                                  (300, 17, 4), (1000, 0, 8), (0, 0, 0)])
+def test_tile_plans_do_not_change_bits(tile_cost, cap, stages):
+    rng = np.random.default_rng(tile_cost + cap + stages)
     n = 20000
     a = random_csr(rng, n, n, 6.0 / n, -1.0, 1.0)
     res = ck.band_k(a, 3, [8, 8])
     m = ck.pack_csrk(a, res.perm, res.level_group_sizes)
     x = rng.uniform(-1.0, 1.0, n)
-    want = ck.spmv_csr3(m, x)
-    m.device().set_plan(tile_nnz, cap)
+    want = O.spmv_grouped(O.csr3_group_rows(m.sr_ptr, m.ssr_ptr), m.base.row_ptr,
+                          m.base.col_idx, m.base.vals, x, 1)
+    m.device().set_plan(tile_cost, cap, stages)
     np.testing.assert_array_equal(ck.spmv_csr3(m, x), want)
     np.testing.assert_array_equal(ck.spmv_gpu35(m, x, ck.BlockDims(4, 8, 12)),
                                   O.spmv_strided(m.base.row_ptr, m.base.col_idx,
@@ -259,3 +261,15 @@ def test_native_library_is_loaded():
     import paper_2203_05096_b200._native as nat
     assert nat._lib is not None or nat.lib() is not None
     assert nat.device_count() >= 1
+
+
+def test_plan_geometry_checks():
+    rng = np.random.default_rng(1)
+    a = random_csr(rng, 500, 500, 0.01)
+    dev = a.device()
+    with pytest.raises(ValueError, match="shared memory"):
+        dev.set_plan(65536, 70000, 8)
+    dev.set_plan(512, 0, 2)
+    plan = dev.plan()
+    assert plan["tile_cost"] == 512 and plan["stages"] == 2
+    assert plan["n_tiles"] == -(-(a.nnz + a.n_rows) // 512)
