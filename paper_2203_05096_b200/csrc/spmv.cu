@@ -160,38 +160,63 @@ struct StageMeta {
 
 // ---- per-row arithmetic ---------------------------------------------------
 
-// serial left-to-right row sum; all gathers of an 8-wide batch are issued
-// before its ordered adds
-template <typename V>
+// Serial left-to-right row sum.  Every batch issues all of its x gathers
+// before the ordered adds: indices past the row end are clamped to the last
+// element (a redundant, L1-resident load) so the loads are unconditional and
+// independent -- predicating them lets the compiler serialise the gathers
+// through one register pair, which left one load in flight per thread.
+template <int B, typename V>
 __device__ __forceinline__ double row_serial(const V *__restrict__ sv,
                                              const uint32_t *__restrict__ sc,
                                              uint32_t s, uint32_t e,
                                              const V *__restrict__ x) {
   double acc = 0.0;
-  for (uint32_t p = s; p < e; p += 8) {
-    double prod[8];
+  if (s == e) return acc;
+  const uint32_t last = e - 1;
+  for (uint32_t p = s; p < e; p += B) {
+    uint32_t c[B];
+    double v[B], xv[B];
 #pragma unroll
-    for (int j = 0; j < 8; ++j)
-      if (p + j < e)
-        prod[j] = __dmul_rn(static_cast<double>(sv[p + j]),
-                            Elem<V>::load_x(x, sc[p + j]));
+    for (int j = 0; j < B; ++j) {
+      const uint32_t q = min(p + j, last);
+      c[j] = sc[q];
+      v[j] = static_cast<double>(sv[q]);
+    }
 #pragma unroll
-    for (int j = 0; j < 8; ++j)
-      if (p + j < e) acc = __dadd_rn(acc, prod[j]);
+    for (int j = 0; j < B; ++j) xv[j] = Elem<V>::load_x(x, c[j]);
+#pragma unroll
+    for (int j = 0; j < B; ++j)
+      if (p + j < e) acc = __dadd_rn(acc, __dmul_rn(v[j], xv[j]));
   }
   return acc;
 }
 
-template <typename V, int NX>
+// Lane partial of the STRIDED order: lane l sums nonzeros l, l+nx, ... in
+// order; batches of B strided elements load before they are added.
+template <int NX, int B, typename V>
 __device__ __forceinline__ double lane_partial(const V *__restrict__ sv,
                                                const uint32_t *__restrict__ sc,
                                                uint32_t s, uint32_t e, int lane,
                                                const V *__restrict__ x) {
   double acc = 0.0;
-  if (lane < NX) {
-    for (uint32_t p = s + lane; p < e; p += NX)
-      acc = __dadd_rn(acc, __dmul_rn(static_cast<double>(sv[p]),
-                                     Elem<V>::load_x(x, sc[p])));
+  if (lane >= NX || s + lane >= e) return acc;
+  const uint32_t first = s + lane;
+  const uint32_t count = (e - first + NX - 1) / NX;  // this lane's elements
+  const uint32_t last = first + (count - 1) * NX;
+  for (uint32_t p = first; p < e; p += B * NX) {
+    uint32_t c[B];
+    double v[B], xv[B];
+#pragma unroll
+    for (int j = 0; j < B; ++j) {
+      const uint32_t q = min(p + j * NX, last);
+      c[j] = sc[q];
+      v[j] = static_cast<double>(sv[q]);
+    }
+#pragma unroll
+    for (int j = 0; j < B; ++j) xv[j] = Elem<V>::load_x(x, c[j]);
+#pragma unroll
+    for (int j = 0; j < B; ++j)
+      if (p + j * NX < e) acc = __dadd_rn(acc, __dmul_rn(v[j], xv[j]));
   }
   return acc;
 }
@@ -215,7 +240,7 @@ __device__ __forceinline__ void compute_rows(uint32_t r0, uint32_t r1,
                                              V *__restrict__ y, int ct) {
   if constexpr (NX == 0) {
     for (uint32_t r = r0 + ct; r < r1; r += kConsumers)
-      y[r] = Elem<V>::out(row_serial<V>(sv, sc, srp(r), srp(r + 1), x));
+      y[r] = Elem<V>::out(row_serial<8, V>(sv, sc, srp(r), srp(r + 1), x));
   } else {
     constexpr int P = pow2_ceil(NX);
     constexpr int kSubPerWarp = 32 / P;
@@ -226,7 +251,7 @@ __device__ __forceinline__ void compute_rows(uint32_t r0, uint32_t r1,
     for (uint32_t base = r0 + warp_first; base < r1; base += kSubs) {
       const uint32_t r = base + (sub - warp_first);
       double acc = 0.0;
-      if (r < r1) acc = lane_partial<V, NX>(sv, sc, srp(r), srp(r + 1), lane, x);
+      if (r < r1) acc = lane_partial<NX, 4, V>(sv, sc, srp(r), srp(r + 1), lane, x);
       acc = subwarp_tree<P>(acc);
       if (r < r1 && lane == 0) y[r] = Elem<V>::out(acc);
     }
@@ -266,7 +291,7 @@ __device__ void compute_direct(uint32_t r0, uint32_t r1,
 }
 
 template <typename V, int NX>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, 2)
     csrk_stream_kernel(const uint32_t *__restrict__ row_ptr,
                        const uint32_t *__restrict__ col_idx,
                        const V *__restrict__ vals, const V *__restrict__ x,
