@@ -57,6 +57,11 @@ static void release(csrk_matrix *m) {
   cudaFree(m->plan.tile_row);
   cudaFree(m->x_stage);
   cudaFree(m->y_stage);
+  for (auto e : m->pipe.ev_x) cudaEventDestroy(e);
+  for (auto e : m->pipe.ev_c) cudaEventDestroy(e);
+  if (m->pipe.h2d) cudaStreamDestroy(m->pipe.h2d);
+  if (m->pipe.comp) cudaStreamDestroy(m->pipe.comp);
+  if (m->pipe.d2h) cudaStreamDestroy(m->pipe.d2h);
   if (m->ev0) cudaEventDestroy(m->ev0);
   if (m->ev1) cudaEventDestroy(m->ev1);
   if (m->stream) cudaStreamDestroy(m->stream);
@@ -346,6 +351,74 @@ int csrk_spmv(const csrk_matrix *m, int value_type, int variant, int nx,
                      static_cast<cudaStream_t>(stream));
 }
 
+// Host-buffer SpMV.  With pinned host x / y and a square matrix the copies
+// and the kernel overlap: x goes up in row-aligned chunks on one stream, the
+// rows of chunk c are computed on a second stream as soon as the x chunks
+// covering their column footprint have landed (Band-k keeps footprints
+// banded), and y chunk c goes down on a third stream -- both PCIe directions
+// busy at once.  Pageable buffers take the plain H2D -> kernel -> D2H path.
+static int ensure_pipe(csrk_matrix *m, int chunks) {
+  auto &pp = m->pipe;
+  if (pp.chunks == chunks && pp.plan_tiles == m->plan.n_tiles) return CSRK_OK;
+  const int64_t nt = m->plan.n_tiles;
+  pp.tile_cut.assign(chunks + 1, 0);
+  pp.row_cut.assign(chunks + 1, 0);
+  std::vector<uint32_t> rc(chunks + 1);
+  for (int c = 0; c <= chunks; ++c) {
+    pp.tile_cut[c] = nt * c / chunks;
+    uint32_t r = 0;
+    CSRK_CUDA_TRY(cudaMemcpy(&r, m->plan.tile_row + pp.tile_cut[c], sizeof(r),
+                             cudaMemcpyDeviceToHost));
+    rc[c] = r;
+    pp.row_cut[c] = r;
+  }
+  uint32_t *d_cut = nullptr, *d_max = nullptr;
+  CSRK_CUDA_TRY(cudaMalloc(&d_cut, (chunks + 1) * sizeof(uint32_t)));
+  CSRK_CUDA_TRY(cudaMalloc(&d_max, chunks * sizeof(uint32_t)));
+  std::vector<uint32_t> mx(chunks);
+  cudaError_t e = cudaMemcpy(d_cut, rc.data(), (chunks + 1) * sizeof(uint32_t),
+                             cudaMemcpyHostToDevice);
+  int rc2 = e == cudaSuccess ? chunk_max_cols(m, d_cut, chunks, d_max, nullptr)
+                             : CSRK_ECUDA;
+  if (rc2 == CSRK_OK)
+    e = cudaMemcpy(mx.data(), d_max, chunks * sizeof(uint32_t), cudaMemcpyDeviceToHost);
+  cudaFree(d_cut);
+  cudaFree(d_max);
+  if (rc2 != CSRK_OK) return rc2;
+  CSRK_CUDA_TRY(e);
+  pp.x_ready.assign(chunks, 0);
+  for (int c = 0; c < chunks; ++c) {
+    int j = 0;
+    while (j + 1 < chunks && pp.row_cut[j + 1] <= static_cast<int64_t>(mx[c])) ++j;
+    pp.x_ready[c] = j;
+  }
+  if (!pp.h2d) {
+    CSRK_CUDA_TRY(cudaStreamCreateWithFlags(&pp.h2d, cudaStreamNonBlocking));
+    CSRK_CUDA_TRY(cudaStreamCreateWithFlags(&pp.comp, cudaStreamNonBlocking));
+    CSRK_CUDA_TRY(cudaStreamCreateWithFlags(&pp.d2h, cudaStreamNonBlocking));
+  }
+  for (auto ev : pp.ev_x) cudaEventDestroy(ev);
+  for (auto ev : pp.ev_c) cudaEventDestroy(ev);
+  pp.ev_x.assign(chunks, nullptr);
+  pp.ev_c.assign(chunks, nullptr);
+  for (int c = 0; c < chunks; ++c) {
+    CSRK_CUDA_TRY(cudaEventCreateWithFlags(&pp.ev_x[c], cudaEventDisableTiming));
+    CSRK_CUDA_TRY(cudaEventCreateWithFlags(&pp.ev_c[c], cudaEventDisableTiming));
+  }
+  pp.chunks = chunks;
+  pp.plan_tiles = nt;
+  return CSRK_OK;
+}
+
+static bool is_pinned(const void *p) {
+  cudaPointerAttributes attr;
+  if (cudaPointerGetAttributes(&attr, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return attr.type == cudaMemoryTypeHost;
+}
+
 int csrk_spmv_host(csrk_matrix *m, int value_type, int variant, int nx,
                    const void *x_host, void *y_host) {
   if (!m || (m->n_rows > 0 && (!x_host || !y_host))) {
@@ -367,6 +440,41 @@ int csrk_spmv_host(csrk_matrix *m, int value_type, int variant, int nx,
     m->y_stage = nullptr;
     CSRK_CUDA_TRY(cudaMalloc(&m->y_stage, yb));
     m->y_stage_bytes = yb;
+  }
+  const int chunks = 16;
+  const bool pipelined = m->n_rows == m->n_cols && m->n_rows >= (1 << 20) &&
+                         m->plan.n_tiles >= 4 * chunks && is_pinned(x_host) &&
+                         is_pinned(y_host);
+  if (pipelined) {
+    CSRK_TRY(ensure_pipe(m, chunks));
+    auto &pp = m->pipe;
+    char *xs = static_cast<char *>(m->x_stage);
+    char *ys = static_cast<char *>(m->y_stage);
+    const char *xh = static_cast<const char *>(x_host);
+    char *yh = static_cast<char *>(y_host);
+    for (int c = 0; c < chunks; ++c) {
+      const size_t off = pp.row_cut[c] * es, len = (pp.row_cut[c + 1] - pp.row_cut[c]) * es;
+      if (len)
+        CSRK_CUDA_TRY(cudaMemcpyAsync(xs + off, xh + off, len, cudaMemcpyHostToDevice,
+                                      pp.h2d));
+      CSRK_CUDA_TRY(cudaEventRecord(pp.ev_x[c], pp.h2d));
+    }
+    CSRK_CUDA_TRY(cudaEventRecord(m->ev0, pp.comp));
+    for (int c = 0; c < chunks; ++c) {
+      CSRK_CUDA_TRY(cudaStreamWaitEvent(pp.comp, pp.ev_x[pp.x_ready[c]], 0));
+      CSRK_TRY(launch_spmv(m, value_type, variant, nx, m->x_stage, m->y_stage, pp.comp,
+                           pp.tile_cut[c], pp.tile_cut[c + 1]));
+      CSRK_CUDA_TRY(cudaEventRecord(pp.ev_c[c], pp.comp));
+      const size_t off = pp.row_cut[c] * es, len = (pp.row_cut[c + 1] - pp.row_cut[c]) * es;
+      CSRK_CUDA_TRY(cudaStreamWaitEvent(pp.d2h, pp.ev_c[c], 0));
+      if (len)
+        CSRK_CUDA_TRY(cudaMemcpyAsync(yh + off, ys + off, len, cudaMemcpyDeviceToHost,
+                                      pp.d2h));
+    }
+    CSRK_CUDA_TRY(cudaEventRecord(m->ev1, pp.comp));
+    CSRK_CUDA_TRY(cudaStreamSynchronize(pp.d2h));
+    CSRK_CUDA_TRY(cudaStreamSynchronize(pp.comp));
+    return CSRK_OK;
   }
   if (m->n_cols)
     CSRK_CUDA_TRY(cudaMemcpyAsync(m->x_stage, x_host, m->n_cols * es,

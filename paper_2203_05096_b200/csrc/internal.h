@@ -5,6 +5,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <string>
+#include <vector>
 
 #include <cuda_runtime.h>
 
@@ -44,7 +45,15 @@ struct csrk_matrix {
   uint32_t *ssr_ptr = nullptr;  // n_ssr + 1 (k == 3)
   csrk::TilePlan plan;          // current streaming plan
   int sm_count = 0;
-  // host-API staging
+  // host-API staging and the overlapped host pipeline (csrk_spmv_host)
+  struct Pipe {
+    int chunks = 0;
+    int64_t plan_tiles = -1;  // n_tiles the cuts were computed for
+    std::vector<int64_t> tile_cut, row_cut;  // chunks + 1
+    std::vector<int> x_ready;                // x chunk needed by chunk c
+    cudaStream_t h2d = nullptr, comp = nullptr, d2h = nullptr;
+    std::vector<cudaEvent_t> ev_x, ev_c;
+  } pipe;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   void *x_stage = nullptr, *y_stage = nullptr;
@@ -62,7 +71,10 @@ int alloc_matrix_arrays(csrk_matrix *m, bool want64, bool want32);
 int ensure_plan(csrk_matrix *m, int64_t tile_cost, int64_t cap, int64_t stages,
                 cudaStream_t s);
 int launch_spmv(const csrk_matrix *m, int value_type, int variant, int nx,
-                const void *x, void *y, cudaStream_t stream);
+                const void *x, void *y, cudaStream_t stream, int64_t t0 = 0,
+                int64_t t1 = -1);
+int chunk_max_cols(const csrk_matrix *m, const uint32_t *row_cut_dev, int chunks,
+                   uint32_t *out_dev, cudaStream_t s);
 int launch_listing3(const csrk_matrix *m, int dx, int dy, const double *x,
                     double *y, int64_t *trace, cudaStream_t stream);
 int launch_listing4(const csrk_matrix *m, int dx, int dy, int dz,

@@ -436,9 +436,33 @@ __global__ void tile_bounds_kernel(const uint32_t *__restrict__ row_ptr,
   tile_row[t] = group_start(sr_ptr, ssr_ptr, cut_k, lo, n_groups, n_rows);
 }
 
+// max column read by the rows of each chunk [row_cut[c], row_cut[c+1])
+__global__ void chunk_max_col_kernel(const uint32_t *__restrict__ row_ptr,
+                                     const uint32_t *__restrict__ col_idx,
+                                     const uint32_t *__restrict__ row_cut,
+                                     uint32_t *__restrict__ out) {
+  const uint32_t c = blockIdx.x;
+  const uint32_t a = row_ptr[row_cut[c]], b = row_ptr[row_cut[c + 1]];
+  uint32_t mx = 0;
+  for (uint32_t p = a + threadIdx.x; p < b; p += blockDim.x)
+    mx = col_idx[p] > mx ? col_idx[p] : mx;
+  for (int o = 16; o > 0; o >>= 1) {
+    const uint32_t v = __shfl_down_sync(0xffffffffu, mx, o);
+    mx = v > mx ? v : mx;
+  }
+  __shared__ uint32_t red[32];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w)
+      mx = red[w] > mx ? red[w] : mx;
+    out[c] = mx;
+  }
+}
+
 template <typename V, int NX>
 int launch_stream(const csrk_matrix *m, const V *vals, const V *x, V *y,
-                  cudaStream_t stream) {
+                  cudaStream_t stream, int64_t t0, int64_t t1) {
   const TilePlan &pl = m->plan;
   const Geometry geo(static_cast<uint32_t>(pl.cap), static_cast<uint32_t>(pl.rcap),
                      static_cast<uint32_t>(pl.stages), sizeof(V));
@@ -453,24 +477,27 @@ int launch_stream(const csrk_matrix *m, const V *vals, const V *x, V *y,
     set_error("stream kernel does not fit on an SM (%zu bytes of shared memory)", smem);
     return CSRK_EINVAL;
   }
+  if (t1 < 0 || t1 > pl.n_tiles) t1 = pl.n_tiles;
+  if (t0 < 0) t0 = 0;
+  const int64_t count = t1 - t0;
   int64_t grid = static_cast<int64_t>(per_sm) * m->sm_count;
-  if (grid > pl.n_tiles) grid = pl.n_tiles;
+  if (grid > count) grid = count;
   if (grid < 1) return CSRK_OK;
   kern<<<static_cast<unsigned>(grid), kThreads, smem, stream>>>(
-      m->row_ptr, m->col_idx, vals, x, y, pl.tile_row,
-      static_cast<uint32_t>(pl.n_tiles), geo.cap, geo.rcap, geo.stages);
+      m->row_ptr, m->col_idx, vals, x, y, pl.tile_row + t0,
+      static_cast<uint32_t>(count), geo.cap, geo.rcap, geo.stages);
   CSRK_CUDA_TRY(cudaGetLastError());
   return CSRK_OK;
 }
 
 template <typename V>
 int dispatch_nx(const csrk_matrix *m, int variant, int nx, const V *vals,
-                const V *x, V *y, cudaStream_t s) {
-  if (variant == CSRK_SERIAL) return launch_stream<V, 0>(m, vals, x, y, s);
+                const V *x, V *y, cudaStream_t s, int64_t t0, int64_t t1) {
+  if (variant == CSRK_SERIAL) return launch_stream<V, 0>(m, vals, x, y, s, t0, t1);
   switch (nx) {
 #define CSRK_NX_CASE(N) \
   case N:               \
-    return launch_stream<V, N>(m, vals, x, y, s);
+    return launch_stream<V, N>(m, vals, x, y, s, t0, t1);
     CSRK_NX_CASE(1)
     CSRK_NX_CASE(2)
     CSRK_NX_CASE(3)
@@ -574,8 +601,17 @@ int ensure_plan(csrk_matrix *m, int64_t tile_cost, int64_t cap, int64_t stages,
   return CSRK_OK;
 }
 
+int chunk_max_cols(const csrk_matrix *m, const uint32_t *row_cut_dev, int chunks,
+                   uint32_t *out_dev, cudaStream_t s) {
+  chunk_max_col_kernel<<<chunks, 256, 0, s>>>(m->row_ptr, m->col_idx, row_cut_dev,
+                                             out_dev);
+  CSRK_CUDA_TRY(cudaGetLastError());
+  return CSRK_OK;
+}
+
 int launch_spmv(const csrk_matrix *m, int value_type, int variant, int nx,
-                const void *x, void *y, cudaStream_t stream) {
+                const void *x, void *y, cudaStream_t stream, int64_t t0,
+                int64_t t1) {
   if (variant != CSRK_SERIAL && variant != CSRK_STRIDED) {
     set_error("unknown SpMV variant %d", variant);
     return CSRK_EINVAL;
@@ -592,7 +628,7 @@ int launch_spmv(const csrk_matrix *m, int value_type, int variant, int nx,
     }
     return dispatch_nx<double>(m, variant, nx, m->vals64,
                                static_cast<const double *>(x),
-                               static_cast<double *>(y), stream);
+                               static_cast<double *>(y), stream, t0, t1);
   }
   if (value_type == CSRK_F32) {
     if (!m->vals32) {
@@ -601,7 +637,7 @@ int launch_spmv(const csrk_matrix *m, int value_type, int variant, int nx,
     }
     return dispatch_nx<float>(m, variant, nx, m->vals32,
                               static_cast<const float *>(x),
-                              static_cast<float *>(y), stream);
+                              static_cast<float *>(y), stream, t0, t1);
   }
   set_error("unknown value type %d", value_type);
   return CSRK_EINVAL;
