@@ -134,16 +134,20 @@ def spmv_csr3(m: CsrKMatrix, x, workers: int = 1, executor=None, *,
     return m.device().spmv_host(x, out=out)
 
 
-def spmv_gpu35(m: CsrKMatrix, x, dims: BlockDims) -> np.ndarray:
+def spmv_gpu35(m: CsrKMatrix, x, dims: BlockDims, *, out=None) -> np.ndarray:
     """Streaming kernel with the GPUSpMV-3.5 summation order: row nonzeros
     strided over ``dims.x`` lanes, then the halving tree.  Bitwise equal to
-    ``emulate_gpu_spmv35(m, x, dims)[0]``; no trace."""
+    ``emulate_gpu_spmv35(m, x, dims)[0]``; no trace.  ``out`` as spmv_csr3."""
     if m.k != 3:
         raise ValueError("emulate_gpu_spmv35 requires k = 3")
     x = _check_x(m.base, x)
     if dims.x not in STRIDED_NX:
-        return emulate_gpu_spmv35(m, x, dims)[0]
-    return m.device().spmv_host(x, variant=nat.CSRK_STRIDED, nx=dims.x)
+        y = emulate_gpu_spmv35(m, x, dims)[0]
+        if out is not None:
+            out[:] = y
+            return out
+        return y
+    return m.device().spmv_host(x, variant=nat.CSRK_STRIDED, nx=dims.x, out=out)
 
 
 def _listing(m: CsrKMatrix, x: np.ndarray, dims: BlockDims, which: int):
