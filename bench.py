@@ -285,6 +285,107 @@ def run_ours(args, log):
     return line
 
 
+def run_loop(args, log):
+    """--config C4 --loop cg|power: BASELINE configs[3], 100 SpMVs as a CG
+    inner loop on the 512^3 7-point Laplacian.  The matrix is generated in
+    HBM (csrk_stencil) in natural order with uniform 8 / 8 groups (k = 3,
+    identity permutation); one step = `--iters` loop iterations captured in
+    one CUDA graph."""
+    import torch
+
+    from paper_2203_05096_b200 import cg, synthetic
+    from paper_2203_05096_b200.bench import spmv_bytes
+
+    torch.cuda.set_device(0)
+    side = args.side
+    t0 = time.perf_counter()
+    dev = synthetic.device_stencil((side, side, side), 7).group_uniform(8, 8)
+    t_gen = time.perf_counter() - t0
+    n, nnz = dev.n_rows, dev.nnz
+    f32 = args.fp32
+    dtype = torch.float32 if f32 else torch.float64
+    vb = 4 if f32 else 8
+    if f32:
+        dev.ensure_f32()
+    log(f"[bench] C4 loop={args.loop}: n={n} nnz={nnz} generated in HBM in {t_gen:.1f}s")
+    g = torch.Generator(device="cuda").manual_seed(0)
+    b = (torch.rand(n, generator=g, device="cuda", dtype=torch.float64) * 2 - 1).to(dtype)
+    x = torch.zeros_like(b)
+    scratch = tuple(torch.empty_like(b) for _ in range(3))
+    iters = args.iters
+
+    def loop(stream):
+        if args.loop == "cg":
+            x.zero_()
+            cg.cg(dev, b, x, iters=iters, stream=stream, scratch=scratch, sync=False)
+        else:
+            x.copy_(b)
+            cg.power_iterations(dev, x, iters=iters, y=scratch[0], stream=stream)
+
+    graph = cg.GraphedLoop(loop)
+    for _ in range(args.warmup):
+        graph.replay()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        ev0.record()
+        for _ in range(args.steps):
+            graph.replay()
+        ev1.record()
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    spmv_flops = 2.0 * nnz * iters
+    gflops = spmv_flops / (ms * 1e-3) / 1e9
+    # bytes per iteration: the SpMV plus the vector kernels (CG: p.Ap reads 2n,
+    # update reads 4n writes 2n, direction reads 2n writes n; power: 2n + 2n)
+    vec_words = 11 * n if args.loop == "cg" else 4 * n
+    it_bytes = spmv_bytes(n, n, nnz, vb) + vec_words * vb
+    gbs = it_bytes * iters / (ms * 1e-3) / 1e9
+    peak, peak_src = measured_peak()
+    # e2e through the public API: b from pinned host, x back to pinned host
+    b_pin = torch.empty(n, dtype=dtype, pin_memory=True)
+    b_pin.copy_(b)
+    x_pin = torch.empty(n, dtype=dtype, pin_memory=True)
+    e2e_t = []
+    for _ in range(max(2, min(args.steps, 5))):
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        bd = b_pin.to("cuda", non_blocking=True)
+        xd = torch.zeros_like(bd)
+        if args.loop == "cg":
+            cg.cg(dev, bd, xd, iters=iters, scratch=scratch, sync=False)
+        else:
+            xd.copy_(bd)
+            cg.power_iterations(dev, xd, iters=iters, y=scratch[0])
+        x_pin.copy_(xd, non_blocking=True)
+        torch.cuda.synchronize()
+        e2e_t.append(time.perf_counter() - t1)
+    e2e_s = sum(e2e_t[1:]) / max(1, len(e2e_t) - 1)
+    return {
+        "metric": METRIC, "value": round(gflops, 2), "unit": "GFLOP/s", "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f32" if f32 else "f64",
+        "data": "synthetic (512^3 7-point Laplacian generated in HBM, b ~ U[-1,1))",
+        "config": {"workload": f"C4: {iters} SpMVs as a {args.loop} inner loop on the "
+                               f"{side}^3 7-point Laplacian, CUDA graph",
+                   "config_id": "C4", "n_rows": n, "nnz": nnz, "iterations_per_step": iters,
+                   "grouping": "natural order, uniform SR 8 / SSR 8 (identity permutation)",
+                   "ms_per_iteration": round(ms / iters, 5),
+                   "l2": "inputs larger than L2; no flush", "parallelism": "1 GPU"},
+        "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(gbs / peak, 4), "peak_source": peak_src,
+                     "traffic": None,
+                     "algorithmic_bytes_per_iteration": int(it_bytes)},
+        "e2e": {"value": round(spmv_flops / e2e_s / 1e9, 2), "unit": "GFLOP/s",
+                "h2d_bytes_per_step": n * vb, "d2h_bytes_per_step": n * vb,
+                "ms_per_step": round(e2e_s * 1e3, 3),
+                "call": f"paper_2203_05096_b200.cg.{'cg' if args.loop == 'cg' else 'power_iterations'}"},
+        "gpu_launches": args.steps * iters * (5 if args.loop == "cg" else 3),
+        "clocks": clk.summary(),
+    }
+
+
 def run_reference(args, log):
     """--impl reference: the reference's CPU CSR-3 algorithm (oracle port),
     all host cores, same config / metric."""
@@ -342,7 +443,11 @@ def main(argv=None):
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--config", default="C2", choices=("C1", "C2", "C3", "C5"))
+    ap.add_argument("--config", default="C2", choices=("C1", "C2", "C3", "C4", "C5"))
+    ap.add_argument("--loop", choices=("cg", "power"), default="cg",
+                    help="C4 only: the iterative loop around the SpMV")
+    ap.add_argument("--iters", type=int, default=100, help="C4: loop iterations per step")
+    ap.add_argument("--side", type=int, default=512, help="C4: grid side")
     ap.add_argument("--fp32", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=10.0)
     args = ap.parse_args(argv)
@@ -354,7 +459,12 @@ def main(argv=None):
         if rank == 0:
             print(msg, file=sys.stderr, flush=True)
 
-    line = run_reference(args, log) if args.impl == "reference" else run_ours(args, log)
+    if args.impl == "reference":
+        line = run_reference(args, log)
+    elif args.config == "C4":
+        line = run_loop(args, log)
+    else:
+        line = run_ours(args, log)
     if rank == 0 and line is not None:
         print(json.dumps(line), flush=True)
 

@@ -160,6 +160,25 @@ int csrk_row_variance(const csrk_matrix *m, double mean, double *out);
 int csrk_stencil(int device, int64_t nz, int64_t ny, int64_t nx, int points,
                  csrk_matrix **out);
 
+/* Give a handle uniform groups (k = 3): srs rows per super-row, ssrs
+ * super-rows per super-super-row, the last of each shorter -- the
+ * identity-permutation CSR-k of a generated stencil. */
+int csrk_matrix_group_uniform(csrk_matrix *m, int64_t srs, int64_t ssrs);
+
+/* ---- solvers around the SpMV -------------------
+ * csrk_cg: `iters` conjugate-gradient iterations for A x = b from the x
+ * given (device vectors of n_rows entries: b, x in/out, and scratch r, p,
+ * ap), every SpMV the streaming kernel (variant / nx as csrk_spmv);
+ * reductions in float64 with a fixed order (deterministic).  No host
+ * synchronisation unless `scalars` is non-NULL (then out = r.r, alpha, beta,
+ * p.Ap of the last iteration), so the call can be captured in a CUDA graph.
+ * csrk_power: `iters` repeated SpMVs x <- A x / max|A x| (y is scratch). */
+int csrk_cg(const csrk_matrix *m, int value_type, int variant, int nx,
+            const void *b, void *x, void *r, void *p, void *ap, int iters,
+            double *scalars, void *stream);
+int csrk_power(const csrk_matrix *m, int value_type, int variant, int nx,
+               void *x, void *y, int iters, void *stream);
+
 /* ---- Band-k reordering (native) -------------------------------------------
  * Bit-exact native restatement of reorder.py (band_k 415-469 and its
  * helpers).  Results are held in an opaque object and read back with

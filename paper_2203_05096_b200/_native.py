@@ -57,6 +57,9 @@ _SIGNATURES = {
     "csrk_gather_f64": ([I64, P, P, P, P], C.c_int),
     "csrk_stats": ([P, I64P], C.c_int),
     "csrk_row_variance": ([P, C.c_double, F64P], C.c_int),
+    "csrk_matrix_group_uniform": ([P, I64, I64], C.c_int),
+    "csrk_cg": ([P, C.c_int, C.c_int, C.c_int, P, P, P, P, P, C.c_int, F64P, P], C.c_int),
+    "csrk_power": ([P, C.c_int, C.c_int, C.c_int, P, P, C.c_int, P], C.c_int),
     "csrk_stencil": ([C.c_int, I64, I64, I64, C.c_int, C.POINTER(P)], C.c_int),
     "csrk_band_k": ([I64, U32P, U32P, C.c_int, F64P, C.POINTER(P)], C.c_int),
     "csrk_bandk_result_sizes": ([P, I64P], C.c_int),
@@ -229,6 +232,18 @@ class DeviceMatrix:
              u32p(sp) if sp is not None else None,
              u32p(ssp) if ssp is not None else None)
         return rp, ci, va, sp, ssp
+
+    def refresh(self):
+        shape = np.zeros(7, dtype=np.int64)
+        call("csrk_matrix_shape", self.ptr, i64p(shape))
+        (self.n_rows, self.n_cols, self.nnz, self.k, self.n_sr, self.n_ssr,
+         self.device) = (int(v) for v in shape)
+
+    def group_uniform(self, srs: int, ssrs: int):
+        """Make this handle CSR-k (k = 3) with uniform group sizes."""
+        call("csrk_matrix_group_uniform", self.ptr, int(srs), int(ssrs))
+        self.refresh()
+        return self
 
     def ensure_f32(self):
         call("csrk_matrix_add_f32", self.ptr)

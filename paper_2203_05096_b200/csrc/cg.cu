@@ -1,0 +1,313 @@
+// Conjugate-gradient loop around the CSR-k SpMV (
+// BASELINE config C4: "100 repeated SpMVs as a CG inner loop").
+//
+// The reference has no solver; this is a new caller of spmv_csr3.  Each CG
+// iteration is five kernels on one stream and never returns to the host, so
+// a whole run of iterations is captured once into a CUDA graph and replayed:
+//   1. Ap = A p                      (csrk_stream_kernel, bitwise spmv_csr3)
+//   2. partial p.Ap                  (block partials, fixed order)
+//   3. alpha = rr / pAp; x += alpha p; r -= alpha Ap; partial r.r
+//   4. beta = rr' / rr; p = r + beta p; rr = rr'   (reads the partials)
+// Scalars live in device memory.  Reductions use a fixed two-level tree
+// (per-block partials, then one block), so results are deterministic run to
+// run.  Vectors are float64 or float32 (reductions always in float64).
+
+#include <cstdint>
+
+#include "internal.h"
+
+namespace csrk {
+namespace {
+
+constexpr int kRedThreads = 512;
+constexpr int kRedBlocks = 148 * 4;  // partial-sum slots
+
+struct CgScalars {
+  double rr;       // r.r of the current residual
+  double pap;      // p.Ap
+  double rr_new;   // r.r after the update
+  double alpha, beta;
+  double pad[3];
+};
+
+template <typename T>
+__device__ __forceinline__ double block_sum(double v, double *red) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x < 32) {
+    s = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+  }
+  return s;  // valid in thread 0
+}
+
+// sum of the kRedBlocks partials in a fixed order (one warp)
+__device__ __forceinline__ double fold_partials(const double *partials) {
+  double s = 0.0;
+  if (threadIdx.x < 32) {
+    for (int i = threadIdx.x; i < kRedBlocks; i += 32) s += partials[i];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+  }
+  return s;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kRedThreads)
+    dot_partial_kernel(const T *__restrict__ a, const T *__restrict__ b, int64_t n,
+                       double *__restrict__ partials) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    s += static_cast<double>(a[i]) * static_cast<double>(b[i]);
+  const double t = block_sum<T>(s, red);
+  if (threadIdx.x == 0) partials[blockIdx.x] = t;
+}
+
+// alpha = rr / pAp; x += alpha p; r -= alpha Ap; partial r.r
+template <typename T>
+__global__ void __launch_bounds__(kRedThreads)
+    cg_update_kernel(T *__restrict__ x, T *__restrict__ r, const T *__restrict__ p,
+                     const T *__restrict__ ap, int64_t n, const double *__restrict__ pap_part,
+                     CgScalars *__restrict__ sc, double *__restrict__ rr_part) {
+  __shared__ double red[32];
+  __shared__ double s_alpha;
+  if (threadIdx.x < 32) {
+    const double pap = fold_partials(pap_part);
+    if (threadIdx.x == 0) {
+      const double alpha = pap != 0.0 ? sc->rr / pap : 0.0;
+      s_alpha = alpha;
+      if (blockIdx.x == 0) {
+        sc->pap = pap;
+        sc->alpha = alpha;
+      }
+    }
+  }
+  __syncthreads();
+  const double alpha = s_alpha;
+  double s = 0.0;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    x[i] = static_cast<T>(static_cast<double>(x[i]) + alpha * static_cast<double>(p[i]));
+    const double ri = static_cast<double>(r[i]) - alpha * static_cast<double>(ap[i]);
+    r[i] = static_cast<T>(ri);
+    const double rv = static_cast<double>(static_cast<T>(ri));
+    s += rv * rv;
+  }
+  const double t = block_sum<T>(s, red);
+  if (threadIdx.x == 0) rr_part[blockIdx.x] = t;
+}
+
+// beta = rr' / rr; p = r + beta p; rr = rr' (block 0 publishes)
+template <typename T>
+__global__ void __launch_bounds__(kRedThreads)
+    cg_direction_kernel(T *__restrict__ p, const T *__restrict__ r, int64_t n,
+                        const double *__restrict__ rr_part, CgScalars *__restrict__ sc) {
+  __shared__ double s_beta, s_rr;
+  if (threadIdx.x < 32) {
+    const double rr_new = fold_partials(rr_part);
+    if (threadIdx.x == 0) {
+      s_beta = sc->rr != 0.0 ? rr_new / sc->rr : 0.0;
+      s_rr = rr_new;
+    }
+  }
+  __syncthreads();
+  const double beta = s_beta;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    p[i] = static_cast<T>(static_cast<double>(r[i]) + beta * static_cast<double>(p[i]));
+  // every block read sc->rr above; a grid-wide order is needed before the
+  // write, so the publish happens in the next kernel (set_rr_kernel)
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    sc->rr_new = s_rr;
+    sc->beta = beta;
+  }
+}
+
+__global__ void set_rr_kernel(CgScalars *sc) { sc->rr = sc->rr_new; }
+
+// r = b - A x computed as r = b - ax; p = r; rr = r.r partials
+template <typename T>
+__global__ void __launch_bounds__(kRedThreads)
+    cg_init_kernel(const T *__restrict__ b, const T *__restrict__ ax, T *__restrict__ r,
+                   T *__restrict__ p, int64_t n, double *__restrict__ rr_part) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const T ri = static_cast<T>(static_cast<double>(b[i]) - static_cast<double>(ax[i]));
+    r[i] = ri;
+    p[i] = ri;
+    s += static_cast<double>(ri) * static_cast<double>(ri);
+  }
+  const double t = block_sum<T>(s, red);
+  if (threadIdx.x == 0) rr_part[blockIdx.x] = t;
+}
+
+__global__ void cg_init_scalar_kernel(const double *__restrict__ rr_part,
+                                      CgScalars *__restrict__ sc) {
+  const double rr = fold_partials(rr_part);
+  if (threadIdx.x == 0) {
+    sc->rr = rr;
+    sc->rr_new = rr;
+  }
+}
+
+// power-iteration normalisation x = y / max|y| (the repeated-SpMV loop of
+// SURVEY.md §8(d)): partial max, then scale
+template <typename T>
+__global__ void absmax_partial_kernel(const T *__restrict__ y, int64_t n,
+                                      double *__restrict__ partials) {
+  __shared__ double red[32];
+  double m = 0.0;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    m = fmax(m, fabs(static_cast<double>(y[i])));
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_down_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    m = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_down_sync(0xffffffffu, m, o));
+    if (threadIdx.x == 0) partials[blockIdx.x] = m;
+  }
+}
+
+template <typename T>
+__global__ void scale_by_max_kernel(const T *__restrict__ y, T *__restrict__ x, int64_t n,
+                                    const double *__restrict__ partials) {
+  __shared__ double s_inv;
+  if (threadIdx.x < 32) {
+    double m = 0.0;
+    for (int i = threadIdx.x; i < kRedBlocks; i += 32) m = fmax(m, partials[i]);
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_down_sync(0xffffffffu, m, o));
+    if (threadIdx.x == 0) s_inv = m > 0.0 ? 1.0 / m : 0.0;
+  }
+  __syncthreads();
+  const double inv = s_inv;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    x[i] = static_cast<T>(static_cast<double>(y[i]) * inv);
+}
+
+struct Scratch {
+  double *pap_part = nullptr, *rr_part = nullptr;
+  CgScalars *sc = nullptr;
+};
+
+template <typename T>
+int cg_run(const csrk_matrix *m, int value_type, int variant, int nx, const T *b, T *x,
+           T *r, T *p, T *ap, int iters, double *scalars_out, cudaStream_t s) {
+  const int64_t n = m->n_rows;
+  Scratch w;
+  CSRK_CUDA_TRY(cudaMallocAsync(&w.pap_part, kRedBlocks * sizeof(double), s));
+  CSRK_CUDA_TRY(cudaMallocAsync(&w.rr_part, kRedBlocks * sizeof(double), s));
+  CSRK_CUDA_TRY(cudaMallocAsync(&w.sc, sizeof(CgScalars), s));
+  CSRK_CUDA_TRY(cudaMemsetAsync(w.pap_part, 0, kRedBlocks * sizeof(double), s));
+  CSRK_CUDA_TRY(cudaMemsetAsync(w.rr_part, 0, kRedBlocks * sizeof(double), s));
+  CSRK_CUDA_TRY(cudaMemsetAsync(w.sc, 0, sizeof(CgScalars), s));
+  int rc = launch_spmv(m, value_type, variant, nx, x, ap, s);  // ap = A x0
+  if (rc == CSRK_OK) {
+    cg_init_kernel<T><<<kRedBlocks, kRedThreads, 0, s>>>(b, ap, r, p, n, w.rr_part);
+    cg_init_scalar_kernel<<<1, 32, 0, s>>>(w.rr_part, w.sc);
+  }
+  for (int it = 0; rc == CSRK_OK && it < iters; ++it) {
+    rc = launch_spmv(m, value_type, variant, nx, p, ap, s);
+    if (rc != CSRK_OK) break;
+    dot_partial_kernel<T><<<kRedBlocks, kRedThreads, 0, s>>>(p, ap, n, w.pap_part);
+    cg_update_kernel<T><<<kRedBlocks, kRedThreads, 0, s>>>(x, r, p, ap, n, w.pap_part,
+                                                          w.sc, w.rr_part);
+    cg_direction_kernel<T><<<kRedBlocks, kRedThreads, 0, s>>>(p, r, n, w.rr_part, w.sc);
+    set_rr_kernel<<<1, 1, 0, s>>>(w.sc);
+  }
+  cudaError_t e = cudaGetLastError();
+  if (rc == CSRK_OK && e != cudaSuccess) {
+    set_error("CUDA error %s in cg: %s", cudaGetErrorName(e), cudaGetErrorString(e));
+    rc = CSRK_ECUDA;
+  }
+  if (rc == CSRK_OK && scalars_out) {
+    CgScalars h;
+    e = cudaMemcpyAsync(&h, w.sc, sizeof(h), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) {
+      set_error("CUDA error %s in cg: %s", cudaGetErrorName(e), cudaGetErrorString(e));
+      rc = CSRK_ECUDA;
+    } else {
+      scalars_out[0] = h.rr;
+      scalars_out[1] = h.alpha;
+      scalars_out[2] = h.beta;
+      scalars_out[3] = h.pap;
+    }
+  }
+  cudaFreeAsync(w.pap_part, s);
+  cudaFreeAsync(w.rr_part, s);
+  cudaFreeAsync(w.sc, s);
+  return rc;
+}
+
+template <typename T>
+int power_run(const csrk_matrix *m, int value_type, int variant, int nx, T *x, T *y,
+              int iters, cudaStream_t s) {
+  double *part = nullptr;
+  CSRK_CUDA_TRY(cudaMallocAsync(&part, kRedBlocks * sizeof(double), s));
+  int rc = CSRK_OK;
+  for (int it = 0; it < iters && rc == CSRK_OK; ++it) {
+    rc = launch_spmv(m, value_type, variant, nx, x, y, s);
+    if (rc != CSRK_OK) break;
+    absmax_partial_kernel<T><<<kRedBlocks, kRedThreads, 0, s>>>(y, m->n_rows, part);
+    scale_by_max_kernel<T><<<kRedBlocks, kRedThreads, 0, s>>>(y, x, m->n_rows, part);
+  }
+  cudaFreeAsync(part, s);
+  if (rc == CSRK_OK) CSRK_CUDA_TRY(cudaGetLastError());
+  return rc;
+}
+
+}  // namespace
+}  // namespace csrk
+
+using namespace csrk;
+
+extern "C" {
+
+int csrk_cg(const csrk_matrix *m, int value_type, int variant, int nx, const void *b,
+            void *x, void *r, void *p, void *ap, int iters, double *scalars,
+            void *stream) {
+  if (!m || !b || !x || !r || !p || !ap || iters < 0) {
+    set_error("invalid argument to csrk_cg");
+    return CSRK_EINVAL;
+  }
+  if (m->n_rows != m->n_cols) {
+    set_error("CG requires a square matrix");
+    return CSRK_EINVAL;
+  }
+  CSRK_CUDA_TRY(cudaSetDevice(m->device));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (value_type == CSRK_F32)
+    return cg_run<float>(m, value_type, variant, nx, static_cast<const float *>(b),
+                         static_cast<float *>(x), static_cast<float *>(r),
+                         static_cast<float *>(p), static_cast<float *>(ap), iters,
+                         scalars, s);
+  return cg_run<double>(m, value_type, variant, nx, static_cast<const double *>(b),
+                        static_cast<double *>(x), static_cast<double *>(r),
+                        static_cast<double *>(p), static_cast<double *>(ap), iters,
+                        scalars, s);
+}
+
+int csrk_power(const csrk_matrix *m, int value_type, int variant, int nx, void *x,
+               void *y, int iters, void *stream) {
+  if (!m || !x || !y || iters < 0) {
+    set_error("invalid argument to csrk_power");
+    return CSRK_EINVAL;
+  }
+  CSRK_CUDA_TRY(cudaSetDevice(m->device));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (value_type == CSRK_F32)
+    return power_run<float>(m, value_type, variant, nx, static_cast<float *>(x),
+                            static_cast<float *>(y), iters, s);
+  return power_run<double>(m, value_type, variant, nx, static_cast<double *>(x),
+                           static_cast<double *>(y), iters, s);
+}
+
+}  // extern "C"

@@ -622,6 +622,57 @@ int stats_device(const csrk_matrix *m, int64_t out[5]) {
   return CSRK_OK;
 }
 
+__global__ void uniform_ptr_kernel(uint32_t *ptr, int64_t count, int64_t size,
+                                   int64_t total) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i <= count;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t v = i * size;
+    ptr[i] = static_cast<uint32_t>(v < total ? v : total);
+  }
+}
+
+int group_uniform(csrk_matrix *m, int64_t srs, int64_t ssrs) {
+  if (srs < 1 || ssrs < 1) {
+    set_error("group sizes must be at least 1");
+    return CSRK_EINVAL;
+  }
+  if (m->n_rows == 0) {
+    set_error("cannot group an empty matrix");
+    return CSRK_EINVAL;
+  }
+  CSRK_CUDA_TRY(cudaSetDevice(m->device));
+  const int64_t n_sr = (m->n_rows + srs - 1) / srs;
+  const int64_t n_ssr = (n_sr + ssrs - 1) / ssrs;
+  uint32_t *sr = nullptr, *ssr = nullptr;
+  CSRK_CUDA_TRY(cudaMalloc(&sr, (n_sr + 1) * sizeof(uint32_t)));
+  cudaError_t e = cudaMalloc(&ssr, (n_ssr + 1) * sizeof(uint32_t));
+  if (e != cudaSuccess) {
+    cudaFree(sr);
+    set_error("out of device memory");
+    return CSRK_ENOMEM;
+  }
+  uniform_ptr_kernel<<<grid_for(n_sr + 1, 256), 256, 0, m->stream>>>(sr, n_sr, srs,
+                                                                     m->n_rows);
+  uniform_ptr_kernel<<<grid_for(n_ssr + 1, 256), 256, 0, m->stream>>>(ssr, n_ssr, ssrs,
+                                                                      n_sr);
+  CSRK_CUDA_TRY(cudaGetLastError());
+  cudaFree(m->sr_ptr);
+  cudaFree(m->ssr_ptr);
+  m->sr_ptr = sr;
+  m->ssr_ptr = ssr;
+  m->k = 3;
+  m->n_sr = n_sr;
+  m->n_ssr = n_ssr;
+  // force a new plan for the new grouping
+  const int64_t tc = m->plan.tile_cost, cap = m->plan.cap, st = m->plan.stages;
+  cudaFree(m->plan.tile_row);
+  m->plan.tile_row = nullptr;
+  m->pipe.plan_tiles = -1;
+  CSRK_TRY(ensure_plan(m, tc, cap, st, m->stream));
+  CSRK_CUDA_TRY(cudaStreamSynchronize(m->stream));
+  return CSRK_OK;
+}
+
 int row_variance(const csrk_matrix *m, double mean, double *out) {
   const int64_t n = m->n_rows;
   if (n == 0) {
@@ -745,6 +796,14 @@ int csrk_stats(const csrk_matrix *m, int64_t out[5]) {
     return CSRK_EINVAL;
   }
   return csrk::stats_device(m, out);
+}
+
+int csrk_matrix_group_uniform(csrk_matrix *m, int64_t srs, int64_t ssrs) {
+  if (!m) {
+    csrk::set_error("null argument");
+    return CSRK_EINVAL;
+  }
+  return csrk::group_uniform(m, srs, ssrs);
 }
 
 int csrk_row_variance(const csrk_matrix *m, double mean, double *out) {

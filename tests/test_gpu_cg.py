@@ -1,0 +1,102 @@
+"""CG / repeated-SpMV loops around the CSR-k kernel:
+agreement with a float64 numpy CG, determinism, CUDA-graph replay, and the
+device stencil + uniform grouping path used for C4."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import paper_2203_05096_b200 as ck
+from oracle import oracle as O
+from paper_2203_05096_b200 import cg, synthetic
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+def _numpy_cg(rp, ci, va, b, iters):
+    def matvec(v):
+        return O.spmv_serial(rp, ci, va, v)
+    x = np.zeros_like(b)
+    r = b - matvec(x)
+    p = r.copy()
+    rr = r @ r
+    for _ in range(iters):
+        ap = matvec(p)
+        alpha = rr / (p @ ap)
+        x += alpha * p
+        r -= alpha * ap
+        rr_new = r @ r
+        p = r + (rr_new / rr) * p
+        rr = rr_new
+    return x, rr
+
+
+def _laplacian(shape=(24, 24, 24)):
+    n, rp, ci, va = synthetic.stencil_arrays(shape, 7)
+    a = ck.CsrMatrix(n, n, rp, ci, va)
+    res = ck.band_k(a, 3, [8, 8])
+    return a, res, ck.pack_csrk(a, res.perm, res.level_group_sizes)
+
+
+def test_cg_matches_numpy_and_converges():
+    a, res, m = _laplacian()
+    n = a.n_rows
+    b_np = np.random.default_rng(0).uniform(-1, 1, n)[res.perm.inv]
+    x_ref, rr_ref = _numpy_cg(m.base.row_ptr, m.base.col_idx, m.base.vals, b_np, 60)
+    b = torch.from_numpy(b_np).cuda()
+    x, info = cg.cg(m, b, iters=60)
+    xs = x.cpu().numpy()
+    assert np.abs(xs - x_ref).max() <= 1e-9 * np.abs(x_ref).max()
+    assert info["rr"] == pytest.approx(rr_ref, rel=1e-6)
+    resid = b_np - O.spmv_serial(m.base.row_ptr, m.base.col_idx, m.base.vals, xs)
+    assert np.linalg.norm(resid) < 1e-3 * np.linalg.norm(b_np)
+    # deterministic: a second run gives the same bits
+    x2, _ = cg.cg(m, b, iters=60)
+    assert torch.equal(x, x2)
+
+
+def test_cg_graph_replay_equals_eager_and_fp32():
+    a, res, m = _laplacian((20, 20, 20))
+    n = a.n_rows
+    b = torch.from_numpy(np.random.default_rng(1).uniform(-1, 1, n)).cuda()
+    x_eager, _ = cg.cg(m, b, iters=25)
+    x = torch.zeros_like(b)
+    scratch = tuple(torch.empty_like(b) for _ in range(3))
+
+    def loop(stream):
+        x.zero_()
+        cg.cg(m, b, x, iters=25, stream=stream, scratch=scratch, sync=False)
+
+    g = cg.GraphedLoop(loop)
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(x, x_eager)
+    x32, info32 = cg.cg(m, b.float(), iters=25)
+    assert (x32.double() - x_eager).abs().max().item() < 1e-3 * x_eager.abs().max().item()
+
+
+def test_power_iterations_normalise():
+    a, res, m = _laplacian((16, 16, 16))
+    n = a.n_rows
+    x0 = np.random.default_rng(2).uniform(0.5, 1.5, n)
+    x = torch.from_numpy(x0.copy()).cuda()
+    cg.power_iterations(m, x, iters=5)
+    v = x0.copy()
+    for _ in range(5):
+        yv = O.spmv_serial(m.base.row_ptr, m.base.col_idx, m.base.vals, v)
+        v = yv * (1.0 / np.abs(yv).max())
+    np.testing.assert_array_equal(x.cpu().numpy(), v)
+
+
+def test_device_stencil_uniform_groups():
+    dev = synthetic.device_stencil((30, 31, 32), 7).group_uniform(8, 8)
+    assert dev.k == 3 and dev.n_sr == -(-dev.n_rows // 8)
+    rp, ci, va, sp, ssp = dev.download()
+    assert sp[-1] == dev.n_rows and ssp[-1] == dev.n_sr
+    x = np.random.default_rng(3).uniform(-1, 1, dev.n_rows)
+    np.testing.assert_array_equal(dev.spmv_host(x), O.spmv_serial(rp, ci, va, x))
+    # the C4 analytic check: Laplacian row sums are 7 - row length
+    y1 = dev.spmv_host(np.ones(dev.n_rows))
+    np.testing.assert_array_equal(y1, 7.0 - np.diff(rp.astype(np.int64)))
