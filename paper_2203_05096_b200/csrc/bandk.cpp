@@ -24,7 +24,10 @@
 // 2^31 because nnz <= 2^31 - 1, format.py:35-37) and int64 adjacency offsets.
 
 #include <algorithm>
+#include <chrono>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <new>
@@ -45,6 +48,26 @@ using i32 = int32_t;
 using i64 = int64_t;
 
 constexpr double kMinMatchShrink = 0.05;  // reorder.py:32
+
+// optional phase timing (CSRK_BANDK_PROFILE=1 prints to stderr)
+struct PhaseClock {
+  static double acc[8];
+  static const char *names[8];
+  int id;
+  std::chrono::steady_clock::time_point t0;
+  explicit PhaseClock(int i) : id(i), t0(std::chrono::steady_clock::now()) {}
+  ~PhaseClock() {
+    acc[id] += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  }
+  static void report() {
+    if (!std::getenv("CSRK_BANDK_PROFILE")) return;
+    for (int i = 0; i < 6; ++i) std::fprintf(stderr, "[band_k] %-10s %8.3f s\n", names[i], acc[i]);
+    for (double &a : acc) a = 0.0;
+  }
+};
+double PhaseClock::acc[8] = {0};
+const char *PhaseClock::names[8] = {"build", "wbo", "relabel", "matching", "contract",
+                                    "expand", "", ""};
 
 struct Graph {
   i32 n = 0;
@@ -69,6 +92,7 @@ void finish_rows(i32 n, const std::vector<i64> &start,
                  bool merge_unit, Graph &g) {
   g.ptr.assign(static_cast<size_t>(n) + 1, 0);
   std::vector<i64> kept(n, 0);
+#pragma omp parallel for schedule(dynamic, 4096)
   for (i32 r = 0; r < n; ++r) {
     uint64_t *b = packed.data() + start[r];
     uint64_t *e = b + cnt[r];
@@ -88,6 +112,7 @@ void finish_rows(i32 n, const std::vector<i64> &start,
   for (i32 r = 0; r < n; ++r) g.ptr[r + 1] = g.ptr[r] + kept[r];
   g.idx.resize(g.ptr[n]);
   g.ew.resize(g.ptr[n]);
+#pragma omp parallel for schedule(dynamic, 4096)
   for (i32 r = 0; r < n; ++r) {
     const uint64_t *b = packed.data() + start[r];
     i64 o = g.ptr[r];
@@ -100,13 +125,19 @@ void finish_rows(i32 n, const std::vector<i64> &start,
 }
 
 Graph build_graph(i64 n64, const uint32_t *row_ptr, const uint32_t *col_idx) {
+  PhaseClock pc(0);
   const i32 n = static_cast<i32>(n64);
+  // counts and fills run in parallel; slot order inside a row is irrelevant
+  // because finish_rows sorts every row
   std::vector<i64> cnt(n, 0);
+#pragma omp parallel for schedule(dynamic, 4096)
   for (i32 r = 0; r < n; ++r)
     for (i64 p = row_ptr[r]; p < row_ptr[r + 1]; ++p) {
       const i32 c = static_cast<i32>(col_idx[p]);
       if (c != r) {
+#pragma omp atomic
         ++cnt[r];
+#pragma omp atomic
         ++cnt[c];
       }
     }
@@ -114,12 +145,18 @@ Graph build_graph(i64 n64, const uint32_t *row_ptr, const uint32_t *col_idx) {
   for (i32 r = 0; r < n; ++r) start[r + 1] = start[r] + cnt[r];
   std::vector<uint64_t> packed(start[n]);
   std::vector<i64> fill(start.begin(), start.end() - 1);
+#pragma omp parallel for schedule(dynamic, 4096)
   for (i32 r = 0; r < n; ++r)
     for (i64 p = row_ptr[r]; p < row_ptr[r + 1]; ++p) {
       const i32 c = static_cast<i32>(col_idx[p]);
       if (c != r) {
-        packed[fill[r]++] = (static_cast<uint64_t>(c) << 32) | 1u;
-        packed[fill[c]++] = (static_cast<uint64_t>(r) << 32) | 1u;
+        i64 a, b;
+#pragma omp atomic capture
+        a = fill[r]++;
+#pragma omp atomic capture
+        b = fill[c]++;
+        packed[a] = (static_cast<uint64_t>(c) << 32) | 1u;
+        packed[b] = (static_cast<uint64_t>(r) << 32) | 1u;
       }
     }
   Graph g;
@@ -131,6 +168,7 @@ Graph build_graph(i64 n64, const uint32_t *row_ptr, const uint32_t *col_idx) {
 // node v becomes fwd[v]  (reorder.py:192-196)
 Graph relabel(const Graph &g, const std::vector<i32> &fwd,
               const std::vector<i32> &inv) {
+  PhaseClock pc(2);
   Graph out;
   const i32 n = g.n;
   std::vector<i64> start(static_cast<size_t>(n) + 1, 0), cnt(n);
@@ -139,6 +177,7 @@ Graph relabel(const Graph &g, const std::vector<i32> &fwd,
     start[i + 1] = start[i] + cnt[i];
   }
   std::vector<uint64_t> packed(start[n]);
+#pragma omp parallel for schedule(dynamic, 4096)
   for (i32 i = 0; i < n; ++i) {
     const i32 v = inv[i];
     i64 o = start[i];
@@ -148,30 +187,39 @@ Graph relabel(const Graph &g, const std::vector<i32> &fwd,
   }
   finish_rows(n, start, cnt, packed, false, out);
   out.nw.resize(n);
+#pragma omp parallel for
   for (i32 i = 0; i < n; ++i) out.nw[i] = g.nw[inv[i]];
   return out;
 }
 
 // collapse nodes by f2c into m coarse nodes (reorder.py:176-184)
 Graph contract(const Graph &g, const std::vector<i32> &f2c, i32 m) {
+  PhaseClock pc(4);
   const i32 n = g.n;
   std::vector<i64> cnt(m, 0);
+#pragma omp parallel for schedule(dynamic, 4096)
   for (i32 v = 0; v < n; ++v) {
     const i32 cv = f2c[v];
-    for (i64 p = g.ptr[v]; p < g.ptr[v + 1]; ++p)
-      if (f2c[g.idx[p]] != cv) ++cnt[cv];
+    i64 c = 0;
+    for (i64 p = g.ptr[v]; p < g.ptr[v + 1]; ++p) c += f2c[g.idx[p]] != cv;
+#pragma omp atomic
+    cnt[cv] += c;
   }
   std::vector<i64> start(static_cast<size_t>(m) + 1, 0);
   for (i32 c = 0; c < m; ++c) start[c + 1] = start[c] + cnt[c];
   std::vector<uint64_t> packed(start[m]);
   std::vector<i64> fill(start.begin(), start.end() - 1);
+#pragma omp parallel for schedule(dynamic, 4096)
   for (i32 v = 0; v < n; ++v) {
     const i32 cv = f2c[v];
     for (i64 p = g.ptr[v]; p < g.ptr[v + 1]; ++p) {
       const i32 cu = f2c[g.idx[p]];
-      if (cu != cv)
-        packed[fill[cv]++] =
-            (static_cast<uint64_t>(cu) << 32) | static_cast<uint32_t>(g.ew[p]);
+      if (cu != cv) {
+        i64 slot;
+#pragma omp atomic capture
+        slot = fill[cv]++;
+        packed[slot] = (static_cast<uint64_t>(cu) << 32) | static_cast<uint32_t>(g.ew[p]);
+      }
     }
   }
   Graph out;
@@ -195,6 +243,7 @@ std::vector<i32> degree_order(const Graph &g) {
 }
 
 std::vector<i32> heavy_edge_matching(const Graph &g) {
+  PhaseClock pc(3);
   const i32 n = g.n;
   std::vector<i32> match(n, -1);
   for (i32 v : degree_order(g)) {
@@ -295,6 +344,7 @@ i32 pseudo_peripheral(const Graph &g, const std::vector<i32> &comp,
 }
 
 Permutation32 weighted_bandwidth_order(const Graph &g) {
+  PhaseClock pc(1);
   const i32 n = g.n;
   KeyLess less{&g};
   // connected components in root-index order; a component's first node is
@@ -423,6 +473,7 @@ struct Level {  // a coarsening map after band ordering of the coarse level
 // _expand_level + _order_members (reorder.py:339-412)
 void expand_level(const Graph &g, const Level &lv, const std::vector<i32> &seq,
                   std::vector<i32> &fine_seq, std::vector<i64> &sizes) {
+  PhaseClock pc(5);
   const i32 n = g.n;
   KeyLess less{&g};
   std::vector<i64> placed(n, -1);
@@ -548,6 +599,7 @@ void band_k(i64 n64, const uint32_t *row_ptr, const uint32_t *col_idx, int k,
   }
   res.fwd.assign(n64, 0);
   for (i64 i = 0; i < n64; ++i) res.fwd[base.inv[seq[i]]] = i;
+  PhaseClock::report();
   res.sizes1 = collected.back();
   if (k == 3) res.sizes2 = collected.front();
 }
