@@ -154,6 +154,29 @@ int csrk_stats(const csrk_matrix *m, int64_t out[5]);
  * float(nnz) / n_rows as numpy computes it. */
 int csrk_row_variance(const csrk_matrix *m, double mean, double *out);
 
+/* Stable LSD radix sort of n (uint64 key, uint32 value) pairs in device
+ * memory by key bits [begin_bit, end_bit) (multiples of 8) -- the sorting
+ * primitive of device-side construction. */
+int csrk_sort_pairs(int device, int64_t n, uint64_t *keys, uint32_t *vals,
+                    int begin_bit, int end_bit, void *stream);
+
+/* Device graphs (first stage of device-side Band-k): the graph of A + A^T
+ * without the diagonal (build_graph, reorder.py:115-135), relabelling by a
+ * permutation (_relabel_graph, reorder.py:192-196) and contraction by a
+ * fine-to-coarse map (_contract, reorder.py:176-184), built on the device by
+ * composite-key radix sorts; arrays identical to the host restatement. */
+typedef struct csrk_dgraph csrk_dgraph;
+int csrk_dgraph_build(const csrk_matrix *a, csrk_dgraph **out);
+int csrk_dgraph_relabel(const csrk_dgraph *g, const int64_t *fwd_host,
+                        csrk_dgraph **out);
+int csrk_dgraph_contract(const csrk_dgraph *g, const int64_t *f2c_host,
+                         int64_t m, csrk_dgraph **out);
+/* out = n, number of directed adjacency entries */
+int csrk_dgraph_sizes(const csrk_dgraph *g, int64_t out[2]);
+int csrk_dgraph_download(const csrk_dgraph *g, int64_t *ptr, int64_t *idx,
+                         int64_t *ew, int64_t *nw);
+int csrk_dgraph_free(csrk_dgraph *g);
+
 /* Synthetic stencil generator writing canonical CSR on the device
  * (SURVEY.md §8(d)); shape = {nz, ny, nx} (nz = 1 for 2D), points = 5, 7, 27.
  * Produces a k = 1 handle (natural order). */

@@ -60,6 +60,13 @@ _SIGNATURES = {
     "csrk_matrix_group_uniform": ([P, I64, I64], C.c_int),
     "csrk_cg": ([P, C.c_int, C.c_int, C.c_int, P, P, P, P, P, C.c_int, F64P, P], C.c_int),
     "csrk_power": ([P, C.c_int, C.c_int, C.c_int, P, P, C.c_int, P], C.c_int),
+    "csrk_dgraph_build": ([P, C.POINTER(P)], C.c_int),
+    "csrk_dgraph_relabel": ([P, I64P, C.POINTER(P)], C.c_int),
+    "csrk_dgraph_contract": ([P, I64P, I64, C.POINTER(P)], C.c_int),
+    "csrk_dgraph_sizes": ([P, I64P], C.c_int),
+    "csrk_dgraph_download": ([P, I64P, I64P, I64P, I64P], C.c_int),
+    "csrk_dgraph_free": ([P], C.c_int),
+    "csrk_sort_pairs": ([C.c_int, I64, P, P, C.c_int, C.c_int, P], C.c_int),
     "csrk_stencil": ([C.c_int, I64, I64, I64, C.c_int, C.POINTER(P)], C.c_int),
     "csrk_band_k": ([I64, U32P, U32P, C.c_int, F64P, C.POINTER(P)], C.c_int),
     "csrk_bandk_result_sizes": ([P, I64P], C.c_int),

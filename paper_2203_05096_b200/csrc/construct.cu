@@ -430,6 +430,10 @@ struct DevBuf {
 
 }  // namespace
 
+int exclusive_scan_i64(const int64_t *in, int64_t n, int64_t *out, cudaStream_t s) {
+  return exclusive_scan(in, n, out, s);
+}
+
 int pack_device(int device, int64_t n, int64_t nnz, const uint32_t *row_ptr_h,
                 const uint32_t *col_idx_h, const double *vals_h,
                 const int64_t *fwd_h, const int64_t *inv_h, int n_levels,

@@ -1,0 +1,80 @@
+"""Sweep the streaming kernel's tile plan (tile cost x ring depth) on B200.
+
+For the given configs, builds the CSR-k matrix once and times the kernel
+(CUDA events, median of 20 launches) for every plan in the grid, in fp64 and
+fp32, with the tuned variant.  Prints one JSON line per (config, dtype, plan)
+and writes gpurun_out/plan_sweep.json.
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import bench  # noqa: E402
+import paper_2203_05096_b200 as ck  # noqa: E402
+from paper_2203_05096_b200.bench import spmv_bytes  # noqa: E402
+
+TILES = (1024, 1536, 2048, 3072, 4096, 6144)
+STAGES = (2, 3, 4)
+
+
+def median_ms(fn, reps=20):
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        b.synchronize()
+        ts.append(a.elapsed_time(b))
+    return float(np.median(ts))
+
+
+def main():
+    configs = sys.argv[1:] or ["C2", "C3", "C5"]
+    out = []
+    for cfg in configs:
+        a, m, xp, params, _ = bench.build_matrix(cfg, lambda s: print(s, file=sys.stderr))
+        n, nnz = a.n_rows, a.nnz
+        dims = params.block_dims
+        variant = "strided" if params.kernel_variant.value == "cuda35" else "serial"
+        dev = m.device()
+        for dtype in (torch.float64, torch.float32):
+            xd = torch.from_numpy(xp).to("cuda", dtype)
+            yd = torch.empty(n, dtype=dtype, device="cuda")
+            vb = 8 if dtype == torch.float64 else 4
+            for variant_i in sorted({variant, "serial"}):
+                for t in TILES:
+                    for s in STAGES:
+                        try:
+                            dev.set_plan(t, 0, s)
+                        except ValueError:
+                            continue
+                        ms = median_ms(lambda: ck.spmv_device(m, xd, yd, dims=dims,
+                                                              variant=variant_i))
+                        gbs = spmv_bytes(n, n, nnz, vb) / (ms * 1e-3) / 1e9
+                        rec = {"config": cfg, "dtype": str(dtype)[6:], "variant": variant_i,
+                               "nx": dims.x if variant_i == "strided" else 0,
+                               "tile_cost": t, "stages": s, "ms": round(ms, 4),
+                               "gbs": round(gbs, 1)}
+                        print(json.dumps(rec), flush=True)
+                        out.append(rec)
+            dev.set_plan(0, 0, 0)
+        del m, dev
+        torch.cuda.empty_cache()
+    os.makedirs("gpurun_out", exist_ok=True)
+    with open("gpurun_out/plan_sweep.json", "w") as fh:
+        json.dump(out, fh, indent=1)
+
+
+if __name__ == "__main__":
+    main()
