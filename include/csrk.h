@@ -176,6 +176,10 @@ int csrk_dgraph_sizes(const csrk_dgraph *g, int64_t out[2]);
 int csrk_dgraph_download(const csrk_dgraph *g, int64_t *ptr, int64_t *idx,
                          int64_t *ew, int64_t *nw);
 int csrk_dgraph_free(csrk_dgraph *g);
+/* weighted_bandwidth_order (reorder.py:281-336) of a device graph, bit-exact:
+ * level-synchronous Cuthill-McKee with min-position parent claims, all
+ * components at once; fwd[n] written to host memory. */
+int csrk_dgraph_wbo(const csrk_dgraph *g, int64_t *fwd_host);
 
 /* Synthetic stencil generator writing canonical CSR on the device
  * (SURVEY.md §8(d)); shape = {nz, ny, nx} (nz = 1 for 2D), points = 5, 7, 27.

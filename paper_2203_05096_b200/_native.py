@@ -66,6 +66,7 @@ _SIGNATURES = {
     "csrk_dgraph_sizes": ([P, I64P], C.c_int),
     "csrk_dgraph_download": ([P, I64P, I64P, I64P, I64P], C.c_int),
     "csrk_dgraph_free": ([P], C.c_int),
+    "csrk_dgraph_wbo": ([P, I64P], C.c_int),
     "csrk_sort_pairs": ([C.c_int, I64, P, P, C.c_int, C.c_int, P], C.c_int),
     "csrk_stencil": ([C.c_int, I64, I64, I64, C.c_int, C.POINTER(P)], C.c_int),
     "csrk_band_k": ([I64, U32P, U32P, C.c_int, F64P, C.POINTER(P)], C.c_int),

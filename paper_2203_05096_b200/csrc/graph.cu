@@ -15,13 +15,6 @@
 
 #include "internal.h"
 
-struct csrk_dgraph {
-  int device = 0;
-  int64_t n = 0, m = 0;
-  int64_t *ptr = nullptr;
-  int32_t *idx = nullptr, *ew = nullptr, *nw = nullptr;
-};
-
 namespace csrk {
 namespace {
 

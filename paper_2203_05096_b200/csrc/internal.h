@@ -60,6 +60,13 @@ struct csrk_matrix {
   size_t x_stage_bytes = 0, y_stage_bytes = 0;
 };
 
+struct csrk_dgraph {
+  int device = 0;
+  int64_t n = 0, m = 0;
+  int64_t *ptr = nullptr;
+  int32_t *idx = nullptr, *ew = nullptr, *nw = nullptr;
+};
+
 namespace csrk {
 
 // padded element count for col_idx / vals allocations: room for the 16-byte
