@@ -166,6 +166,7 @@ int csrk_sort_pairs(int device, int64_t n, uint64_t *keys, uint32_t *vals,
  * fine-to-coarse map (_contract, reorder.py:176-184), built on the device by
  * composite-key radix sorts; arrays identical to the host restatement. */
 typedef struct csrk_dgraph csrk_dgraph;
+typedef struct csrk_bandk_result csrk_bandk_result;
 int csrk_dgraph_build(const csrk_matrix *a, csrk_dgraph **out);
 int csrk_dgraph_relabel(const csrk_dgraph *g, const int64_t *fwd_host,
                         csrk_dgraph **out);
@@ -180,6 +181,16 @@ int csrk_dgraph_free(csrk_dgraph *g);
  * level-synchronous Cuthill-McKee with min-position parent claims, all
  * components at once; fwd[n] written to host memory. */
 int csrk_dgraph_wbo(const csrk_dgraph *g, int64_t *fwd_host);
+/* heavy_edge_matching (reorder.py:138-173) on the device (Jacobi fixed
+ * point over visit ranks); match[n] to host memory, sweeps in *iters. */
+int csrk_dgraph_match(const csrk_dgraph *g, int64_t *match_host, int *iters);
+/* coarsen (reorder.py:199-237) on the device: new coarse graph + f2c[n]. */
+int csrk_dgraph_coarsen(const csrk_dgraph *g, double target, int64_t *f2c_host,
+                        csrk_dgraph **out);
+/* band_k (reorder.py:415-469) entirely on the device, bit-exact with
+ * csrk_band_k; the matrix handle supplies the pattern (any k). */
+int csrk_band_k_device(const csrk_matrix *a, int k, const double *targets,
+                       csrk_bandk_result **out);
 
 /* Synthetic stencil generator writing canonical CSR on the device
  * (SURVEY.md §8(d)); shape = {nz, ny, nx} (nz = 1 for 2D), points = 5, 7, 27.
@@ -210,7 +221,6 @@ int csrk_power(const csrk_matrix *m, int value_type, int variant, int nx,
  * Bit-exact native restatement of reorder.py (band_k 415-469 and its
  * helpers).  Results are held in an opaque object and read back with
  * csrk_bandk_result_get. */
-typedef struct csrk_bandk_result csrk_bandk_result;
 int csrk_band_k(int64_t n, const uint32_t *row_ptr, const uint32_t *col_idx,
                 int k, const double *targets, csrk_bandk_result **out);
 /* sizes: out[0] = n, out[1] = len(level 1 sizes), out[2] = len(level 2) */

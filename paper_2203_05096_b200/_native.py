@@ -67,6 +67,9 @@ _SIGNATURES = {
     "csrk_dgraph_download": ([P, I64P, I64P, I64P, I64P], C.c_int),
     "csrk_dgraph_free": ([P], C.c_int),
     "csrk_dgraph_wbo": ([P, I64P], C.c_int),
+    "csrk_dgraph_match": ([P, I64P, C.POINTER(C.c_int)], C.c_int),
+    "csrk_dgraph_coarsen": ([P, C.c_double, I64P, C.POINTER(P)], C.c_int),
+    "csrk_band_k_device": ([P, C.c_int, F64P, C.POINTER(P)], C.c_int),
     "csrk_sort_pairs": ([C.c_int, I64, P, P, C.c_int, C.c_int, P], C.c_int),
     "csrk_stencil": ([C.c_int, I64, I64, I64, C.c_int, C.POINTER(P)], C.c_int),
     "csrk_band_k": ([I64, U32P, U32P, C.c_int, F64P, C.POINTER(P)], C.c_int),

@@ -23,7 +23,7 @@ BUILD = os.path.join(PKG, "_build")
 LIB_DIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIB_DIR, "libcsrk_cuda.so")
 
-CUDA_SOURCES = ["abi.cu", "spmv.cu", "listing.cu", "construct.cu", "cg.cu", "sort.cu", "graph.cu", "rcm.cu"]
+CUDA_SOURCES = ["abi.cu", "spmv.cu", "listing.cu", "construct.cu", "cg.cu", "sort.cu", "graph.cu", "rcm.cu", "coarsen.cu", "bandk_dev.cu"]
 CXX_SOURCES = ["bandk.cpp"]
 HEADERS = [os.path.join(CSRC, "internal.h"), os.path.join(REPO, "include", "csrk.h")]
 

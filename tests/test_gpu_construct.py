@@ -133,3 +133,89 @@ def test_device_wbo_matches_native(golden):
                     nat.call("csrk_dgraph_free", ct)
         finally:
             nat.call("csrk_dgraph_free", dg)
+
+
+def _dev_graph(a):
+    dg = C.c_void_p()
+    nat.call("csrk_dgraph_build", a.device().ptr, C.byref(dg))
+    return dg
+
+
+def test_device_matching_and_coarsen_match_native(golden):
+    import paper_2203_05096_b200 as ck
+    from paper_2203_05096_b200 import synthetic
+    mats = [golden.csr(name) for name in golden.names]
+    n, rp, ci, va = synthetic.stencil_arrays((30, 40, 50), 7)
+    mats.append(ck.CsrMatrix(n, n, rp, ci, va))
+    for a in mats:
+        g = ck.build_graph(a)
+        dg = _dev_graph(a)
+        try:
+            match = np.zeros(g.n_nodes, dtype=np.int64)
+            iters = C.c_int(0)
+            nat.call("csrk_dgraph_match", dg, nat.i64p(match), C.byref(iters))
+            np.testing.assert_array_equal(match, ck.heavy_edge_matching(g))
+            for target in (2, 3, 7):
+                coarse, cmap = ck.coarsen(g, target)
+                f2c = np.zeros(g.n_nodes, dtype=np.int64)
+                cg = C.c_void_p()
+                nat.call("csrk_dgraph_coarsen", dg, float(target), nat.i64p(f2c),
+                         C.byref(cg))
+                try:
+                    np.testing.assert_array_equal(f2c, cmap.fine_to_coarse)
+                    _assert_graph_equal(cg, coarse, f"coarsen {target}")
+                finally:
+                    nat.call("csrk_dgraph_free", cg)
+        finally:
+            nat.call("csrk_dgraph_free", dg)
+
+
+def _device_band_k(a, k, targets):
+    out = C.c_void_p()
+    t = np.ascontiguousarray(targets, dtype=np.float64)
+    nat.call("csrk_band_k_device", a.device().ptr, k, nat.f64p(t), C.byref(out))
+    try:
+        sizes = np.zeros(3, dtype=np.int64)
+        nat.call("csrk_bandk_result_sizes", out, nat.i64p(sizes))
+        fwd = np.zeros(int(sizes[0]), dtype=np.int64)
+        s1 = np.zeros(int(sizes[1]), dtype=np.int64)
+        s2 = np.zeros(max(1, int(sizes[2])), dtype=np.int64)
+        nat.call("csrk_bandk_result_get", out, nat.i64p(fwd), nat.i64p(s1), nat.i64p(s2))
+    finally:
+        nat.lib().csrk_bandk_result_free(out)
+    return fwd, s1, s2[: int(sizes[2])]
+
+
+def test_device_band_k_bit_exact_on_golden(golden):
+    from conftest import BANDK_TAGS
+    for name in golden.names:
+        a = golden.csr(name)
+        for tag, k, targets in BANDK_TAGS:
+            fwd, s1, s2 = _device_band_k(a, k, targets)
+            np.testing.assert_array_equal(fwd, golden[f"{name}/{tag}/fwd"],
+                                          err_msg=f"{name} {tag}")
+            np.testing.assert_array_equal(s1, golden[f"{name}/{tag}/sizes0"])
+            if k == 3:
+                np.testing.assert_array_equal(s2, golden[f"{name}/{tag}/sizes1"])
+
+
+@pytest.mark.parametrize("name", ["grid2d_200", "grid3d7_32", "grid3d27_20", "irregular_200k",
+                                  "C1"])
+def test_device_band_k_digests(name, configs_golden):
+    import paper_2203_05096_b200 as ck
+    from conftest import digest
+    from paper_2203_05096_b200 import synthetic
+    rec = configs_golden[name]
+    spec = rec["spec"]
+    if spec["kind"] == "stencil":
+        n, rp, ci, va = synthetic.stencil_arrays(spec["shape"], spec["points"],
+                                                 values=spec.get("values", "laplacian"))
+        a = ck.CsrMatrix(n, n, rp, ci, va)
+    else:
+        r, c, v = synthetic.irregular_triplets(spec["rows"], seed=spec.get("seed", 0))
+        a = ck.csr_from_arrays(spec["rows"], spec["rows"], r, c, v)
+    for run in rec["runs"]:
+        fwd, s1, s2 = _device_band_k(a, 3, run["targets"])
+        assert digest(fwd, "<i8") == run["fwd"]
+        assert digest(s1, "<i8") == run["sizes0"]
+        assert digest(s2, "<i8") == run["sizes1"]
