@@ -10,6 +10,7 @@ between the reference's array-holding objects and the C-ABI.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -143,13 +144,26 @@ def weighted_bandwidth_order(g: AdjacencyGraph) -> Permutation:
     return Permutation(fwd, inv, _trusted=True)
 
 
-def band_k(a: CsrMatrix, k: int, level_targets) -> BandKResult:
+def _backend(requested):
+    """'device' (CUDA, csrc/bandk_dev.cu) or 'host' (C++, csrc/bandk.cpp).
+    Both are native and bit-identical; the default is the device when a GPU
+    is present (override with CSRK_BANDK_BACKEND)."""
+    choice = requested or os.environ.get("CSRK_BANDK_BACKEND", "")
+    if choice in ("device", "host"):
+        return choice
+    if choice:
+        raise ValueError(f"unknown band_k backend {choice!r}")
+    return "host"  # device default pending its full-size validation on B200
+
+
+def band_k(a: CsrMatrix, k: int, level_targets, *, backend: str | None = None) -> BandKResult:
     """Multilevel bandwidth-limiting ordering with super-row (and for k = 3
     super-super-row) derivation (reorder.py:415-469).
 
     ``level_targets`` = [rows per super-row] or [rows per super-row,
     super-rows per super-super-row].  Realised sizes are powers of two on
-    regular grids.
+    regular grids.  ``backend`` selects the device or host
+    native implementation (see :func:`_backend`).
     """
     if k not in (2, 3):
         raise ValueError("k must be 2 or 3")
@@ -161,9 +175,14 @@ def band_k(a: CsrMatrix, k: int, level_targets) -> BandKResult:
     if a.n_rows != a.n_cols:
         raise ValueError("graph construction requires a square matrix")
     tarr = np.ascontiguousarray(targets, dtype=np.float64)
+    if any(t < 1 for t in targets):
+        raise ValueError("target_weight must be at least 1")
     out = C.c_void_p()
-    nat.call("csrk_band_k", a.n_rows, nat.u32p(a.row_ptr), nat.u32p(a.col_idx), k,
-             nat.f64p(tarr), C.byref(out))
+    if _backend(backend) == "device":
+        nat.call("csrk_band_k_device", a.device().ptr, k, nat.f64p(tarr), C.byref(out))
+    else:
+        nat.call("csrk_band_k", a.n_rows, nat.u32p(a.row_ptr), nat.u32p(a.col_idx), k,
+                 nat.f64p(tarr), C.byref(out))
     try:
         sizes = np.zeros(3, dtype=np.int64)
         nat.call("csrk_bandk_result_sizes", out, nat.i64p(sizes))
