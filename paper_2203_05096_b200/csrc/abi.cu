@@ -441,10 +441,9 @@ int csrk_spmv_host(csrk_matrix *m, int value_type, int variant, int nx,
     CSRK_CUDA_TRY(cudaMalloc(&m->y_stage, yb));
     m->y_stage_bytes = yb;
   }
-  // ~256K rows per chunk keeps the pipeline fill (x needed by the first
-  // chunk's footprint) short; 4..64 chunks
-  int chunks = static_cast<int>(m->n_rows >> 18);
-  chunks = chunks < 4 ? 4 : (chunks > 64 ? 64 : chunks);
+  // 16 chunks: finer chunks shorten the pipeline fill but each adds a launch
+  // and three stream operations (64 chunks measured slower on C2)
+  const int chunks = 16;
   const bool pipelined = m->n_rows == m->n_cols && m->n_rows >= (1 << 20) &&
                          m->plan.n_tiles >= 4 * chunks && is_pinned(x_host) &&
                          is_pinned(y_host);

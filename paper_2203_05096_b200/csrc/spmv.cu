@@ -468,11 +468,26 @@ int launch_stream(const csrk_matrix *m, const V *vals, const V *x, V *y,
                      static_cast<uint32_t>(pl.stages), sizeof(V));
   const size_t smem = geo.total_bytes();
   auto kern = csrk_stream_kernel<V, NX>;
-  CSRK_CUDA_TRY(cudaFuncSetAttribute(
-      kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  // attribute + occupancy queries cost host time per launch; cache them per
+  // instantiation and shared-memory size (the chunked host pipeline launches
+  // the kernel many times per SpMV)
+  static thread_local size_t cached_smem = 0;
+  static thread_local int cached_per_sm = 0;
+  static thread_local int cached_device = -1;
+  int cur_dev = 0;
+  CSRK_CUDA_TRY(cudaGetDevice(&cur_dev));
   int per_sm = 0;
-  CSRK_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads,
-                                                              smem));
+  if (cached_smem == smem && cached_device == cur_dev) {
+    per_sm = cached_per_sm;
+  } else {
+    CSRK_CUDA_TRY(cudaFuncSetAttribute(
+        kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    CSRK_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads,
+                                                                smem));
+    cached_smem = smem;
+    cached_per_sm = per_sm;
+    cached_device = cur_dev;
+  }
   if (per_sm < 1) {
     set_error("stream kernel does not fit on an SM (%zu bytes of shared memory)", smem);
     return CSRK_EINVAL;
@@ -538,7 +553,7 @@ int ensure_plan(csrk_matrix *m, int64_t tile_cost, int64_t cap, int64_t stages,
   if (cap < 16) cap = 16;
   if (stages <= 0) stages = kDefaultStages;
   if (stages > 8) stages = 8;
-  const int64_t rcap = tile_cost;
+  const int64_t rcap = cap;
   const Geometry geo(static_cast<uint32_t>(cap), static_cast<uint32_t>(rcap),
                      static_cast<uint32_t>(stages), sizeof(double));
   if (geo.total_bytes() > 227 * 1024) {
@@ -559,6 +574,7 @@ int ensure_plan(csrk_matrix *m, int64_t tile_cost, int64_t cap, int64_t stages,
   // cut on group boundaries when every group is small against a tile
   int cut_k = 1;
   int64_t n_cuts = m->n_rows;
+  int64_t max_group = 0;
   if (m->k >= 2 && n_groups > 0) {
     unsigned long long *d = nullptr, h = 0;
     CSRK_CUDA_TRY(cudaMallocAsync(&d, sizeof(h), s));
@@ -574,10 +590,17 @@ int ensure_plan(csrk_matrix *m, int64_t tile_cost, int64_t cap, int64_t stages,
     if (static_cast<int64_t>(h) * 2 <= tile_cost) {
       cut_k = m->k;
       n_cuts = n_groups;
+      max_group = static_cast<int64_t>(h);
     }
   }
+  // A tile runs from the first cut at or past t * pitch to the first cut at
+  // or past (t + 1) * pitch, so it costs less than pitch + (largest group).
+  // Group cuts use pitch = tile_cost - largest group: every tile then fits
+  // the stage.  Row cuts keep pitch = tile_cost; the stage's slack
+  // (cap - tile_cost) covers the row that crosses a boundary.
+  const int64_t pitch = cut_k == 1 ? tile_cost : tile_cost - max_group;
   const int64_t total_cost = m->nnz + m->n_rows;
-  const int64_t n_tiles = (total_cost + tile_cost - 1) / tile_cost;
+  const int64_t n_tiles = (total_cost + pitch - 1) / pitch;
   if (n_tiles > 0x7fffffffLL) {
     set_error("too many tiles (%lld)", static_cast<long long>(n_tiles));
     return CSRK_EINVAL;
@@ -589,7 +612,7 @@ int ensure_plan(csrk_matrix *m, int64_t tile_cost, int64_t cap, int64_t stages,
   CSRK_CUDA_TRY(cudaMalloc(&m->plan.tile_row, (n_tiles + 1) * sizeof(uint32_t)));
   const int64_t blocks = (n_tiles + 1 + 255) / 256;
   tile_bounds_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(
-      m->row_ptr, m->sr_ptr, m->ssr_ptr, cut_k, n_cuts, m->n_rows, tile_cost,
+      m->row_ptr, m->sr_ptr, m->ssr_ptr, cut_k, n_cuts, m->n_rows, pitch,
       n_tiles, m->plan.tile_row);
   CSRK_CUDA_TRY(cudaGetLastError());
   m->plan.tile_cost = tile_cost;
