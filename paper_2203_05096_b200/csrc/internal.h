@@ -18,7 +18,7 @@ void set_error(const char *fmt, ...);
 // A tile plan of the streaming kernel: tile t covers rows
 // [tile_row[t], tile_row[t+1]) made of whole groups.
 constexpr int64_t kDefaultTileCost = 2048;  // nonzeros + rows per tile
-constexpr int64_t kDefaultStages = 3;       // TMA ring depth per CTA
+constexpr int64_t kDefaultStages = 2;       // TMA ring depth per CTA (plan sweep)
 
 struct TilePlan {
   int64_t tile_cost = 0;  // requested nonzeros + rows per tile

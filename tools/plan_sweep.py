@@ -20,8 +20,8 @@ import bench  # noqa: E402
 import paper_2203_05096_b200 as ck  # noqa: E402
 from paper_2203_05096_b200.bench import spmv_bytes  # noqa: E402
 
-TILES = (1024, 1536, 2048, 3072, 4096, 6144)
-STAGES = (2, 3, 4)
+TILES = tuple(int(t) for t in os.environ.get('SWEEP_TILES', '1024,1280,1536,1792,2048,2560,3072').split(','))
+STAGES = tuple(int(t) for t in os.environ.get('SWEEP_STAGES', '2,3').split(','))
 
 
 def median_ms(fn, reps=20):
