@@ -15,7 +15,10 @@
 // until no position changes -- the unique fixed point is the sequential
 // result because a block only reads positions of earlier blocks.
 
+#include <chrono>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "internal.h"
@@ -310,6 +313,20 @@ int expand_level_dev(const csrk_dgraph *g, const Level &lv, const int64_t *seq_c
 
 }  // namespace
 
+// CSRK_BANDK_PROFILE=1: per-phase wall time of the device Band-k
+struct DevPhase {
+  const char *name;
+  std::chrono::steady_clock::time_point t0;
+  cudaStream_t s;
+  DevPhase(const char *n, cudaStream_t st) : name(n), t0(std::chrono::steady_clock::now()), s(st) {}
+  ~DevPhase() {
+    if (!std::getenv("CSRK_BANDK_PROFILE")) return;
+    cudaStreamSynchronize(s);
+    std::fprintf(stderr, "[band_k dev] %-12s %8.3f s\n", name,
+                 std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
+  }
+};
+
 int band_k_dev(const csrk_matrix *a, int k, const double *targets, csrk_bandk_result &res,
                int64_t *fwd_dev_out, cudaStream_t s) {
   const int64_t n = a->n_rows;
@@ -328,7 +345,8 @@ int band_k_dev(const csrk_matrix *a, int k, const double *targets, csrk_bandk_re
   csrk_dgraph *g0 = nullptr;
   int64_t *base = nullptr, *base_inv = nullptr;
   do {
-    if ((rc = graph_build_dev(a, &g0)) != CSRK_OK) break;
+    { DevPhase ph("build", s); rc = graph_build_dev(a, &g0); }
+    if (rc != CSRK_OK) break;
     if (cudaMalloc(&base, n * sizeof(int64_t)) != cudaSuccess ||
         cudaMalloc(&base_inv, n * sizeof(int64_t)) != cudaSuccess) {
       rc = CSRK_ENOMEM;
@@ -336,7 +354,8 @@ int band_k_dev(const csrk_matrix *a, int k, const double *targets, csrk_bandk_re
     }
     tofree.push_back(base);
     tofree.push_back(base_inv);
-    if ((rc = graph_wbo_dev(g0, base, s)) != CSRK_OK) break;
+    { DevPhase ph("wbo-base", s); rc = graph_wbo_dev(g0, base, s); }
+    if (rc != CSRK_OK) break;
     inv64_kernel<<<nbk(n), 256, 0, s>>>(base, n, base_inv);
     csrk_dgraph *g0r = nullptr;
     if ((rc = graph_relabel_dev(g0, base, base_inv, s, &g0r)) != CSRK_OK) break;
@@ -352,7 +371,8 @@ int band_k_dev(const csrk_matrix *a, int k, const double *targets, csrk_bandk_re
       }
       tofree.push_back(reinterpret_cast<int64_t *>(f2c));
       csrk_dgraph *coarse = nullptr;
-      if ((rc = graph_coarsen_dev(fine, targets[t], f2c, &coarse, s)) != CSRK_OK) break;
+      { DevPhase ph("coarsen", s); rc = graph_coarsen_dev(fine, targets[t], f2c, &coarse, s); }
+      if (rc != CSRK_OK) break;
       const int64_t m = coarse->n;
       int64_t *ord = nullptr, *ord_inv = nullptr;
       if (cudaMalloc(&ord, (m > 0 ? m : 1) * sizeof(int64_t)) != cudaSuccess ||
@@ -400,7 +420,8 @@ int band_k_dev(const csrk_matrix *a, int k, const double *targets, csrk_bandk_re
         break;
       }
       std::vector<int64_t> sizes;
-      rc = expand_level_dev(fine, levels[level - 1], seq, fine_seq, sizes, nullptr, s);
+      { DevPhase ph("expand", s);
+        rc = expand_level_dev(fine, levels[level - 1], seq, fine_seq, sizes, nullptr, s); }
       cudaFree(seq);
       seq = fine_seq;
       collected.push_back(std::move(sizes));

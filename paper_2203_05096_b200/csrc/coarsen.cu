@@ -16,6 +16,8 @@
 // coarse weight reaches the target or a round shrinks by less than 5%.
 
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "internal.h"
@@ -224,7 +226,11 @@ int graph_coarsen_dev(const csrk_dgraph *g, double target, int32_t *f2c, csrk_dg
     if (match.alloc(n) != cudaSuccess || new_id.alloc(n) != cudaSuccess ||
         flag.alloc(n) != cudaSuccess || pos.alloc(n + 1) != cudaSuccess)
       return CSRK_ENOMEM;
-    rc = graph_match_dev(cur_g(), match.p, nullptr, s);
+    int sweeps = 0;
+    rc = graph_match_dev(cur_g(), match.p, &sweeps, s);
+    if (std::getenv("CSRK_BANDK_PROFILE"))
+      std::fprintf(stderr, "[band_k dev]   matching n=%lld sweeps=%d\n",
+                   static_cast<long long>(n), sweeps);
     if (rc != CSRK_OK) break;
     rep_flag_kernel<<<nb(n), 256, 0, s>>>(match.p, n, flag.p);
     rc = exclusive_scan_i64(flag.p, n, pos.p, s);

@@ -19,6 +19,8 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "internal.h"
@@ -420,6 +422,9 @@ int graph_wbo_dev(const csrk_dgraph *g, int64_t *fwd_dev, cudaStream_t s) {
     cm_count_kernel<<<nblocks(cnt), 256, 0, s>>>(vals.p, cnt, label.p, qlen.p);
     fsize = cnt;
   }
+  if (std::getenv("CSRK_BANDK_PROFILE"))
+    std::fprintf(stderr, "[band_k dev]   wbo n=%lld components=%d\n",
+                 static_cast<long long>(n), n_comp);
   final_fwd_kernel<<<nblocks(n), 256, 0, s>>>(pos.p, label.p, coff.p, n, fwd_dev);
   CSRK_CUDA_TRY(cudaGetLastError());
   CSRK_CUDA_TRY(cudaStreamSynchronize(s));

@@ -482,11 +482,9 @@ int launch_stream(const csrk_matrix *m, const V *vals, const V *x, V *y,
   } else {
     CSRK_CUDA_TRY(cudaFuncSetAttribute(
         kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    // all of the unified L1 / shared array as shared memory: the stage ring
-    // is the kernel's working set, x reuse is served by L2
-    CSRK_CUDA_TRY(cudaFuncSetAttribute(
-        kern, cudaFuncAttributePreferredSharedMemoryCarveout,
-        cudaSharedmemCarveoutMaxShared));
+    // (the carveout is left to the driver: it keeps the L1 share that the
+    // x gathers of irregular matrices depend on -- forcing max-shared cost
+    // C5 a third of its bandwidth in the plan sweep)
     CSRK_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads,
                                                                 smem));
     cached_smem = smem;
