@@ -86,10 +86,13 @@ __global__ void match_sweep_kernel(const int64_t *__restrict__ ptr,
   }
 }
 
-__global__ void diff_kernel(const uint64_t *__restrict__ a, const uint64_t *__restrict__ b,
-                            int64_t n, int *__restrict__ changed) {
+// compare the previous and new "taken by" arrays, then reset the previous
+// one to free so it can receive the next sweep's claims
+__global__ void diff_reset_kernel(uint64_t *__restrict__ a, const uint64_t *__restrict__ b,
+                                  int64_t n, int *__restrict__ changed) {
   GS(i, n) {
     if (a[i] != b[i]) *changed = 1;
+    a[i] = kFree;
   }
 }
 
@@ -176,22 +179,27 @@ int graph_match_dev(const csrk_dgraph *g, int32_t *match, int *iters, cudaStream
   CSRK_TRY(radix_sort_pairs(keys.p, vals.p, tkeys.p, tvals.p, n, 0, 32, s));
   vrank_kernel<<<nb(n), 256, 0, s>>>(vals.p, n, rank.p);
   fill_u64_kernel<<<nb(n), 256, 0, s>>>(ta.p, n, kFree);
+  fill_u64_kernel<<<nb(n), 256, 0, s>>>(tb.p, n, kFree);
+  // sweeps run in batches of 8 with one host check per batch: sweeps past
+  // the fixed point change nothing, and only the batch's last sweep decides
+  constexpr int kBatch = 8;
   int it = 0;
-  for (;; ++it) {
-    fill_u64_kernel<<<nb(n), 256, 0, s>>>(tb.p, n, kFree);
-    match_sweep_kernel<<<nb(n), 256, 0, s>>>(g->ptr, g->idx, g->ew, rank.p, n, ta.p, tb.p,
-                                             choice.p);
+  for (;;) {
+    for (int j = 0; j < kBatch; ++j, ++it) {
+      match_sweep_kernel<<<nb(n), 256, 0, s>>>(g->ptr, g->idx, g->ew, rank.p, n, ta.p, tb.p,
+                                               choice.p);
+      if (j == kBatch - 1) CSRK_CUDA_TRY(cudaMemsetAsync(flag.p, 0, sizeof(int), s));
+      diff_reset_kernel<<<nb(n), 256, 0, s>>>(ta.p, tb.p, n, flag.p);
+      std::swap(ta.p, tb.p);
+    }
     int h = 0;
-    CSRK_CUDA_TRY(cudaMemsetAsync(flag.p, 0, sizeof(int), s));
-    diff_kernel<<<nb(n), 256, 0, s>>>(ta.p, tb.p, n, flag.p);
     CSRK_CUDA_TRY(cudaMemcpyAsync(&h, flag.p, sizeof(int), cudaMemcpyDeviceToHost, s));
     CSRK_CUDA_TRY(cudaStreamSynchronize(s));
-    std::swap(ta.p, tb.p);
     if (!h) break;
   }
   match_final_kernel<<<nb(n), 256, 0, s>>>(ta.p, choice.p, n, match);
   CSRK_CUDA_TRY(cudaGetLastError());
-  if (iters) *iters = it + 1;
+  if (iters) *iters = it;
   return CSRK_OK;
 }
 

@@ -276,11 +276,14 @@ int graph_wbo_dev(const csrk_dgraph *g, int64_t *fwd_dev, cudaStream_t s) {
 
   // 2. components (label = minimum index)
   label_init_kernel<<<nblocks(n), 256, 0, s>>>(label.p, n);
+  // hook + jump rounds, checked every 4 rounds (extra rounds are no-ops)
   for (int it = 0;; ++it) {
     int h = 0;
-    CSRK_CUDA_TRY(cudaMemsetAsync(counter.p, 0, sizeof(int), s));
-    label_hook_kernel<<<nblocks(n), 256, 0, s>>>(g->ptr, g->idx, n, label.p, counter.p);
-    label_jump_kernel<<<nblocks(n), 256, 0, s>>>(label.p, n);
+    for (int j = 0; j < 4; ++j) {
+      if (j == 3) CSRK_CUDA_TRY(cudaMemsetAsync(counter.p, 0, sizeof(int), s));
+      label_hook_kernel<<<nblocks(n), 256, 0, s>>>(g->ptr, g->idx, n, label.p, counter.p);
+      label_jump_kernel<<<nblocks(n), 256, 0, s>>>(label.p, n);
+    }
     CSRK_CUDA_TRY(cudaMemcpyAsync(&h, counter.p, sizeof(int), cudaMemcpyDeviceToHost, s));
     CSRK_CUDA_TRY(cudaStreamSynchronize(s));
     if (!h) break;
