@@ -1,10 +1,18 @@
 """Band-k reordering and super-row derivation, native.
 
 Drop-in for the reference's ``csrk.reorder`` (pkg/src/csrk/reorder.py).  All
-graph work runs in libcsrk_cuda.so (csrc/bandk.cpp), a C++ restatement that
-reproduces every greedy tie-break of the reference, so permutations and group
-sizes are bit-exact (pinned by tests/golden).  The Python layer only converts
-between the reference's array-holding objects and the C-ABI.
+graph work runs in libcsrk_cuda.so, in two bit-identical implementations that
+reproduce every greedy tie-break of the reference (pinned by tests/golden,
+including the full-size C2 / C3 / C5 digests):
+
+  device  csrc/{graph,rcm,coarsen,bandk_dev}.cu -- radix-sort graph building,
+          level-synchronous exact Cuthill-McKee, Jacobi fixed-point matching
+          and block expansion (the default when a GPU is present);
+  host    csrc/bandk.cpp -- the sequential restatement (OpenMP where rows are
+          independent), used without a GPU and for the graph-level helpers.
+
+The Python layer only converts between the reference's array-holding objects
+and the C-ABI.
 """
 
 from __future__ import annotations
@@ -153,7 +161,7 @@ def _backend(requested):
         return choice
     if choice:
         raise ValueError(f"unknown band_k backend {choice!r}")
-    return "host"  # device default pending its full-size validation on B200
+    return "device" if nat.device_count() > 0 else "host"
 
 
 def band_k(a: CsrMatrix, k: int, level_targets, *, backend: str | None = None) -> BandKResult:
