@@ -225,6 +225,87 @@ __global__ void final_fwd_kernel(const int32_t *__restrict__ pos,
   GSTRIDE(v, n) { fwd[v] = n - 1 - (coff[label[v]] + pos[v]); }
 }
 
+
+// ---- per-component state on the device ----------------------------------
+
+// component rank of every root and the components' first queue offsets
+__global__ void comp_layout_kernel(const uint32_t *__restrict__ roots, int64_t n_comp,
+                                   const int32_t *__restrict__ size,
+                                   const int64_t *__restrict__ size_off,
+                                   int32_t *__restrict__ crank, int64_t *__restrict__ coff) {
+  GSTRIDE(c, n_comp) {
+    const uint32_t r = roots[c];
+    crank[r] = static_cast<int32_t>(c);
+    coff[r] = size_off[c];
+  }
+}
+
+__global__ void comp_sizes_kernel(const uint32_t *__restrict__ roots, int64_t n_comp,
+                                  const int32_t *__restrict__ size, int64_t *__restrict__ out) {
+  GSTRIDE(c, n_comp) { out[c] = size[roots[c]]; }
+}
+
+// pseudo-peripheral state: start = min-key node; best_ecc = -1; active
+__global__ void pp_init_kernel(const uint32_t *__restrict__ roots, int64_t n_comp,
+                               const uint32_t *__restrict__ minrank,
+                               const uint32_t *__restrict__ by_key,
+                               int32_t *__restrict__ start, int32_t *__restrict__ best_node,
+                               int32_t *__restrict__ best_ecc, int8_t *__restrict__ active) {
+  GSTRIDE(c, n_comp) {
+    start[c] = static_cast<int32_t>(by_key[minrank[roots[c]]]);
+    best_node[c] = -1;
+    best_ecc[c] = -1;
+    active[c] = 1;
+  }
+}
+
+// seeds of the next BFS: starts of the still-active components
+__global__ void pp_seeds_kernel(const int32_t *__restrict__ start,
+                                const int8_t *__restrict__ active, int64_t n_comp,
+                                int32_t *__restrict__ seeds, int *__restrict__ count) {
+  GSTRIDE(c, n_comp) {
+    if (active[c]) seeds[atomicAdd(count, 1)] = start[c];
+  }
+}
+
+// reorder.py:270-278 for every active component after its BFS
+__global__ void pp_update_kernel(const uint32_t *__restrict__ roots, int64_t n_comp,
+                                 const int32_t *__restrict__ ecc,
+                                 const uint32_t *__restrict__ lastmin,
+                                 const uint32_t *__restrict__ by_key,
+                                 int32_t *__restrict__ start, int32_t *__restrict__ best_node,
+                                 int32_t *__restrict__ best_ecc, int8_t *__restrict__ active,
+                                 int *__restrict__ still_active) {
+  GSTRIDE(c, n_comp) {
+    if (!active[c]) continue;
+    const uint32_t r = roots[c];
+    const int32_t e = ecc[r];
+    if (e <= best_ecc[c]) {
+      active[c] = 0;
+      continue;
+    }
+    best_ecc[c] = e;
+    best_node[c] = start[c];
+    start[c] = static_cast<int32_t>(by_key[lastmin[r]]);
+    if (start[c] == best_node[c]) {
+      active[c] = 0;
+      continue;
+    }
+    atomicAdd(still_active, 1);
+  }
+}
+
+// Cuthill-McKee level 0: every component's start at queue position 0
+__global__ void cm_init_kernel(const uint32_t *__restrict__ roots, int64_t n_comp,
+                               const int32_t *__restrict__ best_node, int32_t *__restrict__ pos,
+                               int32_t *__restrict__ qlen, int32_t *__restrict__ frontier) {
+  GSTRIDE(c, n_comp) {
+    pos[best_node[c]] = 0;
+    qlen[roots[c]] = 1;
+    frontier[c] = best_node[c];
+  }
+}
+
 template <typename T>
 struct DBuf {
   T *p = nullptr;
@@ -244,15 +325,18 @@ int graph_wbo_dev(const csrk_dgraph *g, int64_t *fwd_dev, cudaStream_t s) {
   const int64_t n = g->n;
   if (n == 0) return CSRK_OK;
   DBuf<uint64_t> keys, tkeys;
-  DBuf<uint32_t> vals, tvals, krank, claim, lastmin, minrank;
+  DBuf<uint32_t> vals, tvals, krank, by_key, claim, lastmin, minrank;
   DBuf<int32_t> label, size, depth, frontier, next, pos, inq, ecc, crank, qlen;
+  DBuf<int32_t> start, best_node, best_ecc;
+  DBuf<int8_t> active;
   DBuf<int> counter;
-  DBuf<int64_t> coff;
+  DBuf<int64_t> coff, csize, csize_off;
   CSRK_CUDA_TRY(keys.alloc(n));
   CSRK_CUDA_TRY(tkeys.alloc(n));
   CSRK_CUDA_TRY(vals.alloc(n));
   CSRK_CUDA_TRY(tvals.alloc(n));
   CSRK_CUDA_TRY(krank.alloc(n));
+  CSRK_CUDA_TRY(by_key.alloc(n));
   CSRK_CUDA_TRY(claim.alloc(n));
   CSRK_CUDA_TRY(lastmin.alloc(n));
   CSRK_CUDA_TRY(minrank.alloc(n));
@@ -269,15 +353,15 @@ int graph_wbo_dev(const csrk_dgraph *g, int64_t *fwd_dev, cudaStream_t s) {
   CSRK_CUDA_TRY(counter.alloc(4));
   CSRK_CUDA_TRY(coff.alloc(n + 1));
 
-  // 1. key ranks: stable sort of (degree, weight) keeps index order on ties
-  key_kernel<<<nblocks(n), 256, 0, s>>>(g->ptr, g->nw, n, keys.p, vals.p);
-  CSRK_TRY(radix_sort_pairs(keys.p, vals.p, tkeys.p, tvals.p, n, 0, 64, s));
-  rank_kernel<<<nblocks(n), 256, 0, s>>>(vals.p, n, krank.p);
+  // 1. key ranks: stable sort of (degree, weight) keeps index order on ties;
+  //    by_key[rank] = node
+  key_kernel<<<nblocks(n), 256, 0, s>>>(g->ptr, g->nw, n, keys.p, by_key.p);
+  CSRK_TRY(radix_sort_pairs(keys.p, by_key.p, tkeys.p, tvals.p, n, 0, 64, s));
+  rank_kernel<<<nblocks(n), 256, 0, s>>>(by_key.p, n, krank.p);
 
-  // 2. components (label = minimum index)
+  // 2. components (label = minimum index), hook + jump rounds checked every 4
   label_init_kernel<<<nblocks(n), 256, 0, s>>>(label.p, n);
-  // hook + jump rounds, checked every 4 rounds (extra rounds are no-ops)
-  for (int it = 0;; ++it) {
+  for (;;) {
     int h = 0;
     for (int j = 0; j < 4; ++j) {
       if (j == 3) CSRK_CUDA_TRY(cudaMemsetAsync(counter.p, 0, sizeof(int), s));
@@ -296,53 +380,33 @@ int graph_wbo_dev(const csrk_dgraph *g, int64_t *fwd_dev, cudaStream_t s) {
   int n_comp = 0;
   CSRK_CUDA_TRY(cudaMemcpyAsync(&n_comp, counter.p, sizeof(int), cudaMemcpyDeviceToHost, s));
   CSRK_CUDA_TRY(cudaStreamSynchronize(s));
+  // roots in component order (-size, root); vals keeps them
   CSRK_TRY(radix_sort_pairs(keys.p, vals.p, tkeys.p, tvals.p, n_comp, 0, 64, s));
-  // host side: the (few or many) roots in component order
-  std::vector<uint32_t> roots(n_comp);
-  CSRK_CUDA_TRY(cudaMemcpyAsync(roots.data(), vals.p, n_comp * sizeof(uint32_t),
-                                cudaMemcpyDeviceToHost, s));
-  std::vector<int32_t> h_size(n);
-  CSRK_CUDA_TRY(cudaMemcpyAsync(h_size.data(), size.p, n * sizeof(int32_t),
-                                cudaMemcpyDeviceToHost, s));
-  std::vector<uint32_t> h_minrank(n), h_sorted(n);
-  CSRK_CUDA_TRY(cudaMemcpyAsync(h_minrank.data(), minrank.p, n * sizeof(uint32_t),
-                                cudaMemcpyDeviceToHost, s));
-  CSRK_CUDA_TRY(cudaStreamSynchronize(s));
-  // node of each key rank
-  std::vector<uint32_t> h_krank(n);
-  CSRK_CUDA_TRY(cudaMemcpy(h_krank.data(), krank.p, n * sizeof(uint32_t),
-                           cudaMemcpyDeviceToHost));
-  for (int64_t v = 0; v < n; ++v) h_sorted[h_krank[v]] = static_cast<uint32_t>(v);
-  std::vector<int32_t> h_crank(n, -1);
-  std::vector<int64_t> h_coff(n + 1, 0);
-  for (int c = 0; c < n_comp; ++c) h_crank[roots[c]] = c;
-  {
-    int64_t acc = 0;
-    for (int c = 0; c < n_comp; ++c) {
-      h_coff[roots[c]] = acc;
-      acc += h_size[roots[c]];
-    }
-  }
-  CSRK_CUDA_TRY(cudaMemcpyAsync(crank.p, h_crank.data(), n * sizeof(int32_t),
-                                cudaMemcpyHostToDevice, s));
-  CSRK_CUDA_TRY(cudaMemcpyAsync(coff.p, h_coff.data(), (n + 1) * sizeof(int64_t),
-                                cudaMemcpyHostToDevice, s));
+  const uint32_t *roots = vals.p;
+  CSRK_CUDA_TRY(csize.alloc(n_comp));
+  CSRK_CUDA_TRY(csize_off.alloc(n_comp + 1));
+  CSRK_CUDA_TRY(start.alloc(n_comp));
+  CSRK_CUDA_TRY(best_node.alloc(n_comp));
+  CSRK_CUDA_TRY(best_ecc.alloc(n_comp));
+  CSRK_CUDA_TRY(active.alloc(n_comp));
+  comp_sizes_kernel<<<nblocks(n_comp), 256, 0, s>>>(roots, n_comp, size.p, csize.p);
+  CSRK_TRY(exclusive_scan_i64(csize.p, n_comp, csize_off.p, s));
+  comp_layout_kernel<<<nblocks(n_comp), 256, 0, s>>>(roots, n_comp, size.p, csize_off.p,
+                                                     crank.p, coff.p);
 
-  // 3. pseudo-peripheral start of every component (reorder.py:263-278)
-  std::vector<int32_t> start(n_comp), best_node(n_comp, -1), best_ecc(n_comp, -1);
-  std::vector<char> active(n_comp, 1);
-  for (int c = 0; c < n_comp; ++c) start[c] = static_cast<int32_t>(h_sorted[h_minrank[roots[c]]]);
-  std::vector<int32_t> h_ecc(n), seeds;
-  std::vector<uint32_t> h_last(n);
-  int n_active = n_comp;
+  // 3. pseudo-peripheral start of every component (reorder.py:263-278),
+  //    all components' BFS runs together, state stays on the device
+  pp_init_kernel<<<nblocks(n_comp), 256, 0, s>>>(roots, n_comp, minrank.p, by_key.p, start.p,
+                                                 best_node.p, best_ecc.p, active.p);
+  int64_t n_active = n_comp;
   while (n_active > 0) {
-    seeds.clear();
-    for (int c = 0; c < n_comp; ++c)
-      if (active[c]) seeds.push_back(start[c]);
-    const int64_t k = static_cast<int64_t>(seeds.size());
+    int k = 0;
+    CSRK_CUDA_TRY(cudaMemsetAsync(counter.p, 0, sizeof(int), s));
+    pp_seeds_kernel<<<nblocks(n_comp), 256, 0, s>>>(start.p, active.p, n_comp, next.p,
+                                                    counter.p);
+    CSRK_CUDA_TRY(cudaMemcpyAsync(&k, counter.p, sizeof(int), cudaMemcpyDeviceToHost, s));
     CSRK_CUDA_TRY(cudaMemsetAsync(depth.p, 0xff, n * sizeof(int32_t), s));
-    CSRK_CUDA_TRY(cudaMemcpyAsync(next.p, seeds.data(), k * sizeof(int32_t),
-                                  cudaMemcpyHostToDevice, s));
+    CSRK_CUDA_TRY(cudaStreamSynchronize(s));
     bfs_seed_kernel<<<nblocks(k), 256, 0, s>>>(next.p, k, depth.p, frontier.p);
     int64_t fsize = k;
     for (int32_t level = 0; fsize > 0; ++level) {
@@ -360,48 +424,24 @@ int graph_wbo_dev(const csrk_dgraph *g, int64_t *fwd_dev, cudaStream_t s) {
     CSRK_CUDA_TRY(cudaMemsetAsync(lastmin.p, 0xff, n * sizeof(uint32_t), s));
     last_level_kernel<<<nblocks(n), 256, 0, s>>>(depth.p, label.p, ecc.p, krank.p, n,
                                                  lastmin.p);
-    CSRK_CUDA_TRY(cudaMemcpyAsync(h_ecc.data(), ecc.p, n * sizeof(int32_t),
-                                  cudaMemcpyDeviceToHost, s));
-    CSRK_CUDA_TRY(cudaMemcpyAsync(h_last.data(), lastmin.p, n * sizeof(uint32_t),
-                                  cudaMemcpyDeviceToHost, s));
+    int still = 0;
+    CSRK_CUDA_TRY(cudaMemsetAsync(counter.p, 0, sizeof(int), s));
+    pp_update_kernel<<<nblocks(n_comp), 256, 0, s>>>(roots, n_comp, ecc.p, lastmin.p, by_key.p,
+                                                     start.p, best_node.p, best_ecc.p,
+                                                     active.p, counter.p);
+    CSRK_CUDA_TRY(cudaMemcpyAsync(&still, counter.p, sizeof(int), cudaMemcpyDeviceToHost, s));
     CSRK_CUDA_TRY(cudaStreamSynchronize(s));
-    for (int c = 0; c < n_comp; ++c) {
-      if (!active[c]) continue;
-      const int32_t r = static_cast<int32_t>(roots[c]);
-      const int32_t e = h_ecc[r];
-      if (e <= best_ecc[c]) {
-        active[c] = 0;
-        --n_active;
-        continue;
-      }
-      best_ecc[c] = e;
-      best_node[c] = start[c];
-      start[c] = static_cast<int32_t>(h_sorted[h_last[r]]);
-      if (start[c] == best_node[c]) {
-        active[c] = 0;
-        --n_active;
-      }
-    }
+    n_active = still;
   }
 
   // 4. Cuthill-McKee queues, all components level by level
   CSRK_CUDA_TRY(cudaMemsetAsync(claim.p, 0xff, n * sizeof(uint32_t), s));
   CSRK_CUDA_TRY(cudaMemsetAsync(inq.p, 0, n * sizeof(int32_t), s));
-  {
-    // level 0: each component's start at position 0, queue length 1
-    std::vector<int32_t> h_pos(n, kNone), h_qlen(n, 0);
-    for (int c = 0; c < n_comp; ++c) {
-      h_pos[best_node[c]] = 0;
-      h_qlen[roots[c]] = 1;
-    }
-    CSRK_CUDA_TRY(cudaMemcpyAsync(frontier.p, best_node.data(), n_comp * sizeof(int32_t),
-                                  cudaMemcpyHostToDevice, s));
-    CSRK_CUDA_TRY(cudaMemcpyAsync(pos.p, h_pos.data(), n * sizeof(int32_t),
-                                  cudaMemcpyHostToDevice, s));
-    CSRK_CUDA_TRY(cudaMemcpyAsync(qlen.p, h_qlen.data(), n * sizeof(int32_t),
-                                  cudaMemcpyHostToDevice, s));
-    CSRK_CUDA_TRY(cudaStreamSynchronize(s));
-  }
+  CSRK_CUDA_TRY(cudaMemsetAsync(pos.p, 0xff, n * sizeof(int32_t), s));
+  CSRK_CUDA_TRY(cudaMemsetAsync(qlen.p, 0, n * sizeof(int32_t), s));
+  cm_init_kernel<<<nblocks(n_comp), 256, 0, s>>>(roots, n_comp, best_node.p, pos.p, qlen.p,
+                                                 frontier.p);
+  // (the level sorts below reuse keys / vals; roots are not needed past here)
   const int kbits = bits_for(n);
   int64_t fsize = n_comp;
   while (fsize > 0) {
