@@ -1,6 +1,7 @@
 // extern "C" entry points of libcsrk_cuda.so (declared in include/csrk.h).
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -450,6 +451,21 @@ int csrk_spmv_host(csrk_matrix *m, int value_type, int variant, int nx,
   if (pipelined) {
     CSRK_TRY(ensure_pipe(m, chunks));
     auto &pp = m->pipe;
+    const bool trace = std::getenv("CSRK_PIPE_TRACE") != nullptr;
+    std::vector<cudaEvent_t> tr;
+    cudaEvent_t tr0 = nullptr;
+    if (trace) {
+      tr.resize(3 * chunks);
+      for (auto &e : tr) cudaEventCreate(&e);
+      cudaEventCreate(&tr0);
+      cudaEventRecord(tr0, pp.h2d);
+      pp.ev_x_t.assign(chunks, nullptr);
+      pp.ev_c_t.assign(chunks, nullptr);
+      for (int c = 0; c < chunks; ++c) {
+        pp.ev_x_t[c] = tr[3 * c];
+        pp.ev_c_t[c] = tr[3 * c + 1];
+      }
+    }
     char *xs = static_cast<char *>(m->x_stage);
     char *ys = static_cast<char *>(m->y_stage);
     const char *xh = static_cast<const char *>(x_host);
@@ -460,6 +476,7 @@ int csrk_spmv_host(csrk_matrix *m, int value_type, int variant, int nx,
         CSRK_CUDA_TRY(cudaMemcpyAsync(xs + off, xh + off, len, cudaMemcpyHostToDevice,
                                       pp.h2d));
       CSRK_CUDA_TRY(cudaEventRecord(pp.ev_x[c], pp.h2d));
+      if (trace) CSRK_CUDA_TRY(cudaEventRecord(pp.ev_x_t[c], pp.h2d));
     }
     CSRK_CUDA_TRY(cudaEventRecord(m->ev0, pp.comp));
     for (int c = 0; c < chunks; ++c) {
@@ -467,6 +484,7 @@ int csrk_spmv_host(csrk_matrix *m, int value_type, int variant, int nx,
       CSRK_TRY(launch_spmv(m, value_type, variant, nx, m->x_stage, m->y_stage, pp.comp,
                            pp.tile_cut[c], pp.tile_cut[c + 1]));
       CSRK_CUDA_TRY(cudaEventRecord(pp.ev_c[c], pp.comp));
+      if (trace) CSRK_CUDA_TRY(cudaEventRecord(pp.ev_c_t[c], pp.comp));
       const size_t off = pp.row_cut[c] * es, len = (pp.row_cut[c + 1] - pp.row_cut[c]) * es;
       CSRK_CUDA_TRY(cudaStreamWaitEvent(pp.d2h, pp.ev_c[c], 0));
       if (len)
@@ -474,8 +492,30 @@ int csrk_spmv_host(csrk_matrix *m, int value_type, int variant, int nx,
                                       pp.d2h));
     }
     CSRK_CUDA_TRY(cudaEventRecord(m->ev1, pp.comp));
+    if (trace) {
+      for (int c = 0; c < chunks; ++c) {
+        CSRK_CUDA_TRY(cudaEventRecord(tr[3 * c + 2], pp.d2h));
+      }
+    }
     CSRK_CUDA_TRY(cudaStreamSynchronize(pp.d2h));
     CSRK_CUDA_TRY(cudaStreamSynchronize(pp.comp));
+    if (trace) {
+      // CSRK_PIPE_TRACE=1: per-chunk completion times (ms after the first
+      // H2D was enqueued) of H2D / kernel, and the D2H stream's end
+      float t_end = 0.f;
+      cudaEventElapsedTime(&t_end, tr0, tr[3 * (chunks - 1) + 2]);
+      for (int c = 0; c < chunks; ++c) {
+        float th = 0.f, tk = 0.f;
+        cudaEventElapsedTime(&th, tr0, pp.ev_x_t[c]);
+        cudaEventElapsedTime(&tk, tr0, pp.ev_c_t[c]);
+        std::fprintf(stderr, "[pipe] chunk %2d rows %9lld x_ready %2d  h2d %.3f  kernel %.3f\n",
+                     c, static_cast<long long>(pp.row_cut[c + 1] - pp.row_cut[c]),
+                     pp.x_ready[c], th, tk);
+      }
+      std::fprintf(stderr, "[pipe] d2h done %.3f ms\n", t_end);
+      for (auto e : tr) cudaEventDestroy(e);
+      cudaEventDestroy(tr0);
+    }
     return CSRK_OK;
   }
   if (m->n_cols)

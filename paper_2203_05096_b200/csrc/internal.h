@@ -53,6 +53,7 @@ struct csrk_matrix {
     std::vector<int> x_ready;                // x chunk needed by chunk c
     cudaStream_t h2d = nullptr, comp = nullptr, d2h = nullptr;
     std::vector<cudaEvent_t> ev_x, ev_c;
+    std::vector<cudaEvent_t> ev_x_t, ev_c_t;  // timing events (trace only)
   } pipe;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
