@@ -107,6 +107,17 @@ class ClockSampler:
         self._stop.set()
         self._thread.join(timeout=10)
 
+    def load_until(self, step, sync, n=3, max_s=3.0):
+        """Keep the GPU under the timed workload (untimed) until the sampler
+        holds `n` samples, so a short timed region still has clock samples
+        taken under the same load right before and during it."""
+        have = len(self.samples)
+        t0 = time.perf_counter()
+        while len(self.samples) < have + n and time.perf_counter() - t0 < max_s:
+            for _ in range(8):
+                step()
+            sync()
+
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
@@ -202,6 +213,7 @@ def run_ours(args, log):
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     with ClockSampler(torch.cuda.current_device()) as clk:
+        clk.load_until(step, torch.cuda.synchronize)
         torch.cuda.synchronize()
         ev0.record(stream)
         for _ in range(args.steps):
@@ -328,6 +340,8 @@ def run_loop(args, log):
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(torch.cuda.current_device()) as clk:
+        clk.load_until(graph.replay, torch.cuda.synchronize, max_s=6.0)
+        torch.cuda.synchronize()
         ev0.record()
         for _ in range(args.steps):
             graph.replay()

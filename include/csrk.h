@@ -93,8 +93,14 @@ int csrk_matrix_add_f32(csrk_matrix *m);
  * stages = TMA ring depth per CTA.  0 = defaults. */
 int csrk_matrix_set_plan(csrk_matrix *m, int64_t tile_cost, int64_t cap,
                          int64_t stages);
-/* out = tile_cost, cap, rcap, stages, n_tiles, group_aligned */
-int csrk_matrix_plan(const csrk_matrix *m, int64_t out[6]);
+/* out = tile_cost, cap, rcap, stages, n_tiles, group_aligned, gather_first */
+int csrk_matrix_plan(const csrk_matrix *m, int64_t out[7]);
+/* x-gather schedule of the f64 streaming kernel (B200 tuning knob, no
+ * reference counterpart; results are bitwise identical either way):
+ * 0 = inline (each row gathers its x while summing), 1 = gather-first (a
+ * tile's x gathers are issued together, products staged in shared memory,
+ * then summed in the row's order) -- for irregular rows (C5). */
+int csrk_matrix_set_gather(csrk_matrix *m, int mode);
 
 /* ---- SpMV ------------------------------------------------------------------
  * y = A x on device-resident x / y (already in the permuted index space, as

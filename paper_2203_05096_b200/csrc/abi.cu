@@ -1,4 +1,5 @@
 // extern "C" entry points of libcsrk_cuda.so (declared in include/csrk.h).
+#include <algorithm>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -358,15 +359,44 @@ int csrk_spmv(const csrk_matrix *m, int value_type, int variant, int nx,
 // covering their column footprint have landed (Band-k keeps footprints
 // banded), and y chunk c goes down on a third stream -- both PCIe directions
 // busy at once.  Pageable buffers take the plain H2D -> kernel -> D2H path.
-static int ensure_pipe(csrk_matrix *m, int chunks) {
+// Chunk weights of the host pipeline (CSRK_PIPE_SHAPE): "uN" = N equal
+// chunks; "rM" (default r12) = ramps 1, 2, 4 | M chunks of 8 | 4, 2, 1.  Small
+// chunks at both ends shorten the fill (the first y chunk can go down while
+// most of x is still going up) and the drain (the last kernel + D2H).
+static std::vector<int> pipe_weights() {
+  const char *env = std::getenv("CSRK_PIPE_SHAPE");
+  std::string shape = env && *env ? env : "r12";
+  int v = std::atoi(shape.c_str() + 1);
+  std::vector<int> w;
+  if (shape[0] == 'u' && v >= 1 && v <= 256) {
+    w.assign(v, 1);
+  } else {
+    if (shape[0] != 'r' || v < 1 || v > 256) v = 12;
+    w = {1, 2, 4};
+    for (int i = 0; i < v; ++i) w.push_back(8);
+    w.insert(w.end(), {4, 2, 1});
+  }
+  return w;
+}
+
+static int ensure_pipe(csrk_matrix *m, const std::vector<int> &weights) {
   auto &pp = m->pipe;
-  if (pp.chunks == chunks && pp.plan_tiles == m->plan.n_tiles) return CSRK_OK;
+  const int chunks = static_cast<int>(weights.size());
+  const char *xc_env = std::getenv("CSRK_PIPE_XCUT");
+  const std::string xmode = xc_env ? xc_env : "";
+  if (pp.weights == weights && pp.plan_tiles == m->plan.n_tiles && pp.xmode == xmode)
+    return CSRK_OK;
+  pp.xmode = xmode;
   const int64_t nt = m->plan.n_tiles;
+  int64_t wsum = 0;
+  for (int w : weights) wsum += w;
   pp.tile_cut.assign(chunks + 1, 0);
   pp.row_cut.assign(chunks + 1, 0);
   std::vector<uint32_t> rc(chunks + 1);
+  int64_t wacc = 0;
   for (int c = 0; c <= chunks; ++c) {
-    pp.tile_cut[c] = nt * c / chunks;
+    pp.tile_cut[c] = nt * wacc / wsum;
+    if (c < chunks) wacc += weights[c];
     uint32_t r = 0;
     CSRK_CUDA_TRY(cudaMemcpy(&r, m->plan.tile_row + pp.tile_cut[c], sizeof(r),
                              cudaMemcpyDeviceToHost));
@@ -387,12 +417,26 @@ static int ensure_pipe(csrk_matrix *m, int chunks) {
   cudaFree(d_max);
   if (rc2 != CSRK_OK) return rc2;
   CSRK_CUDA_TRY(e);
+  // x chunk c ends at the column footprint of row chunk c, so kernel c
+  // waits for exactly x chunks 0..c (x cut on the row cuts instead made
+  // kernel c wait one or two chunks longer -- the band reaches past the cut)
+  const char *xc = std::getenv("CSRK_PIPE_XCUT");
+  const bool by_rows = xc && std::strcmp(xc, "rows") == 0;
+  pp.x_cut.assign(chunks + 1, 0);
   pp.x_ready.assign(chunks, 0);
   for (int c = 0; c < chunks; ++c) {
-    int j = 0;
-    while (j + 1 < chunks && pp.row_cut[j + 1] <= static_cast<int64_t>(mx[c])) ++j;
-    pp.x_ready[c] = j;
+    if (by_rows) {
+      pp.x_cut[c + 1] = pp.row_cut[c + 1];
+      int j = 0;
+      while (j + 1 < chunks && pp.row_cut[j + 1] <= static_cast<int64_t>(mx[c])) ++j;
+      pp.x_ready[c] = j;
+    } else {
+      int64_t e = std::max<int64_t>(pp.x_cut[c], static_cast<int64_t>(mx[c]) + 1);
+      pp.x_cut[c + 1] = std::min<int64_t>(e, m->n_cols);
+      pp.x_ready[c] = c;
+    }
   }
+  pp.x_cut[chunks] = m->n_cols;
   if (!pp.h2d) {
     CSRK_CUDA_TRY(cudaStreamCreateWithFlags(&pp.h2d, cudaStreamNonBlocking));
     CSRK_CUDA_TRY(cudaStreamCreateWithFlags(&pp.comp, cudaStreamNonBlocking));
@@ -407,6 +451,7 @@ static int ensure_pipe(csrk_matrix *m, int chunks) {
     CSRK_CUDA_TRY(cudaEventCreateWithFlags(&pp.ev_c[c], cudaEventDisableTiming));
   }
   pp.chunks = chunks;
+  pp.weights = weights;
   pp.plan_tiles = nt;
   return CSRK_OK;
 }
@@ -419,6 +464,7 @@ static bool is_pinned(const void *p) {
   }
   return attr.type == cudaMemoryTypeHost;
 }
+
 
 int csrk_spmv_host(csrk_matrix *m, int value_type, int variant, int nx,
                    const void *x_host, void *y_host) {
@@ -442,14 +488,17 @@ int csrk_spmv_host(csrk_matrix *m, int value_type, int variant, int nx,
     CSRK_CUDA_TRY(cudaMalloc(&m->y_stage, yb));
     m->y_stage_bytes = yb;
   }
-  // 16 chunks: finer chunks shorten the pipeline fill but each adds a launch
-  // and three stream operations (64 chunks measured slower on C2)
-  const int chunks = 16;
+  // each chunk adds a launch and three stream operations: keep the count low
+  // and put the small chunks where the pipeline fills and drains
+  const std::vector<int> weights = pipe_weights();
+  int64_t wsum = 0;
+  for (int w : weights) wsum += w;
+  const int chunks = static_cast<int>(weights.size());
   const bool pipelined = m->n_rows == m->n_cols && m->n_rows >= (1 << 20) &&
-                         m->plan.n_tiles >= 4 * chunks && is_pinned(x_host) &&
+                         m->plan.n_tiles >= 4 * wsum && is_pinned(x_host) &&
                          is_pinned(y_host);
   if (pipelined) {
-    CSRK_TRY(ensure_pipe(m, chunks));
+    CSRK_TRY(ensure_pipe(m, weights));
     auto &pp = m->pipe;
     const bool trace = std::getenv("CSRK_PIPE_TRACE") != nullptr;
     std::vector<cudaEvent_t> tr;
@@ -470,8 +519,15 @@ int csrk_spmv_host(csrk_matrix *m, int value_type, int variant, int nx,
     char *ys = static_cast<char *>(m->y_stage);
     const char *xh = static_cast<const char *>(x_host);
     char *yh = static_cast<char *>(y_host);
+    // D2H ordering (CSRK_PIPE_D2H): "host" (default) enqueues y chunk c once
+    // the host has seen kernel c finish; "event" makes the D2H stream wait on
+    // the kernel's event.  A copy queued behind a cross-stream wait restarts
+    // the copy engine late (measured: 16 ordered chunks 3.36 ms vs 3.00 ms
+    // host-ordered, tools/pcie_probe.py).
+    const char *d2h_mode = std::getenv("CSRK_PIPE_D2H");
+    const bool host_ordered = !(d2h_mode && std::strcmp(d2h_mode, "event") == 0);
     for (int c = 0; c < chunks; ++c) {
-      const size_t off = pp.row_cut[c] * es, len = (pp.row_cut[c + 1] - pp.row_cut[c]) * es;
+      const size_t off = pp.x_cut[c] * es, len = (pp.x_cut[c + 1] - pp.x_cut[c]) * es;
       if (len)
         CSRK_CUDA_TRY(cudaMemcpyAsync(xs + off, xh + off, len, cudaMemcpyHostToDevice,
                                       pp.h2d));
@@ -481,15 +537,26 @@ int csrk_spmv_host(csrk_matrix *m, int value_type, int variant, int nx,
     CSRK_CUDA_TRY(cudaEventRecord(m->ev0, pp.comp));
     for (int c = 0; c < chunks; ++c) {
       CSRK_CUDA_TRY(cudaStreamWaitEvent(pp.comp, pp.ev_x[pp.x_ready[c]], 0));
-      CSRK_TRY(launch_spmv(m, value_type, variant, nx, m->x_stage, m->y_stage, pp.comp,
+      CSRK_TRY(launch_spmv(m, value_type, variant, nx, m->x_stage, ys, pp.comp,
                            pp.tile_cut[c], pp.tile_cut[c + 1]));
       CSRK_CUDA_TRY(cudaEventRecord(pp.ev_c[c], pp.comp));
       if (trace) CSRK_CUDA_TRY(cudaEventRecord(pp.ev_c_t[c], pp.comp));
+      if (host_ordered) continue;
       const size_t off = pp.row_cut[c] * es, len = (pp.row_cut[c + 1] - pp.row_cut[c]) * es;
       CSRK_CUDA_TRY(cudaStreamWaitEvent(pp.d2h, pp.ev_c[c], 0));
       if (len)
         CSRK_CUDA_TRY(cudaMemcpyAsync(yh + off, ys + off, len, cudaMemcpyDeviceToHost,
                                       pp.d2h));
+    }
+    if (host_ordered) {
+      for (int c = 0; c < chunks; ++c) {
+        const size_t off = pp.row_cut[c] * es,
+                     len = (pp.row_cut[c + 1] - pp.row_cut[c]) * es;
+        CSRK_CUDA_TRY(cudaEventSynchronize(pp.ev_c[c]));
+        if (len)
+          CSRK_CUDA_TRY(cudaMemcpyAsync(yh + off, ys + off, len, cudaMemcpyDeviceToHost,
+                                        pp.d2h));
+      }
     }
     CSRK_CUDA_TRY(cudaEventRecord(m->ev1, pp.comp));
     if (trace) {
@@ -508,11 +575,14 @@ int csrk_spmv_host(csrk_matrix *m, int value_type, int variant, int nx,
         float th = 0.f, tk = 0.f;
         cudaEventElapsedTime(&th, tr0, pp.ev_x_t[c]);
         cudaEventElapsedTime(&tk, tr0, pp.ev_c_t[c]);
-        std::fprintf(stderr, "[pipe] chunk %2d rows %9lld x_ready %2d  h2d %.3f  kernel %.3f\n",
+        std::fprintf(stderr,
+                     "[pipe] chunk %2d rows %9lld x %9lld x_ready %2d  h2d %.3f  kernel %.3f\n",
                      c, static_cast<long long>(pp.row_cut[c + 1] - pp.row_cut[c]),
-                     pp.x_ready[c], th, tk);
+                     static_cast<long long>(pp.x_cut[c + 1] - pp.x_cut[c]), pp.x_ready[c],
+                     th, tk);
       }
-      std::fprintf(stderr, "[pipe] d2h done %.3f ms\n", t_end);
+      std::fprintf(stderr, "[pipe] d2h (%s-ordered) done %.3f ms\n",
+                   host_ordered ? "host" : "event", t_end);
       for (auto e : tr) cudaEventDestroy(e);
       cudaEventDestroy(tr0);
     }
@@ -532,7 +602,7 @@ int csrk_spmv_host(csrk_matrix *m, int value_type, int variant, int nx,
   return CSRK_OK;
 }
 
-int csrk_matrix_plan(const csrk_matrix *m, int64_t out[6]) {
+int csrk_matrix_plan(const csrk_matrix *m, int64_t out[7]) {
   if (!m || !out) {
     set_error("null argument");
     return CSRK_EINVAL;
@@ -543,6 +613,20 @@ int csrk_matrix_plan(const csrk_matrix *m, int64_t out[6]) {
   out[3] = m->plan.stages;
   out[4] = m->plan.n_tiles;
   out[5] = m->plan.group_aligned ? 1 : 0;
+  out[6] = m->plan.gather_first;
+  return CSRK_OK;
+}
+
+int csrk_matrix_set_gather(csrk_matrix *m, int mode) {
+  if (!m) {
+    set_error("null argument");
+    return CSRK_EINVAL;
+  }
+  if (mode != 0 && mode != 1) {
+    set_error("gather mode must be 0 (inline) or 1 (gather-first), got %d", mode);
+    return CSRK_EINVAL;
+  }
+  m->plan.gather_first = mode;
   return CSRK_OK;
 }
 

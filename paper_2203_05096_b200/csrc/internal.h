@@ -27,6 +27,7 @@ struct TilePlan {
   int64_t stages = 0;     // ring depth
   int64_t n_tiles = 0;
   bool group_aligned = false;    // tile cuts only on SSR / SR boundaries
+  int gather_first = 0;          // f64: gather a tile's x before its row sums
   uint32_t *tile_row = nullptr;  // device, n_tiles + 1
 };
 
@@ -48,9 +49,12 @@ struct csrk_matrix {
   // host-API staging and the overlapped host pipeline (csrk_spmv_host)
   struct Pipe {
     int chunks = 0;
+    std::vector<int> weights;  // chunk weights the cuts were computed for
     int64_t plan_tiles = -1;  // n_tiles the cuts were computed for
     std::vector<int64_t> tile_cut, row_cut;  // chunks + 1
     std::vector<int> x_ready;                // x chunk needed by chunk c
+    std::vector<int64_t> x_cut;              // x (column) chunk bounds
+    std::string xmode;                       // CSRK_PIPE_XCUT the cuts used
     cudaStream_t h2d = nullptr, comp = nullptr, d2h = nullptr;
     std::vector<cudaEvent_t> ev_x, ev_c;
     std::vector<cudaEvent_t> ev_x_t, ev_c_t;  // timing events (trace only)

@@ -221,6 +221,54 @@ __device__ __forceinline__ double lane_partial(const V *__restrict__ sv,
   return acc;
 }
 
+// GATHER-FIRST tiles: the consumers first replace every staged value by its
+// product vals[p] * x[col[p]] (__dmul_rn, the same rounding the inline path
+// applies), issuing the whole tile's x gathers at once -- balanced over the
+// 256 consumer threads and independent of the row structure -- and then sum
+// the products from shared memory in the row's exact order.  Bitwise equal
+// to the inline path; it decouples gather memory-level parallelism from row
+// lengths, which is what bounds irregular matrices (C5).
+template <typename V>
+__device__ __forceinline__ void gather_products(V *__restrict__ sv,
+                                                const uint32_t *__restrict__ sc,
+                                                uint32_t q0, uint32_t q1,
+                                                const V *__restrict__ x, int ct) {
+  constexpr int U = 8;
+  if (q0 >= q1) return;
+  const uint32_t last = q1 - 1;
+  for (uint32_t p = q0 + ct; p < q1; p += kConsumers * U) {
+    uint32_t c[U];
+    double xv[U];
+#pragma unroll
+    for (int j = 0; j < U; ++j) c[j] = sc[min(p + j * kConsumers, last)];
+#pragma unroll
+    for (int j = 0; j < U; ++j) xv[j] = Elem<V>::load_x(x, c[j]);
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      const uint32_t q = p + j * kConsumers;
+      if (q < q1) sv[q] = __dmul_rn(static_cast<double>(sv[q]), xv[j]);
+    }
+  }
+}
+
+template <typename V>
+__device__ __forceinline__ double row_products(const V *__restrict__ prod,
+                                               uint32_t s, uint32_t e) {
+  double acc = 0.0;
+  for (uint32_t p = s; p < e; ++p) acc = __dadd_rn(acc, static_cast<double>(prod[p]));
+  return acc;
+}
+
+template <int NX, typename V>
+__device__ __forceinline__ double lane_products(const V *__restrict__ prod,
+                                                uint32_t s, uint32_t e, int lane) {
+  double acc = 0.0;
+  if (lane >= NX) return acc;
+  for (uint32_t p = s + lane; p < e; p += NX)
+    acc = __dadd_rn(acc, static_cast<double>(prod[p]));
+  return acc;
+}
+
 template <int P>
 __device__ __forceinline__ double subwarp_tree(double acc) {
 #pragma unroll
@@ -232,15 +280,19 @@ __device__ __forceinline__ double subwarp_tree(double acc) {
 }
 
 // rows [r0, r1) with staged (or global) arrays; `srp(r)` yields row_ptr[r]
-template <typename V, int NX, typename RowPtr>
+template <typename V, int NX, bool PROD = false, typename RowPtr>
 __device__ __forceinline__ void compute_rows(uint32_t r0, uint32_t r1,
                                              const V *__restrict__ sv,
                                              const uint32_t *__restrict__ sc,
                                              RowPtr srp, const V *__restrict__ x,
                                              V *__restrict__ y, int ct) {
   if constexpr (NX == 0) {
-    for (uint32_t r = r0 + ct; r < r1; r += kConsumers)
-      y[r] = Elem<V>::out(row_serial<8, V>(sv, sc, srp(r), srp(r + 1), x));
+    for (uint32_t r = r0 + ct; r < r1; r += kConsumers) {
+      if constexpr (PROD)
+        y[r] = Elem<V>::out(row_products<V>(sv, srp(r), srp(r + 1)));
+      else
+        y[r] = Elem<V>::out(row_serial<8, V>(sv, sc, srp(r), srp(r + 1), x));
+    }
   } else {
     constexpr int P = pow2_ceil(NX);
     constexpr int kSubPerWarp = 32 / P;
@@ -251,7 +303,12 @@ __device__ __forceinline__ void compute_rows(uint32_t r0, uint32_t r1,
     for (uint32_t base = r0 + warp_first; base < r1; base += kSubs) {
       const uint32_t r = base + (sub - warp_first);
       double acc = 0.0;
-      if (r < r1) acc = lane_partial<NX, 4, V>(sv, sc, srp(r), srp(r + 1), lane, x);
+      if (r < r1) {
+        if constexpr (PROD)
+          acc = lane_products<NX, V>(sv, srp(r), srp(r + 1), lane);
+        else
+          acc = lane_partial<NX, 4, V>(sv, sc, srp(r), srp(r + 1), lane, x);
+      }
       acc = subwarp_tree<P>(acc);
       if (r < r1 && lane == 0) y[r] = Elem<V>::out(acc);
     }
@@ -290,7 +347,7 @@ __device__ void compute_direct(uint32_t r0, uint32_t r1,
   }
 }
 
-template <typename V, int NX>
+template <typename V, int NX, bool GF>
 __global__ void __launch_bounds__(kThreads, 2)
     csrk_stream_kernel(const uint32_t *__restrict__ row_ptr,
                        const uint32_t *__restrict__ col_idx,
@@ -365,8 +422,18 @@ __global__ void __launch_bounds__(kThreads, 2)
       const V *sv = reinterpret_cast<const V *>(st + geo.v_off) - md.va0;
       const uint32_t *sc = reinterpret_cast<const uint32_t *>(st + geo.c_off) - md.ca0;
       const uint32_t *sr = reinterpret_cast<const uint32_t *>(st + geo.r_off) - md.ra0;
-      compute_rows<V, NX>(md.r0, md.r1, sv, sc, [&](uint32_t r) { return sr[r]; },
-                          x, y, ct);
+      if constexpr (GF) {
+        V *svw = const_cast<V *>(sv);
+        gather_products<V>(svw, sc, sr[md.r0], sr[md.r1], x, ct);
+        asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory");
+        compute_rows<V, NX, true>(md.r0, md.r1, sv, sc,
+                                  [&](uint32_t r) { return sr[r]; }, x, y, ct);
+        // generic-proxy writes to the stage precede the next TMA fill of it
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      } else {
+        compute_rows<V, NX>(md.r0, md.r1, sv, sc, [&](uint32_t r) { return sr[r]; },
+                            x, y, ct);
+      }
     } else {
       compute_direct<V, NX>(md.r0, md.r1, row_ptr, col_idx, vals, x, y, ct);
     }
@@ -460,14 +527,14 @@ __global__ void chunk_max_col_kernel(const uint32_t *__restrict__ row_ptr,
   }
 }
 
-template <typename V, int NX>
+template <typename V, int NX, bool GF>
 int launch_stream(const csrk_matrix *m, const V *vals, const V *x, V *y,
                   cudaStream_t stream, int64_t t0, int64_t t1) {
   const TilePlan &pl = m->plan;
   const Geometry geo(static_cast<uint32_t>(pl.cap), static_cast<uint32_t>(pl.rcap),
                      static_cast<uint32_t>(pl.stages), sizeof(V));
   const size_t smem = geo.total_bytes();
-  auto kern = csrk_stream_kernel<V, NX>;
+  auto kern = csrk_stream_kernel<V, NX, GF>;
   // attribute + occupancy queries cost host time per launch; cache them per
   // instantiation and shared-memory size (the chunked host pipeline launches
   // the kernel many times per SpMV)
@@ -508,14 +575,14 @@ int launch_stream(const csrk_matrix *m, const V *vals, const V *x, V *y,
   return CSRK_OK;
 }
 
-template <typename V>
+template <typename V, bool GF>
 int dispatch_nx(const csrk_matrix *m, int variant, int nx, const V *vals,
                 const V *x, V *y, cudaStream_t s, int64_t t0, int64_t t1) {
-  if (variant == CSRK_SERIAL) return launch_stream<V, 0>(m, vals, x, y, s, t0, t1);
+  if (variant == CSRK_SERIAL) return launch_stream<V, 0, GF>(m, vals, x, y, s, t0, t1);
   switch (nx) {
 #define CSRK_NX_CASE(N) \
   case N:               \
-    return launch_stream<V, N>(m, vals, x, y, s, t0, t1);
+    return launch_stream<V, N, GF>(m, vals, x, y, s, t0, t1);
     CSRK_NX_CASE(1)
     CSRK_NX_CASE(2)
     CSRK_NX_CASE(3)
@@ -652,7 +719,11 @@ int launch_spmv(const csrk_matrix *m, int value_type, int variant, int nx,
       set_error("matrix holds no float64 values");
       return CSRK_EINVAL;
     }
-    return dispatch_nx<double>(m, variant, nx, m->vals64,
+    if (m->plan.gather_first)
+      return dispatch_nx<double, true>(m, variant, nx, m->vals64,
+                                       static_cast<const double *>(x),
+                                       static_cast<double *>(y), stream, t0, t1);
+    return dispatch_nx<double, false>(m, variant, nx, m->vals64,
                                static_cast<const double *>(x),
                                static_cast<double *>(y), stream, t0, t1);
   }
@@ -661,7 +732,7 @@ int launch_spmv(const csrk_matrix *m, int value_type, int variant, int nx,
       set_error("matrix holds no float32 values");
       return CSRK_EINVAL;
     }
-    return dispatch_nx<float>(m, variant, nx, m->vals32,
+    return dispatch_nx<float, false>(m, variant, nx, m->vals32,
                               static_cast<const float *>(x),
                               static_cast<float *>(y), stream, t0, t1);
   }

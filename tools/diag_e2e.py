@@ -33,3 +33,7 @@ print(f"e2e spmv_csr3 pinned {e2e:.3f} ms")
 dev = m.device()
 import ctypes
 print("plan", dev.plan())
+import os
+os.environ["CSRK_PIPE_TRACE"] = "1"
+ck.spmv_csr3(m, xn, out=yn)
+del os.environ["CSRK_PIPE_TRACE"]

@@ -22,6 +22,9 @@ from paper_2203_05096_b200.bench import spmv_bytes  # noqa: E402
 
 TILES = tuple(int(t) for t in os.environ.get('SWEEP_TILES', '1024,1280,1536,1792,2048,2560,3072').split(','))
 STAGES = tuple(int(t) for t in os.environ.get('SWEEP_STAGES', '2,3').split(','))
+GATHER = tuple(int(t) for t in os.environ.get('SWEEP_GATHER', '0,1').split(','))
+DTYPES = tuple(getattr(torch, d) for d in os.environ.get('SWEEP_DTYPES', 'float64,float32').split(','))
+VARIANTS = os.environ.get('SWEEP_VARIANTS', '')
 
 
 def median_ms(fn, reps=20):
@@ -48,12 +51,18 @@ def main():
         dims = params.block_dims
         variant = "strided" if params.kernel_variant.value == "cuda35" else "serial"
         dev = m.device()
-        for dtype in (torch.float64, torch.float32):
+        for dtype in DTYPES:
             xd = torch.from_numpy(xp).to("cuda", dtype)
             yd = torch.empty(n, dtype=dtype, device="cuda")
             vb = 8 if dtype == torch.float64 else 4
-            for variant_i in sorted({variant, "serial"}):
-                for t in TILES:
+            variants = VARIANTS.split(',') if VARIANTS else sorted({variant, "serial"})
+            for variant_i in variants:
+                dev.set_plan(0, 0, 0)
+                dev.set_gather(0)
+                want = ck.spmv_device(m, xd, yd, dims=dims, variant=variant_i).clone()
+                for g in (GATHER if vb == 8 else (0,)):
+                  dev.set_gather(g)
+                  for t in TILES:
                     for s in STAGES:
                         try:
                             dev.set_plan(t, 0, s)
@@ -61,14 +70,16 @@ def main():
                             continue
                         ms = median_ms(lambda: ck.spmv_device(m, xd, yd, dims=dims,
                                                               variant=variant_i))
+                        same = bool(torch.equal(yd, want))
                         gbs = spmv_bytes(n, n, nnz, vb) / (ms * 1e-3) / 1e9
                         rec = {"config": cfg, "dtype": str(dtype)[6:], "variant": variant_i,
                                "nx": dims.x if variant_i == "strided" else 0,
-                               "tile_cost": t, "stages": s, "ms": round(ms, 4),
-                               "gbs": round(gbs, 1)}
+                               "gather": g, "tile_cost": t, "stages": s, "ms": round(ms, 4),
+                               "gbs": round(gbs, 1), "bitwise_equal": same}
                         print(json.dumps(rec), flush=True)
                         out.append(rec)
             dev.set_plan(0, 0, 0)
+            dev.set_gather(0)
         del m, dev
         torch.cuda.empty_cache()
     os.makedirs("gpurun_out", exist_ok=True)
