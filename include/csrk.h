@@ -93,14 +93,20 @@ int csrk_matrix_add_f32(csrk_matrix *m);
  * stages = TMA ring depth per CTA.  0 = defaults. */
 int csrk_matrix_set_plan(csrk_matrix *m, int64_t tile_cost, int64_t cap,
                          int64_t stages);
-/* out = tile_cost, cap, rcap, stages, n_tiles, group_aligned, gather_first */
-int csrk_matrix_plan(const csrk_matrix *m, int64_t out[7]);
-/* x-gather schedule of the f64 streaming kernel (B200 tuning knob, no
- * reference counterpart; results are bitwise identical either way):
- * 0 = inline (each row gathers its x while summing), 1 = gather-first (a
- * tile's x gathers are issued together, products staged in shared memory,
- * then summed in the row's order) -- for irregular rows (C5). */
-int csrk_matrix_set_gather(csrk_matrix *m, int mode);
+/* out = tile_cost, cap, rcap, stages, n_tiles, group_aligned, gather mode,
+ *       ctas_per_sm (the f64 value when auto) */
+int csrk_matrix_plan(const csrk_matrix *m, int64_t out[8]);
+/* Schedule of the streaming kernel (B200 tuning knobs with no reference
+ * counterpart; results are bitwise identical under every setting).
+ * gather: 0 = inline (each row gathers its x while summing), 1 = gather-first
+ * (f64 only: a tile's x gathers are issued together, the products staged in
+ * shared memory, then summed in the row's order), 2 = auto (default:
+ * gather-first for the serial order when rows average > 16 nonzeros).
+ * ctas_per_sm: resident CTAs per SM (1..8; 0 = auto: 2 for irregular rows
+ * -- variance > 10 --, else 3 in f64 and 4 in f32); the shared-memory
+ * carveout is set to exactly what they need, and the rest of the 256 KB
+ * stays L1 for the x gathers. */
+int csrk_matrix_set_schedule(csrk_matrix *m, int gather, int ctas_per_sm);
 
 /* ---- SpMV ------------------------------------------------------------------
  * y = A x on device-resident x / y (already in the permuted index space, as

@@ -47,7 +47,7 @@ _SIGNATURES = {
     "csrk_matrix_add_f32": ([P], C.c_int),
     "csrk_matrix_set_plan": ([P, I64, I64, I64], C.c_int),
     "csrk_matrix_plan": ([P, I64P], C.c_int),
-    "csrk_matrix_set_gather": ([P, C.c_int], C.c_int),
+    "csrk_matrix_set_schedule": ([P, C.c_int, C.c_int], C.c_int),
     "csrk_spmv": ([P, C.c_int, C.c_int, C.c_int, P, P, P], C.c_int),
     "csrk_spmv_host": ([P, C.c_int, C.c_int, C.c_int, P, P], C.c_int),
     "csrk_last_kernel_ms": ([P, C.POINTER(C.c_float)], C.c_int),
@@ -264,15 +264,16 @@ class DeviceMatrix:
         """Streaming-kernel tile plan (0 = defaults); see include/csrk.h."""
         call("csrk_matrix_set_plan", self.ptr, int(tile_cost), int(cap), int(stages))
 
-    def set_gather(self, mode: int):
-        """x-gather schedule of the f64 kernel: 0 inline, 1 gather-first."""
-        call("csrk_matrix_set_gather", self.ptr, int(mode))
+    def set_schedule(self, gather: int = 0, ctas_per_sm: int = 0):
+        """Streaming-kernel schedule (see include/csrk.h): x-gather mode
+        (0 inline, 1 gather-first) and resident CTAs per SM (0 = default)."""
+        call("csrk_matrix_set_schedule", self.ptr, int(gather), int(ctas_per_sm))
 
     def plan(self) -> dict:
-        out = np.zeros(7, dtype=np.int64)
+        out = np.zeros(8, dtype=np.int64)
         call("csrk_matrix_plan", self.ptr, i64p(out))
         keys = ("tile_cost", "cap", "rcap", "stages", "n_tiles", "group_aligned",
-                "gather_first")
+                "gather_first", "ctas_per_sm")
         return {k: int(v) for k, v in zip(keys, out)}
 
     def stats(self):

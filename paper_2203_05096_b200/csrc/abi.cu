@@ -602,7 +602,7 @@ int csrk_spmv_host(csrk_matrix *m, int value_type, int variant, int nx,
   return CSRK_OK;
 }
 
-int csrk_matrix_plan(const csrk_matrix *m, int64_t out[7]) {
+int csrk_matrix_plan(const csrk_matrix *m, int64_t out[8]) {
   if (!m || !out) {
     set_error("null argument");
     return CSRK_EINVAL;
@@ -614,19 +614,26 @@ int csrk_matrix_plan(const csrk_matrix *m, int64_t out[7]) {
   out[4] = m->plan.n_tiles;
   out[5] = m->plan.group_aligned ? 1 : 0;
   out[6] = m->plan.gather_first;
+  out[7] = m->plan.ctas_per_sm ? m->plan.ctas_per_sm : auto_ctas(m->plan.row_var, 8);
   return CSRK_OK;
 }
 
-int csrk_matrix_set_gather(csrk_matrix *m, int mode) {
+int csrk_matrix_set_schedule(csrk_matrix *m, int gather, int ctas_per_sm) {
   if (!m) {
     set_error("null argument");
     return CSRK_EINVAL;
   }
-  if (mode != 0 && mode != 1) {
-    set_error("gather mode must be 0 (inline) or 1 (gather-first), got %d", mode);
+  if (gather < 0 || gather > 2) {
+    set_error("gather mode must be 0 (inline), 1 (gather-first) or 2 (auto), got %d",
+              gather);
     return CSRK_EINVAL;
   }
-  m->plan.gather_first = mode;
+  if (ctas_per_sm < 0 || ctas_per_sm > 8) {
+    set_error("ctas_per_sm must be in 0..8, got %d", ctas_per_sm);
+    return CSRK_EINVAL;
+  }
+  m->plan.gather_first = gather;
+  m->plan.ctas_per_sm = ctas_per_sm;
   return CSRK_OK;
 }
 

@@ -19,6 +19,22 @@ void set_error(const char *fmt, ...);
 // [tile_row[t], tile_row[t+1]) made of whole groups.
 constexpr int64_t kDefaultTileCost = 2048;  // nonzeros + rows per tile
 constexpr int64_t kDefaultStages = 2;       // TMA ring depth per CTA (plan sweep)
+constexpr int64_t kDefaultCtasPerSm = 3;    // resident streaming CTAs per SM
+constexpr int kGatherAuto = 2;
+
+// Auto schedule (round-1 plan sweeps, profiles/r01_sched_sweep.txt):
+//  * regular rows: 3 CTAs per SM in f64, 4 in f32 (half the bytes per
+//    nonzero, so more tiles in flight: C2 f32 +9 %);
+//  * irregular rows (variance > 10, the paper's class boundary) are bound by
+//    random x gathers: 2 CTAs per SM, leaving ~120 KB of L1 (C5 +47 %);
+//  * the serial order over rows longer than 16 nonzeros gathers first
+//    (C3 +13 %); short rows keep the inline gathers (C2 -15 % otherwise).
+inline int auto_ctas(double row_var, int value_bytes) {
+  return row_var > 10.0 ? 2 : (value_bytes == 4 ? 4 : 3);
+}
+inline bool auto_gather(int variant, double mean_row) {
+  return variant == CSRK_SERIAL && mean_row > 16.0;
+}
 
 struct TilePlan {
   int64_t tile_cost = 0;  // requested nonzeros + rows per tile
@@ -27,7 +43,13 @@ struct TilePlan {
   int64_t stages = 0;     // ring depth
   int64_t n_tiles = 0;
   bool group_aligned = false;    // tile cuts only on SSR / SR boundaries
-  int gather_first = 0;          // f64: gather a tile's x before its row sums
+  // schedule (csrk_matrix_set_schedule): requested gather mode (0 inline,
+  // 1 gather-first, 2 auto) and CTAs per SM (0 = auto), plus the row
+  // statistics the auto choices read (measured when the plan is built)
+  int gather_first = kGatherAuto;
+  int ctas_per_sm = 0;
+  double mean_row = 0.0, row_var = 0.0;
+  bool row_stats = false;
   uint32_t *tile_row = nullptr;  // device, n_tiles + 1
 };
 

@@ -25,7 +25,9 @@
 //   * a tile that does not fit a stage (a very long row) is computed from
 //     global memory by the consumers ("direct" mode).
 
+#include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "internal.h"
 
@@ -161,10 +163,13 @@ struct StageMeta {
 // ---- per-row arithmetic ---------------------------------------------------
 
 // Serial left-to-right row sum.  Every batch issues all of its x gathers
-// before the ordered adds: indices past the row end are clamped to the last
-// element (a redundant, L1-resident load) so the loads are unconditional and
-// independent -- predicating them lets the compiler serialise the gathers
-// through one register pair, which left one load in flight per thread.
+// before the ordered adds: lanes past the row end load x[0] (their result is
+// discarded), so the loads are unconditional and independent -- predicating
+// them lets the compiler serialise the gathers through one register pair,
+// which left one load in flight per thread.  Pointing every spare lane at the
+// same line costs an L1 wavefront at most once per load instruction, where
+// clamping to each row's last element cost one per lane (random gathers are
+// bound by L1TEX at one 128-byte line per cycle per SM).
 template <int B, typename V>
 __device__ __forceinline__ double row_serial(const V *__restrict__ sv,
                                              const uint32_t *__restrict__ sc,
@@ -179,7 +184,7 @@ __device__ __forceinline__ double row_serial(const V *__restrict__ sv,
 #pragma unroll
     for (int j = 0; j < B; ++j) {
       const uint32_t q = min(p + j, last);
-      c[j] = sc[q];
+      c[j] = p + j <= last ? sc[q] : 0u;
       v[j] = static_cast<double>(sv[q]);
     }
 #pragma unroll
@@ -209,7 +214,7 @@ __device__ __forceinline__ double lane_partial(const V *__restrict__ sv,
 #pragma unroll
     for (int j = 0; j < B; ++j) {
       const uint32_t q = min(p + j * NX, last);
-      c[j] = sc[q];
+      c[j] = p + j * NX <= last ? sc[q] : 0u;
       v[j] = static_cast<double>(sv[q]);
     }
 #pragma unroll
@@ -476,6 +481,19 @@ __global__ void max_group_cost_kernel(const uint32_t *__restrict__ row_ptr,
   if ((threadIdx.x & 31) == 0) atomicMax(out, mx);
 }
 
+// sum over rows of (row length)^2, for the schedule's variance test
+__global__ void row_sq_kernel(const uint32_t *__restrict__ row_ptr, int64_t n_rows,
+                              unsigned long long *out) {
+  unsigned long long acc = 0;
+  for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r < n_rows;
+       r += int64_t(gridDim.x) * blockDim.x) {
+    const unsigned long long l = row_ptr[r + 1] - row_ptr[r];
+    acc += l * l;
+  }
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(out, acc);
+}
+
 // tile_row[t] = first cut point (group start, or row when cut_k == 1) whose
 // cost row_ptr[r] + r reaches t * tile_cost
 __global__ void tile_bounds_kernel(const uint32_t *__restrict__ row_ptr,
@@ -539,23 +557,38 @@ int launch_stream(const csrk_matrix *m, const V *vals, const V *x, V *y,
   // instantiation and shared-memory size (the chunked host pipeline launches
   // the kernel many times per SpMV)
   static thread_local size_t cached_smem = 0;
-  static thread_local int cached_per_sm = 0;
+  static thread_local int cached_per_sm = 0, cached_ctas = 0;
   static thread_local int cached_device = -1;
   int cur_dev = 0;
   CSRK_CUDA_TRY(cudaGetDevice(&cur_dev));
+  const int ctas = pl.ctas_per_sm > 0 ? pl.ctas_per_sm
+                                      : auto_ctas(pl.row_var, static_cast<int>(sizeof(V)));
   int per_sm = 0;
-  if (cached_smem == smem && cached_device == cur_dev) {
+  if (cached_smem == smem && cached_device == cur_dev && cached_ctas == ctas) {
     per_sm = cached_per_sm;
   } else {
     CSRK_CUDA_TRY(cudaFuncSetAttribute(
         kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    // (the carveout is left to the driver: it keeps the L1 share that the
-    // x gathers of irregular matrices depend on -- forcing max-shared cost
-    // C5 a third of its bandwidth in the plan sweep)
+    // Carveout = exactly what `ctas` CTAs need (+1 KB reserved each); the
+    // rest of the SM's 256 KB stays L1, where the x gathers hit.  Left to
+    // the driver, the carveout jumped with the stage size (a 2 KB larger
+    // stage moved C5 from the 200 KB to the 228 KB carveout and cost it a
+    // third of its bandwidth).
+    int smem_sm = 0;
+    CSRK_CUDA_TRY(cudaDeviceGetAttribute(&smem_sm,
+                                         cudaDevAttrMaxSharedMemoryPerMultiprocessor,
+                                         cur_dev));
+    const double need = static_cast<double>(ctas) * (smem + 1024);
+    int pct = static_cast<int>(need * 100.0 / smem_sm + 0.999);
+    pct = pct < 1 ? 1 : (pct > 100 ? 100 : pct);
+    CSRK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                       pct));
     CSRK_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads,
                                                                 smem));
+    if (per_sm > ctas) per_sm = ctas;
     cached_smem = smem;
     cached_per_sm = per_sm;
+    cached_ctas = ctas;
     cached_device = cur_dev;
   }
   if (per_sm < 1) {
@@ -623,7 +656,14 @@ int ensure_plan(csrk_matrix *m, int64_t tile_cost, int64_t cap, int64_t stages,
   if (cap < 16) cap = 16;
   if (stages <= 0) stages = kDefaultStages;
   if (stages > 8) stages = 8;
-  const int64_t rcap = cap;
+  // Row room per stage: a tile holds at most `cap` rows (cost = nonzeros +
+  // rows), but only tiles of near-empty rows get close; half the room keeps
+  // the stage -- and so the shared-memory carveout -- small enough to leave
+  // L1 for the x gathers, and a tile with more rows runs in direct mode.
+  // CSRK_RCAP_DIV overrides the divisor (plan sweeps).
+  int64_t rdiv = 2;
+  if (const char *e = std::getenv("CSRK_RCAP_DIV")) rdiv = std::max(1, std::atoi(e));
+  const int64_t rcap = std::max<int64_t>(16, cap / rdiv);
   const Geometry geo(static_cast<uint32_t>(cap), static_cast<uint32_t>(rcap),
                      static_cast<uint32_t>(stages), sizeof(double));
   if (geo.total_bytes() > 227 * 1024) {
@@ -632,13 +672,27 @@ int ensure_plan(csrk_matrix *m, int64_t tile_cost, int64_t cap, int64_t stages,
     return CSRK_EINVAL;
   }
   if (m->plan.tile_row && m->plan.tile_cost == tile_cost && m->plan.cap == cap &&
-      m->plan.stages == stages)
+      m->plan.rcap == rcap && m->plan.stages == stages)
     return CSRK_OK;
   if (m->sm_count == 0) {
     int dev = 0;
     CSRK_CUDA_TRY(cudaGetDevice(&dev));
     CSRK_CUDA_TRY(cudaDeviceGetAttribute(&m->sm_count, cudaDevAttrMultiProcessorCount,
                                          dev));
+  }
+  if (m->n_rows > 0 && !m->plan.row_stats) {
+    unsigned long long *d = nullptr, h = 0;
+    CSRK_CUDA_TRY(cudaMallocAsync(&d, sizeof(h), s));
+    CSRK_CUDA_TRY(cudaMemsetAsync(d, 0, sizeof(h), s));
+    row_sq_kernel<<<148 * 8, 256, 0, s>>>(m->row_ptr, m->n_rows, d);
+    CSRK_CUDA_TRY(cudaGetLastError());
+    CSRK_CUDA_TRY(cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, s));
+    CSRK_CUDA_TRY(cudaStreamSynchronize(s));
+    cudaFreeAsync(d, s);
+    const double mean = static_cast<double>(m->nnz) / static_cast<double>(m->n_rows);
+    m->plan.mean_row = mean;
+    m->plan.row_var = static_cast<double>(h) / static_cast<double>(m->n_rows) - mean * mean;
+    m->plan.row_stats = true;
   }
   const int64_t n_groups = m->k == 3 ? m->n_ssr : (m->k == 2 ? m->n_sr : m->n_rows);
   // cut on group boundaries when every group is small against a tile
@@ -719,7 +773,8 @@ int launch_spmv(const csrk_matrix *m, int value_type, int variant, int nx,
       set_error("matrix holds no float64 values");
       return CSRK_EINVAL;
     }
-    if (m->plan.gather_first)
+    const int g = m->plan.gather_first;
+    if (g == 1 || (g == kGatherAuto && auto_gather(variant, m->plan.mean_row)))
       return dispatch_nx<double, true>(m, variant, nx, m->vals64,
                                        static_cast<const double *>(x),
                                        static_cast<double *>(y), stream, t0, t1);

@@ -1,0 +1,12 @@
+"""Tabulate plan_sweep JSON lines: python tools/sweep_table.py FILE"""
+import collections
+import json
+import sys
+
+t = collections.defaultdict(dict)
+for line in open(sys.argv[1]):
+    r = json.loads(line)
+    key = (r["config"], r["dtype"], r["variant"], "G%d" % r["gather"], "C%d" % r.get("ctas", 0))
+    t[key]["T%dS%d" % (r["tile_cost"], r["stages"])] = (r["gbs"], r["bitwise_equal"])
+for k, v in t.items():
+    print(" ".join(k), " ".join("%s:%.0f%s" % (a, b[0], "" if b[1] else "!") for a, b in v.items()))
