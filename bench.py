@@ -189,9 +189,9 @@ def run_ours(args, log):
     from paper_2203_05096_b200.bench import spmv_bytes
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    if world > 1:
+    if world > 1 or (os.environ.get("CSRK_DIST") == "1" and "RANK" in os.environ):
         from paper_2203_05096_b200 import dist
-        return dist.bench_main(args, log)
+        return dist.bench_main(args, log, sampler=ClockSampler, peak=measured_peak())
     torch.cuda.set_device(0)
     a, m, xp, params, build_t = build_matrix(args.config, log)
     n, nnz = a.n_rows, a.nnz
@@ -475,7 +475,8 @@ def main(argv=None):
 
     if args.impl == "reference":
         line = run_reference(args, log)
-    elif args.config == "C4":
+    elif args.config == "C4" and int(os.environ.get("WORLD_SIZE", "1")) == 1 and \
+            os.environ.get("CSRK_DIST") != "1":
         line = run_loop(args, log)
     else:
         line = run_ours(args, log)

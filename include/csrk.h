@@ -123,6 +123,13 @@ int csrk_spmv(const csrk_matrix *m, int value_type, int variant, int nx,
  * returns when y is written).  The drop-in call shape of spmv_csr3(m, x). */
 int csrk_spmv_host(csrk_matrix *m, int value_type, int variant, int nx,
                    const void *x_host, void *y_host);
+/* csrk_spmv over the tiles [t0, t1) of the handle's plan only (rows
+ * tile_rows[t0] .. tile_rows[t1]); the multi-GPU step computes the interior
+ * tiles while the x halo is in flight, then the boundary tiles. */
+int csrk_spmv_tiles(const csrk_matrix *m, int value_type, int variant, int nx,
+                    const void *x, void *y, int64_t t0, int64_t t1, void *stream);
+/* the plan's tile row bounds (n_tiles + 1 entries, see csrk_matrix_plan) */
+int csrk_matrix_tile_rows(const csrk_matrix *m, uint32_t *out);
 /* CUDA-event device time of the last csrk_spmv_host kernel, milliseconds */
 int csrk_last_kernel_ms(const csrk_matrix *m, float *ms);
 
@@ -209,6 +216,13 @@ int csrk_band_k_device(const csrk_matrix *a, int k, const double *targets,
  * Produces a k = 1 handle (natural order). */
 int csrk_stencil(int device, int64_t nz, int64_t ny, int64_t nx, int points,
                  csrk_matrix **out);
+/* One rank's slab of a 3D stencil (7 or 27 points) for the row-block
+ * partition (no reference counterpart -- the reference is
+ * single-node): rows of planes [z0, z1), columns numbered from plane
+ * max(z0 - 1, 0), so the handle's x is [lower halo plane | own planes |
+ * upper halo plane] (halo planes only where the grid has them). */
+int csrk_stencil_slab(int device, int64_t nz, int64_t ny, int64_t nx, int points,
+                      int64_t z0, int64_t z1, csrk_matrix **out);
 
 /* Give a handle uniform groups (k = 3): srs rows per super-row, ssrs
  * super-rows per super-super-row, the last of each shorter -- the

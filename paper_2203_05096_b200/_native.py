@@ -49,6 +49,8 @@ _SIGNATURES = {
     "csrk_matrix_plan": ([P, I64P], C.c_int),
     "csrk_matrix_set_schedule": ([P, C.c_int, C.c_int], C.c_int),
     "csrk_spmv": ([P, C.c_int, C.c_int, C.c_int, P, P, P], C.c_int),
+    "csrk_spmv_tiles": ([P, C.c_int, C.c_int, C.c_int, P, P, I64, I64, P], C.c_int),
+    "csrk_matrix_tile_rows": ([P, U32P], C.c_int),
     "csrk_spmv_host": ([P, C.c_int, C.c_int, C.c_int, P, P], C.c_int),
     "csrk_last_kernel_ms": ([P, C.POINTER(C.c_float)], C.c_int),
     "csrk_spmv_listing3": ([P, C.c_int, C.c_int, P, P, P, P], C.c_int),
@@ -73,6 +75,8 @@ _SIGNATURES = {
     "csrk_band_k_device": ([P, C.c_int, F64P, C.POINTER(P)], C.c_int),
     "csrk_sort_pairs": ([C.c_int, I64, P, P, C.c_int, C.c_int, P], C.c_int),
     "csrk_stencil": ([C.c_int, I64, I64, I64, C.c_int, C.POINTER(P)], C.c_int),
+    "csrk_stencil_slab": ([C.c_int, I64, I64, I64, C.c_int, I64, I64, C.POINTER(P)],
+                          C.c_int),
     "csrk_band_k": ([I64, U32P, U32P, C.c_int, F64P, C.POINTER(P)], C.c_int),
     "csrk_bandk_result_sizes": ([P, I64P], C.c_int),
     "csrk_bandk_result_get": ([P, I64P, I64P, I64P], C.c_int),
@@ -300,6 +304,18 @@ class DeviceMatrix:
                  nx=1, f32=False):
         call("csrk_spmv", self.ptr, CSRK_F32 if f32 else CSRK_F64, variant, nx,
              C.c_void_p(x_ptr), C.c_void_p(y_ptr), C.c_void_p(stream))
+
+    def spmv_tiles_ptr(self, x_ptr: int, y_ptr: int, t0: int, t1: int, stream: int = 0,
+                       variant=CSRK_SERIAL, nx=1, f32=False):
+        """csrk_spmv over the plan's tiles [t0, t1) only."""
+        call("csrk_spmv_tiles", self.ptr, CSRK_F32 if f32 else CSRK_F64, variant, nx,
+             C.c_void_p(x_ptr), C.c_void_p(y_ptr), int(t0), int(t1), C.c_void_p(stream))
+
+    def tile_rows(self) -> np.ndarray:
+        """Row bounds of the plan's tiles (n_tiles + 1 entries)."""
+        out = np.empty(self.plan()["n_tiles"] + 1, dtype=np.uint32)
+        call("csrk_matrix_tile_rows", self.ptr, u32p(out))
+        return out
 
     def last_kernel_ms(self) -> float:
         ms = C.c_float(0.0)

@@ -353,6 +353,38 @@ int csrk_spmv(const csrk_matrix *m, int value_type, int variant, int nx,
                      static_cast<cudaStream_t>(stream));
 }
 
+int csrk_spmv_tiles(const csrk_matrix *m, int value_type, int variant, int nx,
+                    const void *x, void *y, int64_t t0, int64_t t1, void *stream) {
+  if (!m || (m->n_rows > 0 && (!x || !y))) {
+    set_error("null argument");
+    return CSRK_EINVAL;
+  }
+  if (t0 < 0 || t1 < t0 || t1 > m->plan.n_tiles) {
+    set_error("tile range [%lld, %lld) outside 0..%lld", static_cast<long long>(t0),
+              static_cast<long long>(t1), static_cast<long long>(m->plan.n_tiles));
+    return CSRK_EINVAL;
+  }
+  if (t1 == t0) return CSRK_OK;
+  CSRK_CUDA_TRY(cudaSetDevice(m->device));
+  return launch_spmv(m, value_type, variant, nx, x, y, static_cast<cudaStream_t>(stream),
+                     t0, t1);
+}
+
+int csrk_matrix_tile_rows(const csrk_matrix *m, uint32_t *out) {
+  if (!m || !out) {
+    set_error("null argument");
+    return CSRK_EINVAL;
+  }
+  if (!m->plan.tile_row) {
+    set_error("matrix has no tile plan");
+    return CSRK_EINVAL;
+  }
+  CSRK_CUDA_TRY(cudaSetDevice(m->device));
+  CSRK_CUDA_TRY(cudaMemcpy(out, m->plan.tile_row, (m->plan.n_tiles + 1) * sizeof(uint32_t),
+                           cudaMemcpyDeviceToHost));
+  return CSRK_OK;
+}
+
 // Host-buffer SpMV.  With pinned host x / y and a square matrix the copies
 // and the kernel overlap: x goes up in row-aligned chunks on one stream, the
 // rows of chunk c are computed on a second stream as soon as the x chunks

@@ -375,12 +375,15 @@ __host__ bool make_stencil(int64_t nz, int points, Stencil &st) {
   return true;
 }
 
+// Rows of planes [z0, z0 + nzl) of an nz x ny x nx grid (the whole grid:
+// z0 = 0, nzl = nz); columns are global indices minus col_base.
 __global__ void stencil_count_kernel(Stencil st, int64_t nz, int64_t ny,
-                                     int64_t nx, int64_t *__restrict__ counts) {
-  const int64_t n = nz * ny * nx;
+                                     int64_t nx, int64_t z0, int64_t nzl,
+                                     int64_t *__restrict__ counts) {
+  const int64_t n = nzl * ny * nx;
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
        i += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t x = i % nx, y = (i / nx) % ny, z = i / (nx * ny);
+    const int64_t x = i % nx, y = (i / nx) % ny, z = z0 + i / (nx * ny);
     int64_t c = 0;
     for (int j = 0; j < st.n; ++j) {
       const int64_t zz = z + st.dz[j], yy = y + st.dy[j], xx = x + st.dx[j];
@@ -391,22 +394,23 @@ __global__ void stencil_count_kernel(Stencil st, int64_t nz, int64_t ny,
 }
 
 __global__ void stencil_fill_kernel(Stencil st, int64_t nz, int64_t ny,
-                                    int64_t nx, const int64_t *__restrict__ ptr,
+                                    int64_t nx, int64_t z0, int64_t nzl,
+                                    int64_t col_base, const int64_t *__restrict__ ptr,
                                     uint32_t *__restrict__ row_ptr,
                                     uint32_t *__restrict__ cols,
                                     double *__restrict__ vals) {
-  const int64_t n = nz * ny * nx;
+  const int64_t n = nzl * ny * nx;
   const double diag = static_cast<double>(st.n - 1);
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i <= n;
        i += int64_t(gridDim.x) * blockDim.x) {
     row_ptr[i] = static_cast<uint32_t>(ptr[i]);
     if (i == n) continue;
-    const int64_t x = i % nx, y = (i / nx) % ny, z = i / (nx * ny);
+    const int64_t x = i % nx, y = (i / nx) % ny, z = z0 + i / (nx * ny);
     int64_t p = ptr[i];
     for (int j = 0; j < st.n; ++j) {
       const int64_t zz = z + st.dz[j], yy = y + st.dy[j], xx = x + st.dx[j];
       if (zz >= 0 && zz < nz && yy >= 0 && yy < ny && xx >= 0 && xx < nx) {
-        cols[p] = static_cast<uint32_t>((zz * ny + yy) * nx + xx);
+        cols[p] = static_cast<uint32_t>((zz * ny + yy) * nx + xx - col_base);
         vals[p] = (st.dz[j] == 0 && st.dy[j] == 0 && st.dx[j] == 0) ? diag : -1.0;
         ++p;
       }
@@ -712,7 +716,7 @@ int row_variance(const csrk_matrix *m, double mean, double *out) {
 }
 
 int stencil_device(int device, int64_t nz, int64_t ny, int64_t nx, int points,
-                   csrk_matrix **out) {
+                   int64_t z0, int64_t z1, csrk_matrix **out) {
   *out = nullptr;
   Stencil st;
   if (nz < 1 || ny < 1 || nx < 1 || !make_stencil(nz, points, st)) {
@@ -721,13 +725,30 @@ int stencil_device(int device, int64_t nz, int64_t ny, int64_t nx, int points,
               static_cast<long long>(nx));
     return CSRK_EINVAL;
   }
-  const int64_t n = nz * ny * nx;
+  if (z0 < 0 || z1 > nz || z0 >= z1) {
+    set_error("slab planes [%lld, %lld) are not a non-empty range of 0..%lld",
+              static_cast<long long>(z0), static_cast<long long>(z1),
+              static_cast<long long>(nz));
+    return CSRK_EINVAL;
+  }
+  const int64_t plane = ny * nx;
+  const int64_t nzl = z1 - z0;
+  const int64_t n = nzl * plane;
+  // halo planes: one below / above the slab where the stencil reaches them
+  const bool reach = st.n == 7 || st.n == 27;
+  const int64_t c0 = reach ? (z0 > 0 ? z0 - 1 : 0) : z0;
+  const int64_t c1 = reach ? (z1 < nz ? z1 + 1 : nz) : z1;
+  const int64_t n_cols = (c1 - c0) * plane;
   CSRK_CUDA_TRY(cudaSetDevice(device));
   // exact nnz on the host: per-axis counts of valid offsets are separable
+  // (planes: rows in [z0, z1) whose neighbour plane z + dz is in the grid)
   int64_t nnz = 0;
-  for (int j = 0; j < st.n; ++j)
-    nnz += (nz - (st.dz[j] != 0)) * (ny - (st.dy[j] != 0)) * (nx - (st.dx[j] != 0));
-  if (nnz > 2147483647LL || n > 4294967295LL) {
+  for (int j = 0; j < st.n; ++j) {
+    const int64_t lo = z0 > -st.dz[j] ? z0 : -st.dz[j];
+    const int64_t hi = z1 < nz - st.dz[j] ? z1 : nz - st.dz[j];
+    nnz += (hi > lo ? hi - lo : 0) * (ny - (st.dy[j] != 0)) * (nx - (st.dx[j] != 0));
+  }
+  if (nnz > 2147483647LL || n > 4294967295LL || n_cols > 4294967295LL) {
     set_error("nnz %lld exceeds the 32-bit index limit 2147483647",
               static_cast<long long>(nnz));
     return CSRK_EINVAL;
@@ -735,7 +756,7 @@ int stencil_device(int device, int64_t nz, int64_t ny, int64_t nx, int points,
   csrk_matrix *m = new csrk_matrix();
   m->device = device;
   m->n_rows = n;
-  m->n_cols = n;
+  m->n_cols = n_cols;
   m->nnz = nnz;
   m->k = 1;
   int rc = alloc_matrix_arrays(m, true, false);
@@ -751,12 +772,12 @@ int stencil_device(int device, int64_t nz, int64_t ny, int64_t nx, int points,
     set_error("out of device memory in stencil generator");
     return CSRK_ENOMEM;
   }
-  stencil_count_kernel<<<grid_for(n, 256), 256, 0, m->stream>>>(st, nz, ny, nx,
-                                                                 counts.p);
+  stencil_count_kernel<<<grid_for(n, 256), 256, 0, m->stream>>>(st, nz, ny, nx, z0,
+                                                                 nzl, counts.p);
   rc = exclusive_scan(counts.p, n, ptr.p, m->stream);
   if (rc == CSRK_OK) {
     stencil_fill_kernel<<<grid_for(n + 1, 256), 256, 0, m->stream>>>(
-        st, nz, ny, nx, ptr.p, m->row_ptr, m->col_idx, m->vals64);
+        st, nz, ny, nx, z0, nzl, c0 * plane, ptr.p, m->row_ptr, m->col_idx, m->vals64);
     if (cudaGetLastError() != cudaSuccess) rc = CSRK_ECUDA;
   }
   if (rc == CSRK_OK) rc = ensure_plan(m, 0, 0, 0, m->stream);
@@ -824,7 +845,20 @@ int csrk_stencil(int device, int64_t nz, int64_t ny, int64_t nx, int points,
     csrk::set_error("null argument");
     return CSRK_EINVAL;
   }
-  return csrk::stencil_device(device, nz, ny, nx, points, out);
+  return csrk::stencil_device(device, nz, ny, nx, points, 0, nz, out);
+}
+
+int csrk_stencil_slab(int device, int64_t nz, int64_t ny, int64_t nx, int points,
+                      int64_t z0, int64_t z1, csrk_matrix **out) {
+  if (!out) {
+    csrk::set_error("null argument");
+    return CSRK_EINVAL;
+  }
+  if (points != 7 && points != 27) {
+    csrk::set_error("slabs need a 3D stencil (7 or 27 points), got %d", points);
+    return CSRK_EINVAL;
+  }
+  return csrk::stencil_device(device, nz, ny, nx, points, z0, z1, out);
 }
 
 }  // extern "C"

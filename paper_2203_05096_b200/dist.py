@@ -18,6 +18,15 @@ filled by one of two exchanges:
 y slices are disjoint, so no reduction is needed.  The exchange code only
 uses tensor slicing and torch.distributed, so it runs unchanged on CPU
 tensors over gloo (tests/test_dist.py) and on CUDA tensors over NCCL.
+
+Generated 3D stencils partition as z-slabs instead (``SlabSpMV``): each rank
+generates its own planes in HBM (csrk_stencil_slab) with columns local to
+[lower halo plane | own planes | upper halo plane], so no rank holds the
+global matrix or a global-length x.  One step sends the first / last owned
+plane to the neighbours (NCCL send / recv over NVLink) while the interior
+tiles -- rows whose stencil stays inside the owned planes -- are computed,
+then computes the two boundary planes.  This is the partition of the
+weak-scaling bench (a C2-sized slab per GPU) and of the multi-GPU CG (C4).
 """
 
 from __future__ import annotations
@@ -28,6 +37,12 @@ from dataclasses import dataclass
 import numpy as np
 
 __all__ = [
+    "slab_cuts",
+    "SlabLayout",
+    "interior_tiles",
+    "SlabExchange",
+    "SlabSpMV",
+    "DistCG",
     "partition_by_nnz",
     "footprints",
     "halo_plan",
@@ -37,6 +52,216 @@ __all__ = [
     "DistSpMV",
     "bench_main",
 ]
+
+
+def slab_cuts(nz: int, world: int) -> list:
+    """Plane cuts: rank g owns planes [cuts[g], cuts[g + 1]).  Equal plane
+    counts (+-1) balance nonzeros to within one plane."""
+    if world < 1 or nz < world:
+        raise ValueError(f"cannot split {nz} planes over {world} ranks")
+    return [nz * g // world for g in range(world + 1)]
+
+
+@dataclass(frozen=True)
+class SlabLayout:
+    """Local index spaces of one rank's slab of an nz x ny x nx grid."""
+
+    nz: int
+    ny: int
+    nx: int
+    rank: int
+    world: int
+    z0: int
+    z1: int
+
+    @classmethod
+    def of(cls, shape, rank: int, world: int) -> "SlabLayout":
+        nz, ny, nx = (int(v) for v in shape)
+        cuts = slab_cuts(nz, world)
+        return cls(nz, ny, nx, rank, world, cuts[rank], cuts[rank + 1])
+
+    @property
+    def plane(self) -> int:
+        return self.ny * self.nx
+
+    @property
+    def has_lo(self) -> bool:
+        return self.z0 > 0
+
+    @property
+    def has_hi(self) -> bool:
+        return self.z1 < self.nz
+
+    @property
+    def n_own(self) -> int:
+        """rows of this rank (and entries of its y)"""
+        return (self.z1 - self.z0) * self.plane
+
+    @property
+    def own_off(self) -> int:
+        """offset of the owned x entries in the local x"""
+        return self.plane if self.has_lo else 0
+
+    @property
+    def n_cols(self) -> int:
+        """length of the local x: own planes plus the halo planes"""
+        return self.n_own + self.plane * (int(self.has_lo) + int(self.has_hi))
+
+    @property
+    def global_row0(self) -> int:
+        return self.z0 * self.plane
+
+    def interior_rows(self) -> tuple:
+        """[a, b): local rows whose 7- / 27-point stencil reads owned x only"""
+        a = self.plane if self.has_lo else 0
+        b = self.n_own - (self.plane if self.has_hi else 0)
+        return a, max(a, b)
+
+
+def interior_tiles(tile_rows, a: int, b: int) -> tuple:
+    """[t_lo, t_hi): the tiles whose rows all lie in [a, b)."""
+    tr = np.asarray(tile_rows, dtype=np.int64)
+    t_lo = int(np.searchsorted(tr, a, side="left"))
+    t_hi = int(np.searchsorted(tr, b, side="right")) - 1
+    return t_lo, max(t_lo, t_hi)
+
+
+class SlabExchange:
+    """Halo planes of a slab's local x: the first owned plane goes to
+    rank - 1 (its upper halo), the last to rank + 1 (its lower halo)."""
+
+    def __init__(self, layout: SlabLayout, group=None):
+        self.lay, self.group = layout, group
+
+    def bytes_received(self, itemsize: int = 8) -> int:
+        return self.lay.plane * itemsize * (int(self.lay.has_lo) + int(self.lay.has_hi))
+
+    def start(self, x_local) -> list:
+        """Post the sends / receives (asynchronous); returns the works."""
+        import torch.distributed as dist
+
+        lay, p = self.lay, self.lay.plane
+        ops = []
+        if lay.has_lo:
+            ops.append(dist.P2POp(dist.isend, x_local[lay.own_off:lay.own_off + p],
+                                  lay.rank - 1, group=self.group))
+            ops.append(dist.P2POp(dist.irecv, x_local[0:p], lay.rank - 1, group=self.group))
+        if lay.has_hi:
+            hi = lay.own_off + lay.n_own
+            ops.append(dist.P2POp(dist.isend, x_local[hi - p:hi], lay.rank + 1,
+                                  group=self.group))
+            ops.append(dist.P2POp(dist.irecv, x_local[hi:hi + p], lay.rank + 1,
+                                  group=self.group))
+        return dist.batch_isend_irecv(ops) if ops else []
+
+    def __call__(self, x_local):
+        for w in self.start(x_local):
+            w.wait()
+        return x_local
+
+
+class SlabSpMV:
+    """y_own = A[own rows, :] x on this rank's slab of a generated 3D stencil
+    (natural order, uniform srs / ssrs groups, k = 3)."""
+
+    def __init__(self, shape, points: int, rank: int, world: int, srs: int = 8,
+                 ssrs: int = 8, device=None, f32: bool = False, group=None):
+        from . import synthetic
+
+        self.lay = SlabLayout.of(shape, rank, world)
+        lay = self.lay
+        self.dev = synthetic.device_slab((lay.nz, lay.ny, lay.nx), points, lay.z0, lay.z1,
+                                         device=device).group_uniform(srs, ssrs)
+        if self.dev.n_cols != lay.n_cols or self.dev.n_rows != lay.n_own:
+            raise AssertionError("slab generator and layout disagree")
+        if f32:
+            self.dev.ensure_f32()
+        self.f32 = f32
+        self.nnz_local = self.dev.nnz
+        self.n_tiles = self.dev.plan()["n_tiles"]
+        self.t_lo, self.t_hi = interior_tiles(self.dev.tile_rows(), *lay.interior_rows())
+        self.exchange = SlabExchange(lay, group)
+
+    def step(self, x_local, y_own):
+        """Exchange the halo planes while the interior tiles run, then the
+        boundary tiles, ordered on the current stream (the NCCL works wait on
+        it and it waits on them)."""
+        import torch
+
+        works = self.exchange.start(x_local) if self.lay.world > 1 else []
+        return self.compute(x_local, y_own, works)
+
+    def compute(self, x_local, y_own, works=()):
+        """Interior tiles, then wait for ``works`` (the halo), then the
+        boundary tiles; a complete local x needs no works."""
+        import torch
+
+        s = torch.cuda.current_stream(x_local.device).cuda_stream
+        xp, yp = x_local.data_ptr(), y_own.data_ptr()
+        self.dev.spmv_tiles_ptr(xp, yp, self.t_lo, self.t_hi, s, f32=self.f32)
+        for w in works:
+            w.wait()
+        if self.t_lo > 0:
+            self.dev.spmv_tiles_ptr(xp, yp, 0, self.t_lo, s, f32=self.f32)
+        if self.t_hi < self.n_tiles:
+            self.dev.spmv_tiles_ptr(xp, yp, self.t_hi, self.n_tiles, s, f32=self.f32)
+        return y_own
+
+    @property
+    def launches_per_step(self) -> int:
+        return int(self.t_hi > self.t_lo) + int(self.t_lo > 0) + int(self.t_hi < self.n_tiles)
+
+
+class DistCG:
+    """Conjugate gradients on a slab-partitioned operator (BASELINE config
+    C4: repeated SpMVs as a CG inner loop, at N GPUs).
+
+    ``op`` has ``.lay`` (a SlabLayout) and ``.step(x_local, y_own)`` (halo
+    exchange + local SpMV).  Vectors are this rank's slices; the search
+    direction lives in a local-x buffer so its halo planes can be exchanged.
+    The two dot products per iteration are all-reduced over the ranks; all
+    scalars stay on the device (no host synchronisation per iteration).
+    Classic CG, the same recurrence as csrk_cg (csrc/cg.cu)."""
+
+    def __init__(self, op, group=None):
+        self.op, self.group = op, group
+
+    def _dot(self, a, b):
+        import torch
+        import torch.distributed as dist
+
+        d = torch.dot(a.double(), b.double()).reshape(1)
+        if dist.is_initialized():
+            dist.all_reduce(d, group=self.group)
+        return d
+
+    def run(self, b_own, x_own, iters: int, scratch=None):
+        """``iters`` CG iterations from x_own (updated in place); returns
+        (x_own, rr) with rr the device tensor of the last r.r."""
+        import torch
+
+        lay = self.op.lay
+        own = slice(lay.own_off, lay.own_off + lay.n_own)
+        if scratch is None:
+            scratch = (torch.zeros(lay.n_cols, dtype=b_own.dtype, device=b_own.device),
+                       torch.empty_like(b_own), torch.empty_like(b_own))
+        p_local, r, ap = scratch
+        p = p_local[own]
+        p.copy_(x_own)
+        self.op.step(p_local, ap)  # ap = A x0
+        torch.sub(b_own, ap, out=r)
+        p.copy_(r)
+        rr = self._dot(r, r)
+        for _ in range(iters):
+            self.op.step(p_local, ap)
+            alpha = rr / self._dot(p, ap)
+            x_own.add_(p * alpha.to(p.dtype))
+            r.sub_(ap * alpha.to(ap.dtype))
+            rr_new = self._dot(r, r)
+            beta = rr_new / rr
+            p.mul_(beta.to(p.dtype)).add_(r)
+            rr = rr_new
+        return x_own, rr
 
 
 def partition_by_nnz(row_ptr, sr_ptr, ssr_ptr, n_parts: int) -> np.ndarray:
@@ -238,9 +463,253 @@ def _cached_build(cfg: str, rank: int, log):
     return m, xp, [int(v) for v in z["params"]]
 
 
-def bench_main(args, log):
-    """bench.py --gpus N under torchrun: halo exchange + local SpMV per step,
-    device time max-reduced over ranks."""
+METRIC = "SpMV GFLOP/s and achieved HBM GB/s (% of peak) at 1/2/4/8 B200 vs host CPU"
+
+
+def _max_over_ranks(v: float) -> float:
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([float(v)], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def _sum_over_ranks(v: int) -> int:
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([int(v)], dtype=torch.int64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return int(t.item())
+
+
+def bench_slabs(args, log, rank: int, world: int, local: int, sampler=None, peak=None,
+                side: int = 256):
+    """Weak scaling: every rank owns a C2-sized slab (side^3 rows: side planes
+    of side x side) of the 3D 7-point Laplacian on a side x side x
+    (side * world) grid, generated in its own HBM; one step = one SpMV of the
+    global matrix (halo planes over NCCL overlapped with the interior tiles).
+    Device time with CUDA events, max over ranks; e2e adds the H2D of each
+    rank's x slice and the D2H of its y slice from / to pinned host memory."""
+    import time
+
+    import torch
+    import torch.distributed as dist
+
+    from .bench import spmv_bytes
+
+    shape = (side * world, side, side)
+    dtype = torch.float32 if args.fp32 else torch.float64
+    vb = 4 if args.fp32 else 8
+    op = SlabSpMV(shape, 7, rank, world, device=local, f32=args.fp32)
+    lay = op.lay
+    gen = torch.Generator(device="cuda").manual_seed(1000 + rank)
+    x_local = torch.zeros(lay.n_cols, dtype=dtype, device="cuda")
+    own = slice(lay.own_off, lay.own_off + lay.n_own)
+    x_local[own] = (torch.rand(lay.n_own, generator=gen, device="cuda",
+                               dtype=torch.float64) * 2 - 1).to(dtype)
+    y = torch.empty(lay.n_own, dtype=dtype, device="cuda")
+
+    def step():
+        op.step(x_local, y)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    # untimed load under the clock sampler: the same step count on every
+    # rank (point-to-point exchanges must pair up), ~0.5 s
+    t0 = time.perf_counter()
+    for _ in range(5):
+        step()
+    torch.cuda.synchronize()
+    est = _max_over_ranks((time.perf_counter() - t0) / 5)
+    burn = max(5, int(0.5 / max(est, 1e-6)))
+
+    class _Null:
+        def __enter__(self):
+            return self
+
+        def __exit__(self, *a):
+            return False
+
+        def summary(self):
+            return None
+
+    clk_ctx = sampler(torch.cuda.current_device()) if (sampler and rank == 0) else _Null()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with clk_ctx as clk:
+        for _ in range(burn):
+            step()
+        torch.cuda.synchronize()
+        dist.barrier()
+        torch.cuda.synchronize()
+        ev0.record()
+        for _ in range(args.steps):
+            step()
+        ev1.record()
+        torch.cuda.synchronize()
+        dist.barrier()
+    ms = _max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
+    nnz_total = _sum_over_ranks(op.nnz_local)
+    rows_total = _sum_over_ranks(lay.n_own)
+
+    # e2e: public API per rank with host buffers (x slice up, y slice down)
+    x_pin = torch.empty(lay.n_own, dtype=dtype, pin_memory=True)
+    x_pin.copy_(x_local[own])
+    y_pin = torch.empty(lay.n_own, dtype=dtype, pin_memory=True)
+    e2e_steps = max(3, min(args.steps, 20))
+    for it in range(e2e_steps + 1):
+        if it == 1:
+            torch.cuda.synchronize()
+            dist.barrier()
+            te = time.perf_counter()
+        x_local[own].copy_(x_pin, non_blocking=True)
+        step()
+        y_pin.copy_(y, non_blocking=True)
+        torch.cuda.synchronize()
+    e2e_s = _max_over_ranks((time.perf_counter() - te) / e2e_steps)
+    if rank != 0:
+        return None
+    algo = spmv_bytes(lay.n_own, lay.n_cols, op.nnz_local, vb)
+    gbs = algo / (ms * 1e-3) / 1e9
+    peak_v, peak_src = peak if peak else (None, None)
+    return {
+        "metric": METRIC,
+        "value": round(2.0 * nnz_total / (ms * 1e-3) / 1e9, 2), "unit": "GFLOP/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32" if args.fp32 else "f64",
+        "data": "synthetic (3D 7-point Laplacian generated in HBM per rank, "
+                "x ~ U[-1,1) per rank)",
+        "config": {"workload": f"C2-sized slab per GPU: 3D 7-point Laplacian "
+                               f"{side}x{side}x{side * world} ({side}^3 rows per rank), "
+                               "natural order, CSR-k k=3 uniform SR 8 / SSR 8",
+                   "n_rows": rows_total, "nnz": nnz_total,
+                   "parallelism": f"z-slab row blocks x{world}, NCCL halo planes "
+                                  "overlapped with the interior tiles",
+                   "halo_bytes_per_rank": op.exchange.bytes_received(vb),
+                   "l2": "inputs larger than L2; no flush"},
+        "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": peak_v,
+                     "unit": "GB/s", "frac": round(gbs / peak_v, 4) if peak_v else None,
+                     "peak_source": peak_src, "per": "rank 0's GPU (its slab's "
+                     "algorithmic bytes / the max-over-ranks step time)",
+                     "traffic": None, "algorithmic_bytes_per_launch": algo},
+        "e2e": {"value": round(2.0 * nnz_total / e2e_s / 1e9, 2), "unit": "GFLOP/s",
+                "h2d_bytes_per_step": lay.n_own * vb * world,
+                "d2h_bytes_per_step": lay.n_own * vb * world,
+                "ms_per_step": round(e2e_s * 1e3, 3),
+                "call": "dist.SlabSpMV.step with pinned host x / y slices per rank"},
+        "cpu_baseline": None,
+        "gpu_launches": args.steps * op.launches_per_step,
+        "clocks": clk.summary() if clk is not None else None,
+    }
+
+
+def bench_cg_slabs(args, log, rank: int, world: int, local: int, sampler=None, peak=None):
+    """C4 at N GPUs (strong scaling): the side^3 7-point Laplacian split into
+    z-slabs, ``args.iters`` CG iterations per step (DistCG: halo planes +
+    interior/boundary SpMV + two all-reduced dots per iteration)."""
+    import time
+
+    import torch
+    import torch.distributed as dist
+
+    from .bench import spmv_bytes
+
+    side = args.side
+    shape = (side, side, side)
+    dtype = torch.float32 if args.fp32 else torch.float64
+    vb = 4 if args.fp32 else 8
+    op = SlabSpMV(shape, 7, rank, world, device=local, f32=args.fp32)
+    lay = op.lay
+    solver = DistCG(op)
+    gen = torch.Generator(device="cuda").manual_seed(2000 + rank)
+    b = (torch.rand(lay.n_own, generator=gen, device="cuda", dtype=torch.float64) * 2
+         - 1).to(dtype)
+    x = torch.zeros_like(b)
+    scratch = (torch.zeros(lay.n_cols, dtype=dtype, device="cuda"), torch.empty_like(b),
+               torch.empty_like(b))
+    iters = args.iters
+
+    def step():
+        x.zero_()
+        solver.run(b, x, iters, scratch=scratch)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    clk_ctx = sampler(torch.cuda.current_device()) if (sampler and rank == 0) else None
+    if clk_ctx is not None:
+        clk_ctx.__enter__()
+    step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    for _ in range(args.steps):
+        step()
+    ev1.record()
+    torch.cuda.synchronize()
+    dist.barrier()
+    if clk_ctx is not None:
+        clk_ctx.__exit__(None, None, None)
+    ms = _max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
+    nnz_total = _sum_over_ranks(op.nnz_local)
+    b_pin = torch.empty(lay.n_own, dtype=dtype, pin_memory=True)
+    b_pin.copy_(b)
+    x_pin = torch.empty(lay.n_own, dtype=dtype, pin_memory=True)
+    torch.cuda.synchronize()
+    dist.barrier()
+    te = time.perf_counter()
+    e2e_steps = 2
+    for _ in range(e2e_steps):
+        b.copy_(b_pin, non_blocking=True)
+        step()
+        x_pin.copy_(x, non_blocking=True)
+        torch.cuda.synchronize()
+    e2e_s = _max_over_ranks((time.perf_counter() - te) / e2e_steps)
+    if rank != 0:
+        return None
+    flops = 2.0 * nnz_total * iters
+    it_bytes = spmv_bytes(lay.n_own, lay.n_cols, op.nnz_local, vb) + 11 * lay.n_own * vb
+    gbs = it_bytes * iters / (ms * 1e-3) / 1e9
+    peak_v, peak_src = peak if peak else (None, None)
+    return {
+        "metric": METRIC, "value": round(flops / (ms * 1e-3) / 1e9, 2), "unit": "GFLOP/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32" if args.fp32 else "f64",
+        "data": "synthetic (7-point Laplacian slabs generated in HBM, b ~ U[-1,1))",
+        "config": {"workload": f"C4: {iters} SpMVs as a CG inner loop on the {side}^3 "
+                               f"7-point Laplacian, z-slabs over {world} GPUs",
+                   "config_id": "C4", "nnz": nnz_total, "iterations_per_step": iters,
+                   "parallelism": f"z-slab row blocks x{world}, NCCL halo planes + "
+                                  "2 all-reduces per iteration",
+                   "ms_per_iteration": round(ms / iters, 5)},
+        "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": peak_v, "unit": "GB/s",
+                     "frac": round(gbs / peak_v, 4) if peak_v else None,
+                     "peak_source": peak_src, "per": "rank 0's GPU", "traffic": None,
+                     "algorithmic_bytes_per_iteration": int(it_bytes)},
+        "e2e": {"value": round(flops / e2e_s / 1e9, 2), "unit": "GFLOP/s",
+                "h2d_bytes_per_step": lay.n_own * vb * world,
+                "d2h_bytes_per_step": lay.n_own * vb * world,
+                "ms_per_step": round(e2e_s * 1e3, 3), "call": "dist.DistCG.run per rank"},
+        "cpu_baseline": None,
+        "gpu_launches": args.steps * iters * op.launches_per_step,
+        "clocks": clk_ctx.summary() if clk_ctx is not None else None,
+    }
+
+
+def bench_main(args, log, sampler=None, peak=None):
+    """bench.py --gpus N under torchrun.  C2 (the default): weak scaling over
+    C2-sized slabs (bench_slabs).  Other configs: the config's CSR-k matrix
+    partitioned by nonzeros over the ranks (strong scaling), halo exchange +
+    local SpMV per step.  Device time max-reduced over ranks."""
     import torch
     import torch.distributed as dist
 
@@ -253,6 +722,12 @@ def bench_main(args, log):
     from . import _native as nat
     nat.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if args.config in ("C2", "C4"):
+        fn = bench_slabs if args.config == "C2" else bench_cg_slabs
+        try:
+            return fn(args, log, rank, world, local, sampler, peak)
+        finally:
+            dist.destroy_process_group()
     m, xp, (ssrs, srs) = _cached_build(args.config, rank, log)
     mode = os.environ.get("CSRK_EXCHANGE", "halo")
     op = DistSpMV(m, rank, world, mode=mode, device=local, f32=args.fp32)

@@ -180,3 +180,21 @@ def device_stencil(shape, points: int, device=None):
     nat.call("csrk_stencil", nat.current_device() if device is None else device,
              dims[0], dims[1], dims[2], int(points), C.byref(out))
     return nat.DeviceMatrix(out)
+
+
+def device_slab(shape, points: int, z0: int, z1: int, device=None):
+    """Rows of planes [z0, z1) of a 3D stencil generated in HBM
+    (csrk_stencil_slab): natural order, columns numbered from plane
+    max(z0 - 1, 0), so x is [lower halo plane | own planes | upper halo
+    plane].  Returns a k = 1 ``_native.DeviceMatrix``; its rows equal rows
+    [z0 * ny * nx, z1 * ny * nx) of :func:`device_stencil` with the columns
+    shifted by ``max(z0 - 1, 0) * ny * nx``."""
+    import ctypes as C
+
+    from . import _native as nat
+
+    nz, ny, nx = (int(s) for s in shape)
+    out = C.c_void_p()
+    nat.call("csrk_stencil_slab", nat.current_device() if device is None else device,
+             nz, ny, nx, int(points), int(z0), int(z1), C.byref(out))
+    return nat.DeviceMatrix(out)

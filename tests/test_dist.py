@@ -141,3 +141,187 @@ def test_partitioned_device_spmv_reassembles_bitwise():
                                           ssr_ptr=blk.ssr_ptr)
             ys.append(dev.spmv_host(x) if blk.r1 > blk.r0 else np.zeros(0))
         np.testing.assert_array_equal(np.concatenate(ys), want)
+
+
+def _host_slab(shape, points, lay):
+    """The rows of a slab from the host generator, columns shifted to the
+    slab's local x (what csrk_stencil_slab writes)."""
+    n, rp, ci, va = synthetic.stencil_arrays(shape, points, values="uniform")
+    r0, r1 = lay.global_row0, lay.global_row0 + lay.n_own
+    p0, p1 = int(rp[r0]), int(rp[r1])
+    base = lay.global_row0 - lay.own_off
+    return ((rp[r0:r1 + 1] - p0).astype(np.uint32), (ci[p0:p1] - base).astype(np.uint32),
+            va[p0:p1], (n, rp, ci, va))
+
+
+@pytest.mark.parametrize("nz,world", [(1, 1), (7, 1), (7, 2), (8, 3), (9, 9), (16, 5)])
+def test_slab_layout(nz, world):
+    shape = (nz, 3, 4)
+    lays = [D.SlabLayout.of(shape, g, world) for g in range(world)]
+    assert sum(l.n_own for l in lays) == nz * 12
+    assert lays[0].global_row0 == 0 and not lays[0].has_lo and not lays[-1].has_hi
+    for g, lay in enumerate(lays):
+        assert lay.n_own >= 12
+        assert lay.n_cols == lay.n_own + 12 * (int(g > 0) + int(g < world - 1))
+        a, b = lay.interior_rows()
+        assert 0 <= a <= b <= lay.n_own
+        rp, ci, _, _ = _host_slab(shape, 7, lay)
+        assert int(ci.max()) < lay.n_cols
+        for r in range(lay.n_own):  # interior rows read owned x only
+            cols = ci[rp[r]:rp[r + 1]]
+            inside = (cols >= lay.own_off).all() and (cols < lay.own_off + lay.n_own).all()
+            if a <= r < b:
+                assert inside
+    with pytest.raises(ValueError):
+        D.slab_cuts(2, 3)
+
+
+def test_interior_tiles():
+    tr = np.array([0, 5, 9, 14, 20, 26, 30])
+    assert D.interior_tiles(tr, 5, 26) == (1, 5)
+    assert D.interior_tiles(tr, 6, 25) == (2, 4)
+    assert D.interior_tiles(tr, 0, 30) == (0, 6)
+    assert D.interior_tiles(tr, 10, 12) == (3, 3)
+
+
+def _slab_worker(rank, world, port, shape, points, result_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        lay = D.SlabLayout.of(shape, rank, world)
+        rp, ci, va, (n, grp, gci, gva) = _host_slab(shape, points, lay)
+        x = np.random.default_rng(7).uniform(-1, 1, n)
+        x_local = torch.full((lay.n_cols,), float("nan"), dtype=torch.float64)
+        g0 = lay.global_row0
+        x_local[lay.own_off:lay.own_off + lay.n_own] = torch.from_numpy(x[g0:g0 + lay.n_own])
+        ex = D.SlabExchange(lay)
+        ex(x_local)
+        base = g0 - lay.own_off
+        ok_x = bool(torch.equal(x_local, torch.from_numpy(x[base:base + lay.n_cols])))
+        y = O.spmv_serial(rp, ci, va, x_local.numpy())
+        want = O.spmv_serial(grp, gci, gva, x)[g0:g0 + lay.n_own]
+        result_q.put((rank, ok_x, bool(np.array_equal(y, want)), ex.bytes_received()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,shape,points", [(2, (6, 5, 4), 7), (3, (7, 4, 5), 27)])
+def test_slab_exchange_over_gloo(world, shape, points):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_slab_worker, args=(r, world, port, shape, points, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    results = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, ok_x, ok_y, nbytes in results:
+        assert ok_x, f"rank {rank}: halo planes not filled"
+        assert ok_y, f"rank {rank}: slab SpMV differs from the global rows"
+        assert nbytes == 8 * shape[1] * shape[2] * (int(rank > 0) + int(rank < world - 1))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("points", [7, 27])
+def test_device_slabs_reassemble_bitwise(points):
+    """csrk_stencil_slab equals the host rows bit for bit, and the per-rank
+    interior + boundary tile launches reassemble the global y."""
+    shape = (23, 17, 19)
+    n, rp, ci, va = synthetic.stencil_arrays(shape, points, values="laplacian")
+    x = np.random.default_rng(11).uniform(-1, 1, n)
+    want = O.spmv_serial(rp, ci, va, x)
+    for world in (1, 2, 3, 5):
+        ys = []
+        for g in range(world):
+            op = D.SlabSpMV(shape, points, g, world)
+            lay = op.lay
+            hrp, hci, hva, _ = _host_slab(shape, points, lay)
+            drp, dci, dva, _, _ = op.dev.download()
+            np.testing.assert_array_equal(drp, hrp)
+            np.testing.assert_array_equal(dci, hci)
+            np.testing.assert_array_equal(dva, hva)
+            base = lay.global_row0 - lay.own_off
+            xl = torch.from_numpy(x[base:base + lay.n_cols].copy()).cuda()
+            y = torch.empty(lay.n_own, dtype=torch.float64, device="cuda")
+            op.compute(xl, y)
+            torch.cuda.synchronize()
+            ys.append(y.cpu().numpy())
+        np.testing.assert_array_equal(np.concatenate(ys), want)
+
+
+class _HostSlabOp:
+    """CPU stand-in for SlabSpMV (exchange over gloo, oracle SpMV)."""
+
+    def __init__(self, shape, points, rank, world):
+        self.lay = D.SlabLayout.of(shape, rank, world)
+        self.rp, self.ci, self.va, _ = _host_slab(shape, points, self.lay)
+        self.ex = D.SlabExchange(self.lay)
+
+    def step(self, x_local, y_own):
+        if self.lay.world > 1:
+            self.ex(x_local)
+        y_own.copy_(torch.from_numpy(O.spmv_serial(self.rp, self.ci, self.va,
+                                                   x_local.numpy())))
+        return y_own
+
+
+def _cg_worker(rank, world, port, shape, iters, result_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        op = _HostSlabOp(shape, 7, rank, world)
+        n = shape[0] * shape[1] * shape[2]
+        b = np.random.default_rng(5).uniform(-1, 1, n)
+        g0 = op.lay.global_row0
+        b_own = torch.from_numpy(b[g0:g0 + op.lay.n_own].copy())
+        x_own = torch.zeros_like(b_own)
+        x_own, rr = D.DistCG(op).run(b_own, x_own, iters)
+        result_q.put((rank, g0, x_own.numpy(), float(rr.item())))
+    finally:
+        dist.destroy_process_group()
+
+
+def _numpy_cg(shape, b, iters):
+    n, rp, ci, va = synthetic.stencil_arrays(shape, 7, values="uniform")
+    a = lambda v: O.spmv_serial(rp, ci, va, v)  # noqa: E731
+    x = np.zeros(n)
+    r = b - a(x)
+    p = r.copy()
+    rr = r @ r
+    for _ in range(iters):
+        ap = a(p)
+        alpha = rr / (p @ ap)
+        x += alpha * p
+        r -= alpha * ap
+        rr_new = r @ r
+        p = r + (rr_new / rr) * p
+        rr = rr_new
+    return x, rr
+
+
+@pytest.mark.parametrize("world", [1, 2, 3])
+def test_dist_cg_over_gloo(world):
+    """Slab-partitioned CG (halo planes + all-reduced dots) equals one-process
+    CG on the whole matrix to rounding."""
+    shape, iters = (9, 6, 5), 12
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_cg_worker, args=(r, world, port, shape, iters, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    results = sorted([q.get(timeout=300) for _ in range(world)], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    x = np.concatenate([t[2] for t in results])
+    b = np.random.default_rng(5).uniform(-1, 1, x.size)
+    want, rr = _numpy_cg(shape, b, iters)
+    np.testing.assert_allclose(x, want, rtol=1e-9, atol=1e-12)
+    assert all(abs(t[3] - rr) <= 1e-9 * max(rr, 1e-300) + 1e-300 for t in results)

@@ -298,3 +298,78 @@ def test_plan_geometry_checks():
     plan = dev.plan()
     assert plan["tile_cost"] == 512 and plan["stages"] == 2
     assert plan["n_tiles"] == -(-(a.nnz + a.n_rows) // 512)
+
+
+def _mixed_rows_matrix(rng, n):
+    """Rows of 0..60 nonzeros (mean > 16, variance >> 10) plus a few long
+    rows: exercises every schedule's inline, gather-first and direct paths."""
+    lens = rng.integers(0, 61, n)
+    lens[rng.choice(n, 5, replace=False)] = 3000
+    rows = np.repeat(np.arange(n), lens)
+    cols = rng.integers(0, n, len(rows))
+    return ck.csr_from_arrays(n, n, rows, cols, rng.uniform(-1.0, 1.0, len(rows)))
+
+
+@pytest.mark.parametrize("gather,ctas", [(0, 0), (1, 0), (2, 0), (0, 1), (1, 2), (2, 3),
+                                         (0, 4), (1, 8)])
+def test_schedules_do_not_change_bits(gather, ctas):
+    """Gather mode x CTAs/SM x tile plan: y is the oracle's bit for bit in
+    both orders (f64) and within 1e-5 of |A||x| (f32)."""
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(10 * gather + ctas)
+    n = 30000
+    a = _mixed_rows_matrix(rng, n)
+    res = ck.band_k(a, 3, [4, 8])
+    m = ck.pack_csrk(a, res.perm, res.level_group_sizes)
+    x = rng.uniform(-1.0, 1.0, n)
+    rp, ci, va = m.base.row_ptr, m.base.col_idx, m.base.vals
+    want = O.spmv_serial(rp, ci, va, x)
+    want4 = O.spmv_strided(rp, ci, va, x, 4)
+    scale = O.abs_row_dot(rp, ci, va, x)
+    dev = m.device()
+    dev.set_schedule(gather, ctas)
+    for tile_cost, stages in ((0, 0), (256, 3), (4096, 2)):
+        dev.set_plan(tile_cost, 0, stages)
+        plan = dev.plan()
+        assert plan["gather_first"] == gather
+        assert plan["ctas_per_sm"] == (ctas or 2)  # variance >> 10: irregular
+        np.testing.assert_array_equal(ck.spmv_csr3(m, x), want)
+        np.testing.assert_array_equal(ck.spmv_gpu35(m, x, ck.BlockDims(4, 8, 12)), want4)
+        xd = torch.from_numpy(x).cuda().float()
+        y32 = ck.spmv_device(m, xd)
+        torch.cuda.synchronize()
+        assert (np.abs(y32.cpu().double().numpy() - want) / np.maximum(scale, 1e-300)).max() <= 1e-5
+
+
+def test_schedule_argument_checks():
+    rng = np.random.default_rng(3)
+    dev = random_csr(rng, 300, 300, 0.02).device()
+    with pytest.raises(ValueError, match="gather"):
+        dev.set_schedule(3, 0)
+    with pytest.raises(ValueError, match="ctas_per_sm"):
+        dev.set_schedule(0, 9)
+
+
+@pytest.mark.parametrize("shape,d2h,xcut", [("u1", "host", "footprint"), ("u3", "event", "rows"),
+                                            ("r1", "host", "rows"), ("r12", "event", "footprint"),
+                                            ("u40", "host", "footprint")])
+def test_pipeline_shapes_bitwise(monkeypatch, shape, d2h, xcut):
+    """Every host-pipeline chunking / ordering gives the plain path's bits."""
+    torch = pytest.importorskip("torch")
+    n, rp, ci, va = synthetic.stencil_arrays((64, 128, 160), 7, values="uniform")
+    a = ck.CsrMatrix(n, n, rp, ci, va)
+    res = ck.band_k(a, 3, [8, 8])
+    m = ck.pack_csrk(a, res.perm, res.level_group_sizes)
+    x = np.random.default_rng(5).uniform(-1.0, 1.0, n)
+    want = O.spmv_grouped(O.csr3_group_rows(m.sr_ptr, m.ssr_ptr), m.base.row_ptr,
+                          m.base.col_idx, m.base.vals, x, 4)
+    monkeypatch.setenv("CSRK_PIPE_SHAPE", shape)
+    monkeypatch.setenv("CSRK_PIPE_D2H", d2h)
+    monkeypatch.setenv("CSRK_PIPE_XCUT", xcut)
+    x_pin = torch.empty(n, dtype=torch.float64, pin_memory=True).numpy()
+    y_pin = torch.empty(n, dtype=torch.float64, pin_memory=True).numpy()
+    x_pin[:] = x
+    for _ in range(2):
+        y_pin[:] = np.nan
+        ck.spmv_csr3(m, x_pin, out=y_pin)
+        np.testing.assert_array_equal(y_pin, want)
