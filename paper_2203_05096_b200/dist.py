@@ -254,12 +254,12 @@ class DistCG:
         rr = self._dot(r, r)
         for _ in range(iters):
             self.op.step(p_local, ap)
-            alpha = rr / self._dot(p, ap)
-            x_own.add_(p * alpha.to(p.dtype))
-            r.sub_(ap * alpha.to(ap.dtype))
+            alpha = (rr / self._dot(p, ap)).to(p.dtype)
+            x_own.addcmul_(p, alpha)  # x += alpha p (no temporaries)
+            r.addcmul_(ap, alpha, value=-1.0)
             rr_new = self._dot(r, r)
-            beta = rr_new / rr
-            p.mul_(beta.to(p.dtype)).add_(r)
+            beta = (rr_new / rr).to(p.dtype)
+            torch.addcmul(r, p, beta, out=p)  # p = r + beta p
             rr = rr_new
         return x_own, rr
 

@@ -143,10 +143,10 @@ def test_partitioned_device_spmv_reassembles_bitwise():
         np.testing.assert_array_equal(np.concatenate(ys), want)
 
 
-def _host_slab(shape, points, lay):
+def _host_slab(shape, points, lay, values="uniform"):
     """The rows of a slab from the host generator, columns shifted to the
-    slab's local x (what csrk_stencil_slab writes)."""
-    n, rp, ci, va = synthetic.stencil_arrays(shape, points, values="uniform")
+    slab's local x (what csrk_stencil_slab writes with Laplacian values)."""
+    n, rp, ci, va = synthetic.stencil_arrays(shape, points, values=values)
     r0, r1 = lay.global_row0, lay.global_row0 + lay.n_own
     p0, p1 = int(rp[r0]), int(rp[r1])
     base = lay.global_row0 - lay.own_off
@@ -239,7 +239,7 @@ def test_device_slabs_reassemble_bitwise(points):
         for g in range(world):
             op = D.SlabSpMV(shape, points, g, world)
             lay = op.lay
-            hrp, hci, hva, _ = _host_slab(shape, points, lay)
+            hrp, hci, hva, _ = _host_slab(shape, points, lay, values="laplacian")
             drp, dci, dva, _, _ = op.dev.download()
             np.testing.assert_array_equal(drp, hrp)
             np.testing.assert_array_equal(dci, hci)

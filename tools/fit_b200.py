@@ -31,6 +31,7 @@ FAMILY = [
     ("stencil3d7", lambda: synthetic.stencil_arrays((160, 160, 160), 7)),
     ("stencil2d9", lambda: synthetic.stencil_arrays((2000, 2000), 9)),
     ("stencil3d27", lambda: synthetic.stencil_arrays((100, 100, 100), 27)),
+    ("stencil3d27_l", lambda: synthetic.stencil_arrays((160, 160, 160), 27)),
     ("irreg_l5", lambda: _irregular(6_000_000, 5)),
     ("irreg_l11", lambda: _irregular(3_000_000, 11)),
     ("irreg_l19", lambda: _irregular(2_000_000, 19)),

@@ -5,12 +5,16 @@ Then, as the paper does for Volta / Ampere with the
 reference's fit_log_model (tuning.py:444-468):
 
   ssrs_coeff, srs_coeff  least-squares fits of size = a - b ln(rdensity)
-                         over the per-matrix optima;
-  case table             the paper's four row-density intervals; dims.x of
-                         each = the lane count that won most often inside it
-                         (the strided order's nx), no size adjustments
-                         (the fitted formulas already are B200 optima);
-  serial threshold       the largest rdensity at which the serial order won.
+                         over the per-matrix optima (the geometric centre of
+                         the sizes within 2 % of the best time: the argmin
+                         of a near-flat grid is noise);
+  case table             the paper's four row-density intervals, no size
+                         adjustments (the fitted formulas already are B200
+                         optima);
+  serial threshold       the geometric midpoint between the densest matrix the
+                         serial order won and the next denser strided win;
+                         case dims.x = the lane count with the smallest mean
+                         slowdown over the interval's strided winners.
 
 Writes paper_2203_05096_b200/data/b200.json (profile keys plus a "fit"
 record of the measurements it came from).
@@ -50,28 +54,62 @@ def best_of(rec):
     return best
 
 
+def strided_best(rec, nx):
+    return min(r[f"strided{nx}_ms"] for r in rec["runs"])
+
+
+NEAR = 1.02  # run-to-run noise of a CUDA-event median (repeat runs of the fit)
+
+
+def near_center(rec, nx, best_ms):
+    """Group sizes the fit uses for one matrix: the geometric centre of every
+    (SSRS, SRS) whose time in the winning variant is within NEAR of the best.
+    Group sizes move B200 time by only a few percent once the tile plan fits
+    a stage, so 14-26 of the 30 grid points tie within the noise and the
+    plain argmin is a coin toss; the centre of the tied set is stable."""
+    key = "serial_ms" if nx == 0 else f"strided{nx}_ms"
+    near = [(r["ssrs"], r["srs"]) for r in rec["runs"] if r[key] <= best_ms * NEAR]
+    ls = sum(math.log2(a) for a, _ in near) / len(near)
+    lr = sum(math.log2(b) for _, b in near) / len(near)
+    return 2.0 ** ls, 2.0 ** lr, len(near)
+
+
 def main(path):
     with open(path) as fh:
         data = json.load(fh)
     rows = []
     for name, rec in sorted(data.items(), key=lambda kv: kv[1]["rdensity"]):
-        ms, ssrs, srs, nx = best_of(rec)
+        ms, ssrs_arg, srs_arg, nx = best_of(rec)
+        ssrs, srs, n_near = near_center(rec, nx, ms)
         serial_ms = min(r["serial_ms"] for r in rec["runs"])
         rows.append({"matrix": name, "rdensity": rec["rdensity"], "variance": rec["variance"],
-                     "nnz": rec["nnz"], "best_ms": ms, "ssrs": ssrs, "srs": srs,
+                     "nnz": rec["nnz"], "best_ms": ms, "ssrs": round(ssrs, 3),
+                     "srs": round(srs, 3), "argmin_ssrs": ssrs_arg, "argmin_srs": srs_arg,
+                     "n_within_2pct": n_near,
                      "nx": nx, "serial_best_ms": serial_ms,
                      "gflops": round(2 * rec["nnz"] / (ms * 1e-3) / 1e9, 1)})
     ssrs_coeff = T.fit_log_model([(r["rdensity"], r["ssrs"]) for r in rows])
     srs_coeff = T.fit_log_model([(r["rdensity"], r["srs"]) for r in rows])
+    # serial threshold: the decision boundary between the densest matrix the
+    # serial order won and the next denser one the strided order won
+    # (geometric midpoint), not the last serial win itself -- a matrix just
+    # above the densest serial win belongs to the serial side of the gap
     serial_rd = [r["rdensity"] for r in rows if r["nx"] == 0]
     threshold = max(serial_rd) if serial_rd else 0.0
+    above = [r["rdensity"] for r in rows if r["nx"] > 0 and r["rdensity"] > threshold]
+    if serial_rd and above:
+        threshold = math.sqrt(threshold * min(above))
     cases = []
     lo = 0.0
     for upper, default in zip(UPPERS, DEFAULT_DIMS):
         inside = [r for r in rows if r["rdensity"] > lo and (upper is None or r["rdensity"] <= upper)
                   and r["nx"] > 0]
         if inside:
-            nx = collections.Counter(r["nx"] for r in inside).most_common(1)[0][0]
+            # the lane count with the smallest mean slowdown against each
+            # matrix's best time inside the interval (a vote would split)
+            cand = sorted({r["nx"] for r in inside})
+            nx = min(cand, key=lambda c: sum(strided_best(data[r["matrix"]], c) / r["best_ms"]
+                                             for r in inside))
             dims = BlockDims(nx, default[1], max(1, default[2]) if nx * default[1] * default[2]
                              <= 1024 else 1)
         else:
