@@ -338,6 +338,7 @@ int csrk_matrix_set_plan(csrk_matrix *m, int64_t tile_cost, int64_t cap,
   }
   CSRK_CUDA_TRY(cudaSetDevice(m->device));
   CSRK_TRY(ensure_plan(m, tile_cost, cap, stages, m->stream));
+  m->plan.auto_tile = tile_cost <= 0;
   CSRK_CUDA_TRY(cudaStreamSynchronize(m->stream));
   return CSRK_OK;
 }
@@ -349,6 +350,7 @@ int csrk_spmv(const csrk_matrix *m, int value_type, int variant, int nx,
     return CSRK_EINVAL;
   }
   CSRK_CUDA_TRY(cudaSetDevice(m->device));
+  CSRK_TRY(prepare_plan(m, variant, nx));
   return launch_spmv(m, value_type, variant, nx, x, y,
                      static_cast<cudaStream_t>(stream));
 }
@@ -506,6 +508,7 @@ int csrk_spmv_host(csrk_matrix *m, int value_type, int variant, int nx,
   }
   const size_t es = value_type == CSRK_F32 ? sizeof(float) : sizeof(double);
   CSRK_CUDA_TRY(cudaSetDevice(m->device));
+  CSRK_TRY(prepare_plan(m, variant, nx));
   const size_t xb = static_cast<size_t>(m->n_cols) * es + 16;
   const size_t yb = static_cast<size_t>(m->n_rows) * es + 16;
   if (m->x_stage_bytes < xb) {

@@ -36,6 +36,32 @@ inline bool auto_gather(int variant, double mean_row) {
   return variant == CSRK_SERIAL && mean_row > 16.0;
 }
 
+// Tile cost for a launch in the STRIDED order: the 256 consumer threads
+// hold 256 / P rows per pass (P = nx rounded up to a power of two), and a
+// tile whose last pass is mostly empty idles that share of the threads until
+// the stage is released.  When the default 2048-cost tile fills its passes
+// below 85 %, shrink it to a whole number of full passes (5 % slack for the
+// row-count spread of group-aligned cuts).  C3 (27-nonzero rows) with nx = 4:
+// 74 rows = 1.2 passes of 64 -> 1684-cost tiles of ~61 rows, 5.1 -> 5.6 TB/s
+// (profiles/r01_sched_sweep.txt).  The serial order keeps 2048: short rows
+// fill 256 rows per tile, long rows gather first.
+inline int64_t auto_tile_cost(double mean_row, int variant, int nx) {
+  if (variant != CSRK_STRIDED) return kDefaultTileCost;
+  int p = 1;
+  while (p < nx) p <<= 1;
+  const double per_row = mean_row + 1.0;
+  const double slots = 256.0 / p;
+  const double rows = static_cast<double>(kDefaultTileCost) / per_row;
+  const double passes = rows / slots > 1.0 ? static_cast<double>(static_cast<int64_t>(rows / slots + 0.999999)) : 1.0;
+  if (rows / (passes * slots) >= 0.85) return kDefaultTileCost;
+  double full = static_cast<double>(static_cast<int64_t>(rows / slots));
+  if (full < 1.0) full = 1.0;
+  int64_t tc = static_cast<int64_t>(full * slots * per_row * 0.95);
+  if (tc > kDefaultTileCost) tc = kDefaultTileCost;
+  if (tc < 512) tc = 512;
+  return tc;
+}
+
 struct TilePlan {
   int64_t tile_cost = 0;  // requested nonzeros + rows per tile
   int64_t cap = 0;        // stage capacity, nonzeros
@@ -50,6 +76,7 @@ struct TilePlan {
   int ctas_per_sm = 0;
   double mean_row = 0.0, row_var = 0.0;
   bool row_stats = false;
+  bool auto_tile = true;  // tile cost follows the launch's order (auto_tile_cost)
   uint32_t *tile_row = nullptr;  // device, n_tiles + 1
 };
 
@@ -104,6 +131,9 @@ inline int64_t padded_rows(int64_t n_rows) { return ((n_rows + 1 + 3) / 4) * 4 +
 int alloc_matrix_arrays(csrk_matrix *m, bool want64, bool want32);
 int ensure_plan(csrk_matrix *m, int64_t tile_cost, int64_t cap, int64_t stages,
                 cudaStream_t s);
+// before a whole-matrix launch: re-plan for the launch's order when the plan
+// is automatic (cached; rebuilds only when the tile cost changes)
+int prepare_plan(const csrk_matrix *m, int variant, int nx);
 int launch_spmv(const csrk_matrix *m, int value_type, int variant, int nx,
                 const void *x, void *y, cudaStream_t stream, int64_t t0 = 0,
                 int64_t t1 = -1);

@@ -739,12 +739,26 @@ int ensure_plan(csrk_matrix *m, int64_t tile_cost, int64_t cap, int64_t stages,
       m->row_ptr, m->sr_ptr, m->ssr_ptr, cut_k, n_cuts, m->n_rows, pitch,
       n_tiles, m->plan.tile_row);
   CSRK_CUDA_TRY(cudaGetLastError());
+  m->pipe.plan_tiles = -1;  // host-pipeline cuts index the old tiles
   m->plan.tile_cost = tile_cost;
   m->plan.cap = cap;
   m->plan.rcap = rcap;
   m->plan.stages = stages;
   m->plan.n_tiles = n_tiles;
   m->plan.group_aligned = cut_k != 1 || m->k == 1;
+  return CSRK_OK;
+}
+
+int prepare_plan(const csrk_matrix *cm, int variant, int nx) {
+  csrk_matrix *m = const_cast<csrk_matrix *>(cm);  // the plan is a cache
+  if (!m->plan.auto_tile || m->n_rows == 0) return CSRK_OK;
+  if (!m->plan.row_stats) CSRK_TRY(ensure_plan(m, 0, 0, 0, m->stream));
+  const int64_t tc = auto_tile_cost(m->plan.mean_row, variant, nx);
+  if (tc == m->plan.tile_cost) return CSRK_OK;
+  const bool keep = m->plan.auto_tile;
+  CSRK_TRY(ensure_plan(m, tc, 0, m->plan.stages, m->stream));
+  m->plan.auto_tile = keep;
+  CSRK_CUDA_TRY(cudaStreamSynchronize(m->stream));
   return CSRK_OK;
 }
 

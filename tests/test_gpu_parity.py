@@ -373,3 +373,37 @@ def test_pipeline_shapes_bitwise(monkeypatch, shape, d2h, xcut):
         y_pin[:] = np.nan
         ck.spmv_csr3(m, x_pin, out=y_pin)
         np.testing.assert_array_equal(y_pin, want)
+
+
+def test_auto_plan_follows_the_order():
+    """An automatic plan re-tiles for strided launches whose rows would leave
+    a pass mostly empty (27-nonzero rows, nx = 4), keeps 2048 for the serial
+    order, and never changes bits -- including the pinned host pipeline run
+    right after a re-plan."""
+    torch = pytest.importorskip("torch")
+    n, rp, ci, va = synthetic.stencil_arrays((100, 100, 105), 27, values="uniform")
+    a = ck.CsrMatrix(n, n, rp, ci, va)  # > 1 M rows: the pinned pipeline engages
+    res = ck.band_k(a, 3, [8, 8])
+    m = ck.pack_csrk(a, res.perm, res.level_group_sizes)
+    x = np.random.default_rng(9).uniform(-1.0, 1.0, n)
+    b = m.base
+    want = O.spmv_serial(b.row_ptr, b.col_idx, b.vals, x)
+    dev = m.device()
+    for _ in range(2):
+        np.testing.assert_array_equal(ck.spmv_csr3(m, x), want)
+        assert dev.plan()["tile_cost"] == 2048
+        for nx in (2, 4, 8):
+            np.testing.assert_array_equal(ck.spmv_gpu35(m, x, ck.BlockDims(nx, 1, 1)),
+                                          O.spmv_strided(b.row_ptr, b.col_idx, b.vals, x, nx))
+            tc = dev.plan()["tile_cost"]
+            assert (tc == 2048) if nx == 2 else (1024 < tc < 2048)
+    x_pin = torch.empty(n, dtype=torch.float64, pin_memory=True).numpy()
+    y_pin = torch.empty(n, dtype=torch.float64, pin_memory=True).numpy()
+    x_pin[:] = x
+    ck.spmv_gpu35(m, x_pin, ck.BlockDims(4, 1, 1), out=y_pin)
+    np.testing.assert_array_equal(y_pin, O.spmv_strided(b.row_ptr, b.col_idx, b.vals, x, 4))
+    ck.spmv_csr3(m, x_pin, out=y_pin)
+    np.testing.assert_array_equal(y_pin, want)
+    dev.set_plan(1000, 0, 2)  # explicit plans stay put
+    ck.spmv_gpu35(m, x, ck.BlockDims(4, 1, 1))
+    assert dev.plan()["tile_cost"] == 1000

@@ -49,7 +49,6 @@ def main():
     for cfg in configs:
         a, m, xp, params, _ = bench.build_matrix(cfg, lambda s: print(s, file=sys.stderr))
         n, nnz = a.n_rows, a.nnz
-        dims = params.block_dims
         variant = "strided" if params.kernel_variant.value == "cuda35" else "serial"
         dev = m.device()
         for dtype in DTYPES:
@@ -57,7 +56,15 @@ def main():
             yd = torch.empty(n, dtype=dtype, device="cuda")
             vb = 8 if dtype == torch.float64 else 4
             variants = VARIANTS.split(',') if VARIANTS else sorted({variant, "serial"})
+            nx_list = [int(v) for v in os.environ.get("SWEEP_NX", "").split(",") if v]
+            if nx_list:  # strided with explicit lane counts: "strided:<nx>"
+                variants = [v for v in variants if v != "strided"] + \
+                    [f"strided:{k}" for k in nx_list]
             for variant_i in variants:
+                dims = params.block_dims
+                if variant_i.startswith("strided:"):
+                    variant_i, k = variant_i.split(":")
+                    dims = ck.BlockDims(int(k), 1, 1)
                 dev.set_plan(0, 0, 0)
                 dev.set_schedule(0, 0)
                 want = ck.spmv_device(m, xd, yd, dims=dims, variant=variant_i).clone()
