@@ -8,9 +8,11 @@
 // here: the nodes of BFS level L+1 are exactly the
 // unvisited neighbours of level L; a node is appended by the FIRST level-L
 // node (in queue order) adjacent to it, so its queue position is the pair
-// (min position of a level-L neighbour, key rank).  Sorting each new level by
-// (component rank, parent position, key rank) reproduces the sequential queue
-// exactly.  All components advance together.
+// (min position of a level-L neighbour, key rank).  Ordering each new level
+// by (component rank, parent position, key rank) reproduces the sequential
+// queue exactly; the frontier is kept in that order, so each parent's
+// children form one run of the next level and only need ranking among
+// themselves.  All components advance together.
 //
 //   krank      rank of every node by (degree, weight, index): one stable sort
 //   components label propagation + pointer jumping; label = min index, which
@@ -116,11 +118,16 @@ __global__ void bfs_seed_kernel(const int32_t *__restrict__ seeds, int64_t k,
   }
 }
 
+// one BFS level; the frontier size is read from the device (`sizes[0]`) and
+// the next level's is counted into `sizes[1]`, so a batch of levels is
+// queued without host round trips (levels past the last do nothing)
 __global__ void bfs_expand_kernel(const int64_t *__restrict__ ptr,
                                   const int32_t *__restrict__ idx,
-                                  const int32_t *__restrict__ frontier, int64_t fsize, int32_t level,
+                                  const int32_t *__restrict__ frontier,
+                                  const int *__restrict__ sizes, int32_t level,
                                   int32_t *__restrict__ depth, int32_t *__restrict__ next,
                                   int *__restrict__ next_count) {
+  const int64_t fsize = sizes[0];
   GSTRIDE(i, fsize) {
     const int32_t v = frontier[i];
     for (int64_t p = ptr[v]; p < ptr[v + 1]; ++p) {
@@ -151,71 +158,137 @@ __global__ void last_level_kernel(const int32_t *__restrict__ depth,
 }
 
 // ---- Cuthill-McKee levels ----------------------------------------------
+//
+// The frontier is kept in queue order -- by (component rank, position) --
+// so a frontier INDEX orders parents exactly as their positions do.  A new
+// node is claimed by the smallest index of a frontier neighbour; the
+// children of one parent then form one contiguous run of the next level
+// (runs in parent order), ordered inside by key rank.  Per level: claim,
+// count per parent, an exclusive scan, and a placement that ranks each
+// parent's children by counting -- no sort of the level.
+
+constexpr int32_t kBigDegree = 128;  // parents of larger degree: block path
 
 __global__ void cm_claim_kernel(const int64_t *__restrict__ ptr, const int32_t *__restrict__ idx,
                                 const int32_t *__restrict__ frontier, int64_t fsize,
-                                const int32_t *__restrict__ pos, uint32_t *__restrict__ claim,
-                                int32_t *__restrict__ inq, int32_t *__restrict__ next,
-                                int *__restrict__ next_count) {
+                                const int32_t *__restrict__ pos, uint32_t *__restrict__ claim) {
   GSTRIDE(i, fsize) {
     const int32_t v = frontier[i];
-    const uint32_t pv = static_cast<uint32_t>(pos[v]);
     for (int64_t p = ptr[v]; p < ptr[v + 1]; ++p) {
       const int32_t u = idx[p];
-      if (pos[u] != kNone) continue;
-      atomicMin(&claim[u], pv);
-      if (atomicExch(&inq[u], 1) == 0) next[atomicAdd(next_count, 1)] = u;
+      if (pos[u] == kNone && claim[u] > static_cast<uint32_t>(i))
+        atomicMin(&claim[u], static_cast<uint32_t>(i));
     }
   }
 }
 
-// single-component levels: one 64-bit key (claim << kbits | krank)
-__global__ void cm_key_kernel(const int32_t *__restrict__ next, int64_t k,
-                              const uint32_t *__restrict__ claim,
-                              const uint32_t *__restrict__ krank, int kbits,
-                              uint64_t *__restrict__ keys, uint32_t *__restrict__ vals) {
-  GSTRIDE(i, k) {
-    const int32_t u = next[i];
-    keys[i] = (static_cast<uint64_t>(claim[u]) << kbits) | krank[u];
-    vals[i] = static_cast<uint32_t>(u);
+// children won by each parent; parents of large degree go to the big list
+__global__ void cm_count_kernel(const int64_t *__restrict__ ptr, const int32_t *__restrict__ idx,
+                                const int32_t *__restrict__ frontier, int64_t fsize,
+                                const int32_t *__restrict__ pos,
+                                const uint32_t *__restrict__ claim, int64_t *__restrict__ cnt,
+                                int32_t *__restrict__ big, int *__restrict__ n_big) {
+  GSTRIDE(i, fsize) {
+    const int32_t v = frontier[i];
+    int64_t c = 0;
+    for (int64_t p = ptr[v]; p < ptr[v + 1]; ++p) {
+      const int32_t u = idx[p];
+      c += (pos[u] == kNone && claim[u] == static_cast<uint32_t>(i));
+    }
+    cnt[i] = c;
+    if (ptr[v + 1] - ptr[v] > kBigDegree && c > 0) big[atomicAdd(n_big, 1)] = static_cast<int32_t>(i);
   }
 }
 
-__global__ void comp_key_kernel(const uint32_t *__restrict__ order, int64_t k,
-                                const int32_t *__restrict__ label,
-                                const int32_t *__restrict__ crank,
-                                uint64_t *__restrict__ keys) {
-  GSTRIDE(i, k) { keys[i] = static_cast<uint32_t>(crank[label[order[i]]]); }
+// first slot of every component's run in the next level
+__global__ void cm_runs_kernel(const int32_t *__restrict__ frontier, int64_t fsize,
+                               const int32_t *__restrict__ label,
+                               const int64_t *__restrict__ off, int64_t *__restrict__ lvl_start) {
+  GSTRIDE(i, fsize) {
+    const int32_t c = label[frontier[i]];
+    if (i == 0 || label[frontier[i - 1]] != c) lvl_start[c] = off[i];
+  }
 }
 
-// positions: u at sorted index i of component c gets qlen[c] + (i - first
-// index of c in this level); qlen grows by the level's count of c
-__global__ void cm_place_kernel(const uint32_t *__restrict__ order, int64_t k,
-                                const int32_t *__restrict__ label, int32_t *__restrict__ qlen,
-                                int32_t *__restrict__ pos, uint32_t *__restrict__ claim,
-                                int32_t *__restrict__ inq, int32_t *__restrict__ frontier) {
-  GSTRIDE(i, k) {
-    const int32_t u = static_cast<int32_t>(order[i]);
+// small parents: one thread places all its children in the next level
+// (rank = its children with a smaller key rank); positions are committed by
+// cm_commit_kernel, so `pos == none` still marks this level's children
+__global__ void cm_place_kernel(const int64_t *__restrict__ ptr, const int32_t *__restrict__ idx,
+                                const int32_t *__restrict__ frontier, int64_t fsize,
+                                const uint32_t *__restrict__ claim,
+                                const uint32_t *__restrict__ krank,
+                                const int32_t *__restrict__ pos,
+                                const int64_t *__restrict__ off, int32_t *__restrict__ next) {
+  GSTRIDE(i, fsize) {
+    const int32_t v = frontier[i];
+    const int64_t a = ptr[v], b = ptr[v + 1];
+    if (b - a > kBigDegree || off[i + 1] == off[i]) continue;
+    const uint32_t me = static_cast<uint32_t>(i);
+    for (int64_t p = a; p < b; ++p) {
+      const int32_t u = idx[p];
+      if (claim[u] != me || pos[u] != kNone) continue;
+      const uint32_t ku = krank[u];
+      int64_t r = 0;
+      for (int64_t q = a; q < b; ++q) {
+        const int32_t w = idx[q];
+        r += (claim[w] == me && pos[w] == kNone && krank[w] < ku);
+      }
+      next[off[i] + r] = u;
+    }
+  }
+}
+
+// big parents: one block each, one thread per adjacency entry
+__global__ void cm_place_big_kernel(const int64_t *__restrict__ ptr,
+                                    const int32_t *__restrict__ idx,
+                                    const int32_t *__restrict__ frontier,
+                                    const int32_t *__restrict__ big, const int *__restrict__ n_big,
+                                    const uint32_t *__restrict__ claim,
+                                    const uint32_t *__restrict__ krank,
+                                    const int32_t *__restrict__ pos,
+                                    const int64_t *__restrict__ off, int32_t *__restrict__ next) {
+  for (int bi = blockIdx.x; bi < *n_big; bi += gridDim.x) {
+    const int64_t i = big[bi];
+    const int32_t v = frontier[i];
+    const int64_t a = ptr[v], b = ptr[v + 1];
+    const uint32_t me = static_cast<uint32_t>(i);
+    for (int64_t p = a + threadIdx.x; p < b; p += blockDim.x) {
+      const int32_t u = idx[p];
+      if (claim[u] != me || pos[u] != kNone) continue;
+      const uint32_t ku = krank[u];
+      int64_t r = 0;
+      for (int64_t q = a; q < b; ++q) {
+        const int32_t w = idx[q];
+        r += (claim[w] == me && pos[w] == kNone && krank[w] < ku);
+      }
+      next[off[i] + r] = u;
+    }
+  }
+}
+
+// queue positions of the placed level: component c's run starts at
+// lvl_start[c] and continues its queue at qlen[c]
+__global__ void cm_commit_kernel(const int32_t *__restrict__ next, int64_t total,
+                                 const int32_t *__restrict__ label,
+                                 const int32_t *__restrict__ qlen,
+                                 const int64_t *__restrict__ lvl_start, int32_t *__restrict__ pos) {
+  GSTRIDE(j, total) {
+    const int32_t u = next[j];
     const int32_t c = label[u];
-    // first index of this component's run (components are contiguous runs)
-    int64_t lo = 0, hi = i;
-    while (lo < hi) {
-      const int64_t mid = (lo + hi) / 2;
-      if (label[order[mid]] == c)
-        hi = mid;
-      else
-        lo = mid + 1;
-    }
-    pos[u] = qlen[c] + static_cast<int32_t>(i - lo);
-    claim[u] = kInf;
-    inq[u] = 0;
-    frontier[i] = u;
+    pos[u] = qlen[c] + static_cast<int32_t>(j - lvl_start[c]);
   }
 }
 
-__global__ void cm_count_kernel(const uint32_t *__restrict__ order, int64_t k,
-                                const int32_t *__restrict__ label, int32_t *__restrict__ qlen) {
-  GSTRIDE(i, k) { atomicAdd(&qlen[label[order[i]]], 1); }
+// queue lengths grow by each component's run in the placed level
+__global__ void cm_qlen_kernel(const int32_t *__restrict__ frontier, int64_t fsize,
+                               const int32_t *__restrict__ label,
+                               const int64_t *__restrict__ off,
+                               const int64_t *__restrict__ lvl_start, int32_t *__restrict__ qlen) {
+  GSTRIDE(i, fsize) {
+    const int32_t c = label[frontier[i]];
+    if (i == fsize - 1 || label[frontier[i + 1]] != c)
+      qlen[c] += static_cast<int32_t>(off[i + 1] - lvl_start[c]);
+  }
 }
 
 __global__ void final_fwd_kernel(const int32_t *__restrict__ pos,
@@ -313,11 +386,6 @@ struct DBuf {
   cudaError_t alloc(int64_t n) { return cudaMalloc(&p, (n > 0 ? n : 1) * sizeof(T)); }
 };
 
-int bits_for(int64_t n) {
-  int b = 1;
-  while ((int64_t(1) << b) <= n) ++b;
-  return b;
-}
 
 }  // namespace
 
@@ -326,7 +394,7 @@ int graph_wbo_dev(const csrk_dgraph *g, int64_t *fwd_dev, cudaStream_t s) {
   if (n == 0) return CSRK_OK;
   DBuf<uint64_t> keys, tkeys;
   DBuf<uint32_t> vals, tvals, krank, by_key, claim, lastmin, minrank;
-  DBuf<int32_t> label, size, depth, frontier, next, pos, inq, ecc, crank, qlen;
+  DBuf<int32_t> label, size, depth, frontier, next, pos, ecc, crank, qlen;
   DBuf<int32_t> start, best_node, best_ecc;
   DBuf<int8_t> active;
   DBuf<int> counter;
@@ -346,7 +414,6 @@ int graph_wbo_dev(const csrk_dgraph *g, int64_t *fwd_dev, cudaStream_t s) {
   CSRK_CUDA_TRY(frontier.alloc(n));
   CSRK_CUDA_TRY(next.alloc(n));
   CSRK_CUDA_TRY(pos.alloc(n));
-  CSRK_CUDA_TRY(inq.alloc(n));
   CSRK_CUDA_TRY(ecc.alloc(n));
   CSRK_CUDA_TRY(crank.alloc(n));
   CSRK_CUDA_TRY(qlen.alloc(n));
@@ -398,6 +465,10 @@ int graph_wbo_dev(const csrk_dgraph *g, int64_t *fwd_dev, cudaStream_t s) {
   //    all components' BFS runs together, state stays on the device
   pp_init_kernel<<<nblocks(n_comp), 256, 0, s>>>(roots, n_comp, minrank.p, by_key.p, start.p,
                                                  best_node.p, best_ecc.p, active.p);
+  constexpr int kBfsBatch = 8;  // even: the frontier ends each batch in `frontier`
+  DBuf<int> lsize;
+  CSRK_CUDA_TRY(lsize.alloc(kBfsBatch + 1));
+  const unsigned bfs_grid = nblocks(n) < 148 * 8 ? nblocks(n) : 148 * 8;
   int64_t n_active = n_comp;
   while (n_active > 0) {
     int k = 0;
@@ -408,16 +479,20 @@ int graph_wbo_dev(const csrk_dgraph *g, int64_t *fwd_dev, cudaStream_t s) {
     CSRK_CUDA_TRY(cudaMemsetAsync(depth.p, 0xff, n * sizeof(int32_t), s));
     CSRK_CUDA_TRY(cudaStreamSynchronize(s));
     bfs_seed_kernel<<<nblocks(k), 256, 0, s>>>(next.p, k, depth.p, frontier.p);
-    int64_t fsize = k;
-    for (int32_t level = 0; fsize > 0; ++level) {
-      int cnt = 0;
-      CSRK_CUDA_TRY(cudaMemsetAsync(counter.p, 0, sizeof(int), s));
-      bfs_expand_kernel<<<nblocks(fsize), 256, 0, s>>>(g->ptr, g->idx, frontier.p, fsize, level,
-                                                       depth.p, next.p, counter.p);
-      CSRK_CUDA_TRY(cudaMemcpyAsync(&cnt, counter.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    // levels in batches of kBfsBatch with one host check per batch: the
+    // frontier sizes live in lsize[0..kBfsBatch] on the device
+    int last = k;
+    for (int32_t level = 0; last > 0;) {
+      CSRK_CUDA_TRY(cudaMemsetAsync(lsize.p, 0, (kBfsBatch + 1) * sizeof(int), s));
+      CSRK_CUDA_TRY(cudaMemcpyAsync(lsize.p, &last, sizeof(int), cudaMemcpyHostToDevice, s));
+      for (int j = 0; j < kBfsBatch; ++j, ++level) {
+        bfs_expand_kernel<<<bfs_grid, 256, 0, s>>>(g->ptr, g->idx, frontier.p, lsize.p + j,
+                                                   level, depth.p, next.p, lsize.p + j + 1);
+        std::swap(frontier.p, next.p);
+      }
+      CSRK_CUDA_TRY(cudaMemcpyAsync(&last, lsize.p + kBfsBatch, sizeof(int),
+                                    cudaMemcpyDeviceToHost, s));
       CSRK_CUDA_TRY(cudaStreamSynchronize(s));
-      std::swap(frontier.p, next.p);
-      fsize = cnt;
     }
     CSRK_CUDA_TRY(cudaMemsetAsync(ecc.p, 0xff, n * sizeof(int32_t), s));
     ecc_kernel<<<nblocks(n), 256, 0, s>>>(depth.p, label.p, n, ecc.p);
@@ -434,36 +509,44 @@ int graph_wbo_dev(const csrk_dgraph *g, int64_t *fwd_dev, cudaStream_t s) {
     n_active = still;
   }
 
-  // 4. Cuthill-McKee queues, all components level by level
+  // 4. Cuthill-McKee queues, all components level by level (see the CM
+  //    kernels above): one host round trip per level, for its size
   CSRK_CUDA_TRY(cudaMemsetAsync(claim.p, 0xff, n * sizeof(uint32_t), s));
-  CSRK_CUDA_TRY(cudaMemsetAsync(inq.p, 0, n * sizeof(int32_t), s));
   CSRK_CUDA_TRY(cudaMemsetAsync(pos.p, 0xff, n * sizeof(int32_t), s));
   CSRK_CUDA_TRY(cudaMemsetAsync(qlen.p, 0, n * sizeof(int32_t), s));
   cm_init_kernel<<<nblocks(n_comp), 256, 0, s>>>(roots, n_comp, best_node.p, pos.p, qlen.p,
                                                  frontier.p);
-  // (the level sorts below reuse keys / vals; roots are not needed past here)
-  const int kbits = bits_for(n);
+  DBuf<int64_t> cnt, off, lvl_start;
+  DBuf<int32_t> big;
+  CSRK_CUDA_TRY(cnt.alloc(n));
+  CSRK_CUDA_TRY(off.alloc(n + 1));
+  CSRK_CUDA_TRY(lvl_start.alloc(n));
+  CSRK_CUDA_TRY(big.alloc(n));
   int64_t fsize = n_comp;
-  while (fsize > 0) {
-    int cnt = 0;
-    CSRK_CUDA_TRY(cudaMemsetAsync(counter.p, 0, sizeof(int), s));
+  for (;;) {
     cm_claim_kernel<<<nblocks(fsize), 256, 0, s>>>(g->ptr, g->idx, frontier.p, fsize, pos.p,
-                                                   claim.p, inq.p, next.p, counter.p);
-    CSRK_CUDA_TRY(cudaMemcpyAsync(&cnt, counter.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+                                                   claim.p);
+    CSRK_CUDA_TRY(cudaMemsetAsync(counter.p, 0, sizeof(int), s));
+    cm_count_kernel<<<nblocks(fsize), 256, 0, s>>>(g->ptr, g->idx, frontier.p, fsize, pos.p,
+                                                   claim.p, cnt.p, big.p, counter.p);
+    CSRK_TRY(exclusive_scan_i64(cnt.p, fsize, off.p, s));
+    int64_t total = 0;
+    CSRK_CUDA_TRY(cudaMemcpyAsync(&total, off.p + fsize, sizeof(total), cudaMemcpyDeviceToHost,
+                                  s));
     CSRK_CUDA_TRY(cudaStreamSynchronize(s));
-    if (cnt == 0) break;
-    cm_key_kernel<<<nblocks(cnt), 256, 0, s>>>(next.p, cnt, claim.p, krank.p, kbits, keys.p,
-                                               vals.p);
-    const int key_bits = ((2 * kbits + 7) / 8) * 8;
-    CSRK_TRY(radix_sort_pairs(keys.p, vals.p, tkeys.p, tvals.p, cnt, 0, key_bits, s));
-    if (n_comp > 1) {
-      comp_key_kernel<<<nblocks(cnt), 256, 0, s>>>(vals.p, cnt, label.p, crank.p, keys.p);
-      CSRK_TRY(radix_sort_pairs(keys.p, vals.p, tkeys.p, tvals.p, cnt, 0, 32, s));
-    }
-    cm_place_kernel<<<nblocks(cnt), 256, 0, s>>>(vals.p, cnt, label.p, qlen.p, pos.p, claim.p,
-                                                 inq.p, frontier.p);
-    cm_count_kernel<<<nblocks(cnt), 256, 0, s>>>(vals.p, cnt, label.p, qlen.p);
-    fsize = cnt;
+    if (total == 0) break;
+    cm_runs_kernel<<<nblocks(fsize), 256, 0, s>>>(frontier.p, fsize, label.p, off.p,
+                                                  lvl_start.p);
+    cm_place_kernel<<<nblocks(fsize), 256, 0, s>>>(g->ptr, g->idx, frontier.p, fsize, claim.p,
+                                                   krank.p, pos.p, off.p, next.p);
+    cm_place_big_kernel<<<148, 256, 0, s>>>(g->ptr, g->idx, frontier.p, big.p, counter.p,
+                                            claim.p, krank.p, pos.p, off.p, next.p);
+    cm_commit_kernel<<<nblocks(total), 256, 0, s>>>(next.p, total, label.p, qlen.p,
+                                                    lvl_start.p, pos.p);
+    cm_qlen_kernel<<<nblocks(fsize), 256, 0, s>>>(frontier.p, fsize, label.p, off.p,
+                                                  lvl_start.p, qlen.p);
+    std::swap(frontier.p, next.p);
+    fsize = total;
   }
   if (std::getenv("CSRK_BANDK_PROFILE"))
     std::fprintf(stderr, "[band_k dev]   wbo n=%lld components=%d\n",

@@ -100,6 +100,43 @@ def test_device_graph_build_relabel_contract(golden):
             nat.call("csrk_dgraph_free", dg)
 
 
+def _hub_graphs():
+    """Parents of degree > 128 take the block placement path of the device
+    Cuthill-McKee levels: a star, a random graph with hubs, and several
+    components of stars and paths."""
+    import paper_2203_05096_b200 as ck
+    rng = np.random.default_rng(17)
+    out = []
+    n = 3000  # star: every leaf is a child of the centre
+    rows = np.r_[np.zeros(n - 1, dtype=np.int64), np.arange(1, n)]
+    cols = np.r_[np.arange(1, n), np.zeros(n - 1, dtype=np.int64)]
+    out.append(ck.csr_from_arrays(n, n, rows, cols, np.ones(len(rows))))
+    n = 20000  # sparse random graph plus 8 hubs of degree ~1500
+    r = rng.integers(0, n, 60000)
+    c = rng.integers(0, n, 60000)
+    hubs = rng.choice(n, 8, replace=False)
+    hr = np.repeat(hubs, 1500)
+    hc = rng.integers(0, n, len(hr))
+    rows = np.r_[r, c, hr, hc]
+    cols = np.r_[c, r, hc, hr]
+    out.append(ck.csr_from_arrays(n, n, rows, cols, np.ones(len(rows))))
+    parts, off = [], 0  # components: stars of 200..400 leaves and paths
+    for k in range(6):
+        m = 200 + 40 * k
+        if k % 2 == 0:
+            rr = np.r_[np.full(m, off), off + 1 + np.arange(m)]
+            cc = np.r_[off + 1 + np.arange(m), np.full(m, off)]
+        else:
+            rr = np.r_[off + np.arange(m), off + 1 + np.arange(m)]
+            cc = np.r_[off + 1 + np.arange(m), off + np.arange(m)]
+        parts.append((rr, cc))
+        off += m + 1
+    rows = np.concatenate([p[0] for p in parts])
+    cols = np.concatenate([p[1] for p in parts])
+    out.append(ck.csr_from_arrays(off, off, rows, cols, np.ones(len(rows))))
+    return out
+
+
 def test_device_wbo_matches_native(golden):
     """Level-synchronous device RCM equals the sequential order exactly, on
     the golden graphs (many have several components / isolated nodes), on a
@@ -111,6 +148,7 @@ def test_device_wbo_matches_native(golden):
     mats.append(ck.CsrMatrix(n, n, rp, ci, va))
     n, rp, ci, va = synthetic.stencil_arrays((300, 300), 5)
     mats.append(ck.CsrMatrix(n, n, rp, ci, va))
+    mats.extend(_hub_graphs())
     for a in mats:
         g = ck.build_graph(a)
         dg = C.c_void_p()
