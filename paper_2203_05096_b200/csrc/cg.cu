@@ -202,8 +202,14 @@ int cg_run(const csrk_matrix *m, int value_type, int variant, int nx, const T *b
            T *r, T *p, T *ap, int iters, double *scalars_out, cudaStream_t s) {
   const int64_t n = m->n_rows;
   Scratch w;
+  keep_async_pool();
+
   CSRK_CUDA_TRY(cudaMallocAsync(&w.pap_part, kRedBlocks * sizeof(double), s));
+  keep_async_pool();
+
   CSRK_CUDA_TRY(cudaMallocAsync(&w.rr_part, kRedBlocks * sizeof(double), s));
+  keep_async_pool();
+
   CSRK_CUDA_TRY(cudaMallocAsync(&w.sc, sizeof(CgScalars), s));
   CSRK_CUDA_TRY(cudaMemsetAsync(w.pap_part, 0, kRedBlocks * sizeof(double), s));
   CSRK_CUDA_TRY(cudaMemsetAsync(w.rr_part, 0, kRedBlocks * sizeof(double), s));
@@ -251,6 +257,8 @@ template <typename T>
 int power_run(const csrk_matrix *m, int value_type, int variant, int nx, T *x, T *y,
               int iters, cudaStream_t s) {
   double *part = nullptr;
+  keep_async_pool();
+
   CSRK_CUDA_TRY(cudaMallocAsync(&part, kRedBlocks * sizeof(double), s));
   int rc = CSRK_OK;
   for (int it = 0; it < iters && rc == CSRK_OK; ++it) {

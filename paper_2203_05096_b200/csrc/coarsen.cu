@@ -15,6 +15,7 @@
 // representatives min(v, match[v]) in index order, contract} until the mean
 // coarse weight reaches the target or a round shrinks by less than 5%.
 
+#include <chrono>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -207,6 +208,16 @@ int graph_match_dev(const csrk_dgraph *g, int32_t *match, int *iters, cudaStream
 int graph_coarsen_dev(const csrk_dgraph *g, double target, int32_t *f2c, csrk_dgraph **out,
                       cudaStream_t s) {
   const int64_t total = g->n;
+  const bool prof = std::getenv("CSRK_BANDK_PROFILE") != nullptr;
+  auto t_last = std::chrono::steady_clock::now();
+  auto phase = [&](const char *name, int64_t nn) {
+    if (!prof) return;
+    cudaStreamSynchronize(s);
+    const auto t = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[band_k dev]     coarsen %-9s n=%-9lld %.3f s\n", name,
+                 static_cast<long long>(nn), std::chrono::duration<double>(t - t_last).count());
+    t_last = t;
+  };
   iota32_kernel<<<nb(total), 256, 0, s>>>(f2c, total);
   csrk_dgraph *cur = nullptr;  // owned intermediate (null = g itself)
   auto cur_g = [&]() -> const csrk_dgraph * { return cur ? cur : g; };
@@ -227,6 +238,7 @@ int graph_coarsen_dev(const csrk_dgraph *g, double target, int32_t *f2c, csrk_dg
       if (cur) graph_free_dev(cur);
       cur = rel;
       compose64_kernel<<<nb(total), 256, 0, s>>>(f2c, band.p, total);
+      phase("order", n);
     }
     first = false;
     DB<int32_t> match, new_id;
@@ -236,6 +248,7 @@ int graph_coarsen_dev(const csrk_dgraph *g, double target, int32_t *f2c, csrk_dg
       return CSRK_ENOMEM;
     int sweeps = 0;
     rc = graph_match_dev(cur_g(), match.p, &sweeps, s);
+    phase("matching", n);
     if (std::getenv("CSRK_BANDK_PROFILE"))
       std::fprintf(stderr, "[band_k dev]   matching n=%lld sweeps=%d\n",
                    static_cast<long long>(n), sweeps);
@@ -251,6 +264,7 @@ int graph_coarsen_dev(const csrk_dgraph *g, double target, int32_t *f2c, csrk_dg
     csrk_dgraph *con = nullptr;
     rc = graph_contract_dev(cur_g(), new_id.p, m, s, &con);
     if (rc != CSRK_OK) break;
+    phase("contract", n);
     if (cur) graph_free_dev(cur);
     cur = con;
     if (static_cast<double>(n - m) < 0.05 * static_cast<double>(n)) break;

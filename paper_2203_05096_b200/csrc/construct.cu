@@ -99,7 +99,11 @@ int exclusive_scan(const int64_t *in, int64_t n, int64_t *out, cudaStream_t s) {
   }
   const int64_t blocks = (n + kScanTile - 1) / kScanTile;
   int64_t *sums = nullptr, *offs = nullptr;
+  keep_async_pool();
+
   CSRK_CUDA_TRY(cudaMallocAsync(&sums, (blocks + 1) * sizeof(int64_t), s));
+  keep_async_pool();
+
   CSRK_CUDA_TRY(cudaMallocAsync(&offs, (blocks + 1) * sizeof(int64_t), s));
   scan_reduce_kernel<<<static_cast<unsigned>(blocks), kScanThreads, 0, s>>>(in, n,
                                                                             sums);

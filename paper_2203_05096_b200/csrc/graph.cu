@@ -158,6 +158,7 @@ struct Buf {
     if (p) cudaFreeAsync(p, s);
   }
   cudaError_t alloc(int64_t n) {
+    keep_async_pool();
     return cudaMallocAsync(&p, (n > 0 ? n : 1) * sizeof(T), s);
   }
 };

@@ -20,6 +20,7 @@
 //   pseudo-peripheral starts: repeated multi-source BFS (reorder.py:263-278)
 
 #include <algorithm>
+#include <chrono>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -392,6 +393,17 @@ struct DBuf {
 int graph_wbo_dev(const csrk_dgraph *g, int64_t *fwd_dev, cudaStream_t s) {
   const int64_t n = g->n;
   if (n == 0) return CSRK_OK;
+  // CSRK_BANDK_PROFILE=1: wall time of each phase (synchronising)
+  const bool prof = std::getenv("CSRK_BANDK_PROFILE") != nullptr && n > (1 << 20);
+  auto t_last = std::chrono::steady_clock::now();
+  auto phase = [&](const char *name) {
+    if (!prof) return;
+    cudaStreamSynchronize(s);
+    const auto t = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[band_k dev]     wbo %-10s %.3f s\n", name,
+                 std::chrono::duration<double>(t - t_last).count());
+    t_last = t;
+  };
   DBuf<uint64_t> keys, tkeys;
   DBuf<uint32_t> vals, tvals, krank, by_key, claim, lastmin, minrank;
   DBuf<int32_t> label, size, depth, frontier, next, pos, ecc, crank, qlen;
@@ -419,12 +431,14 @@ int graph_wbo_dev(const csrk_dgraph *g, int64_t *fwd_dev, cudaStream_t s) {
   CSRK_CUDA_TRY(qlen.alloc(n));
   CSRK_CUDA_TRY(counter.alloc(4));
   CSRK_CUDA_TRY(coff.alloc(n + 1));
+  phase("alloc");
 
   // 1. key ranks: stable sort of (degree, weight) keeps index order on ties;
   //    by_key[rank] = node
   key_kernel<<<nblocks(n), 256, 0, s>>>(g->ptr, g->nw, n, keys.p, by_key.p);
   CSRK_TRY(radix_sort_pairs(keys.p, by_key.p, tkeys.p, tvals.p, n, 0, 64, s));
   rank_kernel<<<nblocks(n), 256, 0, s>>>(by_key.p, n, krank.p);
+  phase("keys");
 
   // 2. components (label = minimum index), hook + jump rounds checked every 4
   label_init_kernel<<<nblocks(n), 256, 0, s>>>(label.p, n);
@@ -461,6 +475,7 @@ int graph_wbo_dev(const csrk_dgraph *g, int64_t *fwd_dev, cudaStream_t s) {
   comp_layout_kernel<<<nblocks(n_comp), 256, 0, s>>>(roots, n_comp, size.p, csize_off.p,
                                                      crank.p, coff.p);
 
+  phase("components");
   // 3. pseudo-peripheral start of every component (reorder.py:263-278),
   //    all components' BFS runs together, state stays on the device
   pp_init_kernel<<<nblocks(n_comp), 256, 0, s>>>(roots, n_comp, minrank.p, by_key.p, start.p,
@@ -509,6 +524,7 @@ int graph_wbo_dev(const csrk_dgraph *g, int64_t *fwd_dev, cudaStream_t s) {
     n_active = still;
   }
 
+  phase("pseudo-per");
   // 4. Cuthill-McKee queues, all components level by level (see the CM
   //    kernels above): one host round trip per level, for its size
   CSRK_CUDA_TRY(cudaMemsetAsync(claim.p, 0xff, n * sizeof(uint32_t), s));
@@ -551,6 +567,7 @@ int graph_wbo_dev(const csrk_dgraph *g, int64_t *fwd_dev, cudaStream_t s) {
   if (std::getenv("CSRK_BANDK_PROFILE"))
     std::fprintf(stderr, "[band_k dev]   wbo n=%lld components=%d\n",
                  static_cast<long long>(n), n_comp);
+  phase("cm-levels");
   final_fwd_kernel<<<nblocks(n), 256, 0, s>>>(pos.p, label.p, coff.p, n, fwd_dev);
   CSRK_CUDA_TRY(cudaGetLastError());
   CSRK_CUDA_TRY(cudaStreamSynchronize(s));

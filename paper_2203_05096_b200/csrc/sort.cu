@@ -96,7 +96,11 @@ int radix_sort_pairs(uint64_t *keys, uint32_t *vals, uint64_t *tmp_keys,
   if (n <= 1) return CSRK_OK;
   const int64_t tiles = (n + kSortTile - 1) / kSortTile;
   int64_t *hist = nullptr, *offs = nullptr;
+  keep_async_pool();
+
   CSRK_CUDA_TRY(cudaMallocAsync(&hist, 256 * tiles * sizeof(int64_t), s));
+  keep_async_pool();
+
   CSRK_CUDA_TRY(cudaMallocAsync(&offs, (256 * tiles + 1) * sizeof(int64_t), s));
   uint64_t *kin = keys, *kout = tmp_keys;
   uint32_t *vin = vals, *vout = tmp_vals;
@@ -136,7 +140,11 @@ extern "C" int csrk_sort_pairs(int device, int64_t n, uint64_t *keys, uint32_t *
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   uint64_t *tk = nullptr;
   uint32_t *tv = nullptr;
+  csrk::keep_async_pool();
+
   CSRK_CUDA_TRY(cudaMallocAsync(&tk, (n > 0 ? n : 1) * sizeof(uint64_t), s));
+  csrk::keep_async_pool();
+
   CSRK_CUDA_TRY(cudaMallocAsync(&tv, (n > 0 ? n : 1) * sizeof(uint32_t), s));
   const int rc = csrk::radix_sort_pairs(keys, vals, tk, tv, n, begin_bit, end_bit, s);
   cudaFreeAsync(tk, s);

@@ -682,6 +682,8 @@ int ensure_plan(csrk_matrix *m, int64_t tile_cost, int64_t cap, int64_t stages,
   }
   if (m->n_rows > 0 && !m->plan.row_stats) {
     unsigned long long *d = nullptr, h = 0;
+    keep_async_pool();
+
     CSRK_CUDA_TRY(cudaMallocAsync(&d, sizeof(h), s));
     CSRK_CUDA_TRY(cudaMemsetAsync(d, 0, sizeof(h), s));
     row_sq_kernel<<<148 * 8, 256, 0, s>>>(m->row_ptr, m->n_rows, d);
@@ -701,6 +703,8 @@ int ensure_plan(csrk_matrix *m, int64_t tile_cost, int64_t cap, int64_t stages,
   int64_t max_group = 0;
   if (m->k >= 2 && n_groups > 0) {
     unsigned long long *d = nullptr, h = 0;
+    keep_async_pool();
+
     CSRK_CUDA_TRY(cudaMallocAsync(&d, sizeof(h), s));
     CSRK_CUDA_TRY(cudaMemsetAsync(d, 0, sizeof(h), s));
     int64_t blocks = (n_groups + 255) / 256;
