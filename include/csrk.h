@@ -211,6 +211,17 @@ int csrk_dgraph_coarsen(const csrk_dgraph *g, double target, int64_t *f2c_host,
 int csrk_band_k_device(const csrk_matrix *a, int k, const double *targets,
                        csrk_bandk_result **out);
 
+/* Canonical CSR from coordinate triplets on the device; replaces the body of
+ * csr_from_arrays (format.py:233-284) after its range checks: a stable sort
+ * by (row, col) and duplicates summed in input order exactly as
+ * np.add.reduceat does (first value + numpy's pairwise sum of the rest), so
+ * row_ptr / col_idx / vals are bit-identical.  Indices must already be in
+ * range (the caller validates, with the reference's messages).  k = 1
+ * handle, natural order. */
+int csrk_coo_to_csr(int device, int64_t n_rows, int64_t n_cols, int64_t count,
+                    const int64_t *rows, const int64_t *cols, const double *vals,
+                    csrk_matrix **out);
+
 /* Synthetic stencil generator writing canonical CSR on the device
  * (SURVEY.md §8(d)); shape = {nz, ny, nx} (nz = 1 for 2D), points = 5, 7, 27.
  * Produces a k = 1 handle (natural order). */

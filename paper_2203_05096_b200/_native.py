@@ -75,6 +75,7 @@ _SIGNATURES = {
     "csrk_band_k_device": ([P, C.c_int, F64P, C.POINTER(P)], C.c_int),
     "csrk_sort_pairs": ([C.c_int, I64, P, P, C.c_int, C.c_int, P], C.c_int),
     "csrk_stencil": ([C.c_int, I64, I64, I64, C.c_int, C.POINTER(P)], C.c_int),
+    "csrk_coo_to_csr": ([C.c_int, I64, I64, I64, I64P, I64P, F64P, C.POINTER(P)], C.c_int),
     "csrk_stencil_slab": ([C.c_int, I64, I64, I64, C.c_int, I64, I64, C.POINTER(P)],
                           C.c_int),
     "csrk_band_k": ([I64, U32P, U32P, C.c_int, F64P, C.POINTER(P)], C.c_int),

@@ -719,6 +719,160 @@ int row_variance(const csrk_matrix *m, double mean, double *out) {
   return CSRK_OK;
 }
 
+// ---- coordinate triplets -> canonical CSR (reference format.py:233-284) ---
+//
+// csr_from_arrays sorts the triplets stably by (row, col) (np.lexsort) and
+// sums duplicate coordinates with np.add.reduceat, whose float64 reduction
+// is v0 + pairwise_sum(v1 .. v_{L-1}) with numpy's pairwise_sum (blocks of
+// 8 accumulators up to 128 elements, halves above; sequential from -0.0
+// below 8).  Here: a stable LSD radix sort of (row << cb | col, input index)
+// pairs, run heads, and one thread per run summing in exactly that order.
+
+__global__ void coo_key_kernel(const int64_t *__restrict__ rows, const int64_t *__restrict__ cols,
+                               int64_t count, int cb, uint64_t *__restrict__ keys,
+                               uint32_t *__restrict__ idx) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < count;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    keys[i] = (static_cast<uint64_t>(rows[i]) << cb) | static_cast<uint64_t>(cols[i]);
+    idx[i] = static_cast<uint32_t>(i);
+  }
+}
+
+__global__ void coo_head_kernel(const uint64_t *__restrict__ keys, int64_t count,
+                                int64_t *__restrict__ head) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < count;
+       i += int64_t(gridDim.x) * blockDim.x)
+    head[i] = (i == 0 || keys[i] != keys[i - 1]) ? 1 : 0;
+}
+
+// numpy's pairwise_sum over v[idx[a .. a+n)] (loops_utils.h.src)
+__device__ double np_pairwise(const double *__restrict__ v, const uint32_t *__restrict__ idx,
+                              int64_t a, int64_t n) {
+  if (n < 8) {
+    double res = -0.0;
+    for (int64_t i = 0; i < n; ++i) res += v[idx[a + i]];
+    return res;
+  }
+  if (n <= 128) {
+    double r[8];
+    for (int j = 0; j < 8; ++j) r[j] = v[idx[a + j]];
+    int64_t i = 8;
+    for (; i < n - (n % 8); i += 8)
+      for (int j = 0; j < 8; ++j) r[j] += v[idx[a + i + j]];
+    double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+    for (; i < n; ++i) res += v[idx[a + i]];
+    return res;
+  }
+  int64_t n2 = n / 2;
+  n2 -= n2 % 8;
+  return np_pairwise(v, idx, a, n2) + np_pairwise(v, idx, a + n2, n - n2);
+}
+
+__global__ void coo_runs_kernel(const uint64_t *__restrict__ keys,
+                                const uint32_t *__restrict__ idx, const double *__restrict__ v,
+                                const int64_t *__restrict__ head, const int64_t *__restrict__ pos,
+                                int64_t count, int cb, uint32_t *__restrict__ col_idx,
+                                double *__restrict__ vals, int64_t *__restrict__ row_count) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < count;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    if (!head[i]) continue;
+    int64_t e = i + 1;
+    while (e < count && !head[e]) ++e;
+    const int64_t u = pos[i];
+    const uint64_t k = keys[i];
+    col_idx[u] = static_cast<uint32_t>(k & ((uint64_t(1) << cb) - 1));
+    double s = v[idx[i]];
+    if (e - i > 1) s += np_pairwise(v, idx, i + 1, e - i - 1);
+    vals[u] = s;
+    atomicAdd(reinterpret_cast<unsigned long long *>(&row_count[k >> cb]), 1ull);
+  }
+}
+
+int coo_to_csr_device(int device, int64_t n_rows, int64_t n_cols, int64_t count,
+                      const int64_t *rows_h, const int64_t *cols_h, const double *vals_h,
+                      csrk_matrix **out) {
+  *out = nullptr;
+  if (n_rows < 0 || n_cols < 0 || count < 0 || n_rows > 4294967295LL ||
+      n_cols > 4294967295LL) {
+    set_error("invalid shape %lld x %lld", static_cast<long long>(n_rows),
+              static_cast<long long>(n_cols));
+    return CSRK_EINVAL;
+  }
+  if (count > 2147483647LL) {
+    set_error("entry count %lld exceeds the 32-bit index limit",
+              static_cast<long long>(count));
+    return CSRK_EINVAL;
+  }
+  CSRK_CUDA_TRY(cudaSetDevice(device));
+  csrk_matrix *m = new csrk_matrix();
+  m->device = device;
+  m->n_rows = n_rows;
+  m->n_cols = n_cols;
+  m->k = 1;
+  cudaStream_t s = nullptr;
+  int rc = CSRK_OK;
+  auto fail = [&](int code, const char *what) {
+    if (code == CSRK_ECUDA || code == CSRK_ENOMEM) set_error("%s failed", what);
+    csrk_matrix_free(m);
+    return code;
+  };
+  int cb = 1;
+  while ((int64_t(1) << cb) < n_cols) ++cb;
+  int rb = 1;
+  while ((int64_t(1) << rb) < n_rows) ++rb;
+  const int key_bits = ((cb + rb + 7) / 8) * 8;
+  DevBuf<int64_t> r, c, head, pos, rcount, rptr;
+  DevBuf<double> v;
+  DevBuf<uint64_t> keys, tkeys;
+  DevBuf<uint32_t> idx, tidx;
+  if (r.alloc(count) || c.alloc(count) || v.alloc(count) || keys.alloc(count) ||
+      tkeys.alloc(count) || idx.alloc(count) || tidx.alloc(count) || head.alloc(count) ||
+      pos.alloc(count + 1) || rcount.alloc(n_rows) || rptr.alloc(n_rows + 1))
+    return fail(CSRK_ENOMEM, "device memory for the triplets");
+  if (count) {
+    if (cudaMemcpy(r.p, rows_h, count * 8, cudaMemcpyHostToDevice) ||
+        cudaMemcpy(c.p, cols_h, count * 8, cudaMemcpyHostToDevice) ||
+        cudaMemcpy(v.p, vals_h, count * 8, cudaMemcpyHostToDevice))
+      return fail(CSRK_ECUDA, "triplet upload");
+    coo_key_kernel<<<grid_for(count, 256), 256, 0, s>>>(r.p, c.p, count, cb, keys.p, idx.p);
+    rc = radix_sort_pairs(keys.p, idx.p, tkeys.p, tidx.p, count, 0, key_bits, s);
+    if (rc != CSRK_OK) return fail(rc, "triplet sort");
+    coo_head_kernel<<<grid_for(count, 256), 256, 0, s>>>(keys.p, count, head.p);
+    rc = exclusive_scan(head.p, count, pos.p, s);
+    if (rc != CSRK_OK) return fail(rc, "run scan");
+  } else if (cudaMemset(pos.p, 0, sizeof(int64_t))) {
+    return fail(CSRK_ECUDA, "run scan");
+  }
+  int64_t nnz = 0;
+  if (cudaMemcpy(&nnz, pos.p + count, sizeof(nnz), cudaMemcpyDeviceToHost))
+    return fail(CSRK_ECUDA, "run count");
+  m->nnz = nnz;
+  rc = alloc_matrix_arrays(m, true, false);
+  if (rc != CSRK_OK) {
+    csrk_matrix_free(m);
+    return rc;
+  }
+  if (cudaMemset(rcount.p, 0, (n_rows > 0 ? n_rows : 1) * sizeof(int64_t)))
+    return fail(CSRK_ECUDA, "row counts");
+  if (count)
+    coo_runs_kernel<<<grid_for(count, 256), 256, 0, s>>>(keys.p, idx.p, v.p, head.p, pos.p,
+                                                         count, cb, m->col_idx, m->vals64,
+                                                         rcount.p);
+  rc = exclusive_scan(rcount.p, n_rows, rptr.p, s);
+  if (rc != CSRK_OK) return fail(rc, "row pointer scan");
+  i64_to_u32_kernel<<<grid_for(n_rows + 1, 256), 256, 0, s>>>(rptr.p, m->row_ptr, n_rows + 1);
+  if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(s) != cudaSuccess)
+    return fail(CSRK_ECUDA, "triplet assembly");
+  rc = ensure_plan(m, 0, 0, 0, m->stream);
+  if (rc == CSRK_OK && cudaStreamSynchronize(m->stream) != cudaSuccess) rc = CSRK_ECUDA;
+  if (rc != CSRK_OK) {
+    csrk_matrix_free(m);
+    return rc;
+  }
+  *out = m;
+  return CSRK_OK;
+}
+
 int stencil_device(int device, int64_t nz, int64_t ny, int64_t nx, int points,
                    int64_t z0, int64_t z1, csrk_matrix **out) {
   *out = nullptr;
@@ -850,6 +1004,16 @@ int csrk_stencil(int device, int64_t nz, int64_t ny, int64_t nx, int points,
     return CSRK_EINVAL;
   }
   return csrk::stencil_device(device, nz, ny, nx, points, 0, nz, out);
+}
+
+int csrk_coo_to_csr(int device, int64_t n_rows, int64_t n_cols, int64_t count,
+                    const int64_t *rows, const int64_t *cols, const double *vals,
+                    csrk_matrix **out) {
+  if (!out || (count > 0 && (!rows || !cols || !vals))) {
+    csrk::set_error("null argument");
+    return CSRK_EINVAL;
+  }
+  return csrk::coo_to_csr_device(device, n_rows, n_cols, count, rows, cols, vals, out);
 }
 
 int csrk_stencil_slab(int device, int64_t nz, int64_t ny, int64_t nx, int points,

@@ -18,6 +18,7 @@ What runs where:
 
 from __future__ import annotations
 
+import ctypes
 from typing import Iterable, Sequence
 
 import numpy as np
@@ -259,10 +260,14 @@ class CsrKMatrix(_Frozen):
                 f"nnz={self.base.nnz}, num_super_rows={self.num_super_rows})")
 
 
+DEVICE_COO_MIN = 1 << 16  # triplet count from which csr_from_arrays runs on the GPU
+
+
 def csr_from_arrays(n_rows: int, n_cols: int, rows, cols, vals) -> CsrMatrix:
     """Canonical CSR from coordinate triplets in any order; duplicate
     coordinates are summed in their input order (reference
-    format.py:233-284).  Host-side input staging."""
+    format.py:233-284).  Large inputs are assembled on the GPU
+    (csrk_coo_to_csr), bit-identical to the host restatement below."""
     r = np.asarray(rows, dtype=np.int64)
     c = np.asarray(cols, dtype=np.int64)
     v = np.asarray(vals, dtype=VALUE_DTYPE)
@@ -280,6 +285,18 @@ def csr_from_arrays(n_rows: int, n_cols: int, rows, cols, vals) -> CsrMatrix:
     if count == 0:
         return CsrMatrix(n_rows, n_cols, np.zeros(n_rows + 1, dtype=np.int64),
                          np.empty(0, dtype=np.int64), np.empty(0), _trusted=True)
+    if count >= DEVICE_COO_MIN and nat.device_count() > 0:
+        # on the GPU: stable radix sort + duplicate runs summed in numpy's
+        # reduceat order (csrk_coo_to_csr); the result keeps its device copy
+        out = ctypes.c_void_p()
+        r, c, v = (np.ascontiguousarray(t) for t in (r, c, v))
+        nat.call("csrk_coo_to_csr", nat.current_device(), n_rows, n_cols, count,
+                 nat.i64p(r), nat.i64p(c), nat.f64p(v), ctypes.byref(out))
+        dev = nat.DeviceMatrix(out)
+        rp, ci, va, _, _ = dev.download()
+        m = CsrMatrix(n_rows, n_cols, rp, ci, va, _trusted=True)
+        m._set("_dev", dev)
+        return m
     # stable order by (row, col); equal coordinates keep their input order
     order = np.lexsort((c, r))
     r, c, v = r[order], c[order], v[order]

@@ -257,3 +257,48 @@ def test_device_band_k_digests(name, configs_golden):
         assert digest(fwd, "<i8") == run["fwd"]
         assert digest(s1, "<i8") == run["sizes0"]
         assert digest(s2, "<i8") == run["sizes1"]
+
+
+@pytest.mark.parametrize("case", ["dups", "long_runs", "zeros", "wide"])
+def test_device_coo_to_csr_bitwise(monkeypatch, case):
+    """csrk_coo_to_csr equals the host restatement of csr_from_arrays
+    (reference format.py:233-284) bit for bit: stable (row, col) order and
+    duplicates summed as np.add.reduceat does (runs of 1..500)."""
+    import paper_2203_05096_b200 as ck
+    from paper_2203_05096_b200 import format as F
+    rng = np.random.default_rng(len(case))
+    if case == "dups":
+        n_rows, n_cols, count = 70001, 3001, 400000
+        r = rng.integers(0, n_rows, count)
+        c = rng.integers(0, n_cols, count)
+        v = rng.standard_normal(count) * 10.0 ** rng.uniform(-8, 8, count)
+    elif case == "long_runs":  # the same coordinate 1..500 times
+        n_rows, n_cols = 1000, 1000
+        lens = rng.integers(1, 500, 600)
+        r = np.repeat(rng.integers(0, n_rows, 600), lens)
+        c = np.repeat(rng.integers(0, n_cols, 600), lens)
+        v = rng.standard_normal(len(r)) * 10.0 ** rng.uniform(-12, 12, len(r))
+        perm = rng.permutation(len(r))
+        r, c, v = r[perm], c[perm], v[perm]
+    elif case == "zeros":  # signed zeros and cancellation
+        n_rows, n_cols, count = 50000, 50000, 200000
+        r = rng.integers(0, 300, count)
+        c = rng.integers(0, 300, count)
+        v = rng.choice(np.array([0.0, -0.0, 1.0, -1.0, 1e-300, -3.0]), count)
+    else:  # wide: 32-bit columns, most rows empty
+        n_rows, n_cols, count = 3_000_000, 4_000_000_000, 300000
+        r = rng.integers(0, n_rows, count)
+        c = rng.integers(0, n_cols, count)
+        v = rng.uniform(-1, 1, count)
+    monkeypatch.setattr(F, "DEVICE_COO_MIN", 1 << 62)
+    want = ck.csr_from_arrays(n_rows, n_cols, r, c, v)
+    monkeypatch.setattr(F, "DEVICE_COO_MIN", 1)
+    got = ck.csr_from_arrays(n_rows, n_cols, r, c, v)
+    assert got._dev is not None
+    np.testing.assert_array_equal(got.row_ptr, want.row_ptr)
+    np.testing.assert_array_equal(got.col_idx, want.col_idx)
+    assert np.array_equal(got.vals.view(np.uint64), want.vals.view(np.uint64))
+    # the attached device copy is the same matrix
+    rp, ci, va, _, _ = got.device().download()
+    np.testing.assert_array_equal(rp, want.row_ptr)
+    np.testing.assert_array_equal(va, want.vals)
