@@ -195,7 +195,7 @@ def spmv_device(m, x, y=None, *, dims: BlockDims | None = None, variant: str = "
                 stream=None):
     """Device-resident SpMV on torch CUDA tensors (float64 or float32).
 
-    ``m`` is a CsrMatrix or CsrKMatrix; ``x`` / ``y`` are contiguous CUDA
+    ``m`` is a CsrMatrix, CsrKMatrix or DeviceMatrix; ``x`` / ``y`` are contiguous CUDA
     tensors in the permuted index space.  ``variant`` "serial" gives the
     reference's row order, "strided" the GPUSpMV-3.5 order with
     ``dims.x`` lanes.  Launches asynchronously on ``stream`` (default: the
@@ -204,7 +204,7 @@ def spmv_device(m, x, y=None, *, dims: BlockDims | None = None, variant: str = "
     import torch
 
     base = m.base if isinstance(m, CsrKMatrix) else m
-    dev = m.device()
+    dev = m if isinstance(m, nat.DeviceMatrix) else m.device()
     f32 = x.dtype == torch.float32
     if x.dtype not in (torch.float32, torch.float64):
         raise ValueError("x must be float32 or float64")

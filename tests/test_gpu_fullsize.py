@@ -61,3 +61,59 @@ def test_full_size_pipeline_matches_reference(name, configs_golden, capsys):
         assert digest(res.perm.fwd, "<i8") == rec["runs"][0]["fwd"]
         with capsys.disabled():
             print(f"[{name}] host band_k {t_host:.2f}s")
+
+
+_OFFS7 = ((-1, 0, 0), (0, -1, 0), (0, 0, -1), (0, 0, 0), (0, 0, 1), (0, 1, 0), (1, 0, 0))
+
+
+def _stencil7_cols(i, n):
+    """Columns of row i of the n^3 7-point Laplacian, ascending."""
+    z, y, x = i // (n * n), (i // n) % n, i % n
+    out = []
+    for dz, dy, dx in _OFFS7:
+        zz, yy, xx = z + dz, y + dy, x + dx
+        if 0 <= zz < n and 0 <= yy < n and 0 <= xx < n:
+            out.append((zz * n + yy) * n + xx)
+    return out
+
+
+@pytest.mark.parametrize("variant", ["serial", "strided"])
+def test_c4_full_size_properties(variant):
+    """C4 (512^3, 938 M nonzeros) where no CPU oracle fits:
+    x = 1 gives y_i = 6 - (in-grid neighbours of i) exactly, and 20,000
+    sampled rows of a random x equal the reference's row order bit for bit
+    (serial order; the strided order is checked on the x = 1 property)."""
+    torch = pytest.importorskip("torch")
+    n = 512
+    dev = synthetic.device_stencil((n, n, n), 7).group_uniform(8, 8)
+    assert dev.nnz == 7 * n ** 3 - 6 * n ** 2
+    rows = n ** 3
+    dims = ck.BlockDims(4, 8, 8)
+    ones = torch.ones(rows, dtype=torch.float64, device="cuda")
+    y = torch.empty_like(ones)
+    ck.spmv_device(dev, ones, y, dims=dims, variant=variant)
+    idx = torch.arange(rows, device="cuda", dtype=torch.int64)
+    xi, yi, zi = idx % n, (idx // n) % n, idx // (n * n)
+    deg = torch.zeros_like(idx)
+    for c in (xi, yi, zi):
+        deg += (c > 0).long() + (c < n - 1).long()
+    assert torch.equal(y, (6 - deg).double())
+    del idx, xi, yi, zi, deg
+    if variant != "serial":
+        return
+    g = torch.Generator(device="cuda").manual_seed(3)
+    xr = torch.rand(rows, generator=g, device="cuda", dtype=torch.float64) * 2 - 1
+    ck.spmv_device(dev, xr, y, variant="serial")
+    rng = np.random.default_rng(4)
+    sample = np.concatenate([rng.integers(0, rows, 20000), [0, rows - 1, n * n - 1, n - 1]])
+    ys = y[torch.from_numpy(sample).cuda()].cpu().numpy()
+    cols = [_stencil7_cols(int(i), n) for i in sample]
+    flat = np.array([c for cs in cols for c in cs], dtype=np.int64)
+    xv = xr[torch.from_numpy(flat).cuda()].cpu().numpy()
+    pos = 0
+    for k, i in enumerate(sample.tolist()):
+        acc = 0.0  # the reference's left-to-right row sum (kernels.py:117-147)
+        for j in cols[k]:
+            acc += (6.0 if j == i else -1.0) * float(xv[pos])
+            pos += 1
+        assert ys[k] == acc, i
