@@ -94,8 +94,8 @@ int csrk_matrix_add_f32(csrk_matrix *m);
 int csrk_matrix_set_plan(csrk_matrix *m, int64_t tile_cost, int64_t cap,
                          int64_t stages);
 /* out = tile_cost, cap, rcap, stages, n_tiles, group_aligned, gather mode,
- *       ctas_per_sm (the f64 value when auto) */
-int csrk_matrix_plan(const csrk_matrix *m, int64_t out[8]);
+ *       ctas_per_sm (the f64 value when auto), layout, sliced copy built */
+int csrk_matrix_plan(const csrk_matrix *m, int64_t out[10]);
 /* Schedule of the streaming kernel (B200 tuning knobs with no reference
  * counterpart; results are bitwise identical under every setting).
  * gather: 0 = inline (each row gathers its x while summing), 1 = gather-first
@@ -107,6 +107,14 @@ int csrk_matrix_plan(const csrk_matrix *m, int64_t out[8]);
  * carveout is set to exactly what they need, and the rest of the 256 KB
  * stays L1 for the x gathers. */
 int csrk_matrix_set_schedule(csrk_matrix *m, int gather, int ctas_per_sm);
+/* Layout of serial-order f64 launches: 0 = the CSR arrays (default), 1 =
+ * sliced tiles.  A sliced tile keeps the tile's rows sorted by length in
+ * slices of 32 rows with element j of a slice contiguous (SELL-32 per tile),
+ * built once per plan on the device (an extra copy of the values and
+ * columns); each row is still summed left to right by one thread, so y is
+ * bitwise the same.  Opt-in: it removes the shared-memory bank conflicts of
+ * the CSR stage but measured no faster on B200. */
+int csrk_matrix_set_layout(csrk_matrix *m, int layout);
 
 /* ---- SpMV ------------------------------------------------------------------
  * y = A x on device-resident x / y (already in the permuted index space, as

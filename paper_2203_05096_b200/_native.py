@@ -48,6 +48,7 @@ _SIGNATURES = {
     "csrk_matrix_set_plan": ([P, I64, I64, I64], C.c_int),
     "csrk_matrix_plan": ([P, I64P], C.c_int),
     "csrk_matrix_set_schedule": ([P, C.c_int, C.c_int], C.c_int),
+    "csrk_matrix_set_layout": ([P, C.c_int], C.c_int),
     "csrk_spmv": ([P, C.c_int, C.c_int, C.c_int, P, P, P], C.c_int),
     "csrk_spmv_tiles": ([P, C.c_int, C.c_int, C.c_int, P, P, I64, I64, P], C.c_int),
     "csrk_matrix_tile_rows": ([P, U32P], C.c_int),
@@ -274,11 +275,15 @@ class DeviceMatrix:
         (0 inline, 1 gather-first) and resident CTAs per SM (0 = default)."""
         call("csrk_matrix_set_schedule", self.ptr, int(gather), int(ctas_per_sm))
 
+    def set_layout(self, layout: int):
+        """Serial f64 layout: 0 CSR (default), 1 sliced tiles (include/csrk.h)."""
+        call("csrk_matrix_set_layout", self.ptr, int(layout))
+
     def plan(self) -> dict:
-        out = np.zeros(8, dtype=np.int64)
+        out = np.zeros(10, dtype=np.int64)
         call("csrk_matrix_plan", self.ptr, i64p(out))
         keys = ("tile_cost", "cap", "rcap", "stages", "n_tiles", "group_aligned",
-                "gather_first", "ctas_per_sm")
+                "gather_first", "ctas_per_sm", "layout", "sliced")
         return {k: int(v) for k, v in zip(keys, out)}
 
     def stats(self):

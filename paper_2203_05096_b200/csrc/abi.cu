@@ -57,6 +57,7 @@ static void release(csrk_matrix *m) {
   cudaFree(m->sr_ptr);
   cudaFree(m->ssr_ptr);
   cudaFree(m->plan.tile_row);
+  csrk::free_sliced(m);
   cudaFree(m->x_stage);
   cudaFree(m->y_stage);
   for (auto e : m->pipe.ev_x) cudaEventDestroy(e);
@@ -350,7 +351,7 @@ int csrk_spmv(const csrk_matrix *m, int value_type, int variant, int nx,
     return CSRK_EINVAL;
   }
   CSRK_CUDA_TRY(cudaSetDevice(m->device));
-  CSRK_TRY(prepare_plan(m, variant, nx));
+  CSRK_TRY(prepare_plan(m, value_type, variant, nx));
   return launch_spmv(m, value_type, variant, nx, x, y,
                      static_cast<cudaStream_t>(stream));
 }
@@ -368,6 +369,8 @@ int csrk_spmv_tiles(const csrk_matrix *m, int value_type, int variant, int nx,
   }
   if (t1 == t0) return CSRK_OK;
   CSRK_CUDA_TRY(cudaSetDevice(m->device));
+  if (sliced_wanted(m, value_type, variant))  // tile ranges index the current plan
+    CSRK_TRY(ensure_sliced(const_cast<csrk_matrix *>(m), m->stream));
   return launch_spmv(m, value_type, variant, nx, x, y, static_cast<cudaStream_t>(stream),
                      t0, t1);
 }
@@ -508,7 +511,7 @@ int csrk_spmv_host(csrk_matrix *m, int value_type, int variant, int nx,
   }
   const size_t es = value_type == CSRK_F32 ? sizeof(float) : sizeof(double);
   CSRK_CUDA_TRY(cudaSetDevice(m->device));
-  CSRK_TRY(prepare_plan(m, variant, nx));
+  CSRK_TRY(prepare_plan(m, value_type, variant, nx));
   const size_t xb = static_cast<size_t>(m->n_cols) * es + 16;
   const size_t yb = static_cast<size_t>(m->n_rows) * es + 16;
   if (m->x_stage_bytes < xb) {
@@ -637,7 +640,7 @@ int csrk_spmv_host(csrk_matrix *m, int value_type, int variant, int nx,
   return CSRK_OK;
 }
 
-int csrk_matrix_plan(const csrk_matrix *m, int64_t out[8]) {
+int csrk_matrix_plan(const csrk_matrix *m, int64_t out[10]) {
   if (!m || !out) {
     set_error("null argument");
     return CSRK_EINVAL;
@@ -650,6 +653,26 @@ int csrk_matrix_plan(const csrk_matrix *m, int64_t out[8]) {
   out[5] = m->plan.group_aligned ? 1 : 0;
   out[6] = m->plan.gather_first;
   out[7] = m->plan.ctas_per_sm ? m->plan.ctas_per_sm : auto_ctas(m->plan.row_var, 8);
+  out[8] = m->plan.layout;
+  out[9] = (m->sliced.col && m->sliced.gen == m->plan.gen) ? 1 : 0;
+  return CSRK_OK;
+}
+
+int csrk_matrix_set_layout(csrk_matrix *m, int layout) {
+  if (!m) {
+    set_error("null argument");
+    return CSRK_EINVAL;
+  }
+  if (layout < 0 || layout > 1) {
+    set_error("layout must be 0 (CSR) or 1 (sliced tiles), got %d", layout);
+    return CSRK_EINVAL;
+  }
+  m->plan.layout = layout;
+  if (layout == 0) {
+    CSRK_CUDA_TRY(cudaSetDevice(m->device));
+    CSRK_CUDA_TRY(cudaStreamSynchronize(m->stream));
+    free_sliced(m);
+  }
   return CSRK_OK;
 }
 

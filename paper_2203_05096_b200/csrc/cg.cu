@@ -291,7 +291,7 @@ int csrk_cg(const csrk_matrix *m, int value_type, int variant, int nx, const voi
     return CSRK_EINVAL;
   }
   CSRK_CUDA_TRY(cudaSetDevice(m->device));
-  CSRK_TRY(prepare_plan(m, variant, nx));
+  CSRK_TRY(prepare_plan(m, value_type, variant, nx));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (value_type == CSRK_F32)
     return cg_run<float>(m, value_type, variant, nx, static_cast<const float *>(b),
@@ -311,7 +311,7 @@ int csrk_power(const csrk_matrix *m, int value_type, int variant, int nx, void *
     return CSRK_EINVAL;
   }
   CSRK_CUDA_TRY(cudaSetDevice(m->device));
-  CSRK_TRY(prepare_plan(m, variant, nx));
+  CSRK_TRY(prepare_plan(m, value_type, variant, nx));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (value_type == CSRK_F32)
     return power_run<float>(m, value_type, variant, nx, static_cast<float *>(x),

@@ -78,10 +78,22 @@ struct TilePlan {
   double mean_row = 0.0, row_var = 0.0;
   bool row_stats = false;
   bool auto_tile = true;  // tile cost follows the launch's order (auto_tile_cost)
+  int layout = 0;         // serial f64 layout: 0 CSR, 1 sliced tiles
+  uint64_t gen = 0;       // bumped whenever tile_row is rebuilt
   uint32_t *tile_row = nullptr;  // device, n_tiles + 1
 };
 
 }  // namespace csrk
+
+// Sliced-tile copy of the matrix for the serial f64 kernel (SELL-32 inside
+// every tile of the plan it was built for; csrc/spmv.cu).
+struct csrk_sliced {
+  uint64_t gen = ~0ull;  // plan generation it belongs to
+  int64_t n_slices = 0, entries = 0;
+  uint32_t *col = nullptr, *meta = nullptr, *info = nullptr, *base = nullptr;
+  double *val = nullptr;
+  unsigned long long *te = nullptr;
+};
 
 struct csrk_matrix {
   int device = 0;
@@ -95,6 +107,7 @@ struct csrk_matrix {
   uint32_t *sr_ptr = nullptr;   // n_sr + 1 (k >= 2)
   uint32_t *ssr_ptr = nullptr;  // n_ssr + 1 (k == 3)
   csrk::TilePlan plan;          // current streaming plan
+  csrk_sliced sliced;           // optional sliced copy (serial f64 launches)
   int sm_count = 0;
   // host-API staging and the overlapped host pipeline (csrk_spmv_host)
   struct Pipe {
@@ -153,7 +166,12 @@ int ensure_plan(csrk_matrix *m, int64_t tile_cost, int64_t cap, int64_t stages,
                 cudaStream_t s);
 // before a whole-matrix launch: re-plan for the launch's order when the plan
 // is automatic (cached; rebuilds only when the tile cost changes)
-int prepare_plan(const csrk_matrix *m, int variant, int nx);
+int prepare_plan(const csrk_matrix *m, int value_type, int variant, int nx);
+// the sliced copy for the current plan (built when a serial f64 launch
+// uses it: layout 1)
+bool sliced_wanted(const csrk_matrix *m, int value_type, int variant);
+int ensure_sliced(csrk_matrix *m, cudaStream_t s);
+void free_sliced(csrk_matrix *m);
 int launch_spmv(const csrk_matrix *m, int value_type, int variant, int nx,
                 const void *x, void *y, cudaStream_t stream, int64_t t0 = 0,
                 int64_t t1 = -1);

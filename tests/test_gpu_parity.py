@@ -407,3 +407,50 @@ def test_auto_plan_follows_the_order():
     dev.set_plan(1000, 0, 2)  # explicit plans stay put
     ck.spmv_gpu35(m, x, ck.BlockDims(4, 1, 1))
     assert dev.plan()["tile_cost"] == 1000
+
+
+@pytest.mark.parametrize("layout", [0, 1])
+@pytest.mark.parametrize("kind", ["mixed", "stencil", "irregular", "empty_rows"])
+def test_sliced_layout_bitwise(layout, kind):
+    """Serial f64 launches through the sliced tiles (SELL-32 per tile, rows
+    sorted by length) equal the reference's row order bit for bit, under
+    several plans (staged and direct tiles), for whole launches, tile ranges
+    and the pinned host pipeline."""
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(len(kind) + layout)
+    if kind == "mixed":
+        a = _mixed_rows_matrix(rng, 20000)
+    elif kind == "stencil":
+        n, rp, ci, va = synthetic.stencil_arrays((30, 31, 32), 7, values="uniform")
+        a = ck.CsrMatrix(n, n, rp, ci, va)
+    elif kind == "irregular":
+        r, c, v = synthetic.irregular_triplets(60000, seed=3)
+        a = ck.csr_from_arrays(60000, 60000, r, c, v)
+    else:  # every third row empty, others 1..40 nonzeros
+        n = 30000
+        lens = rng.integers(1, 41, n)
+        lens[::3] = 0
+        rows = np.repeat(np.arange(n), lens)
+        a = ck.csr_from_arrays(n, n, rows, rng.integers(0, n, len(rows)),
+                               rng.uniform(-1, 1, len(rows)))
+    res = ck.band_k(a, 3, [4, 8])
+    m = ck.pack_csrk(a, res.perm, res.level_group_sizes)
+    b = m.base
+    x = rng.uniform(-1.0, 1.0, b.n_rows)
+    want = O.spmv_serial(b.row_ptr, b.col_idx, b.vals, x)
+    dev = m.device()
+    dev.set_layout(layout)
+    xd = torch.from_numpy(x).cuda()
+    for tile_cost, stages in ((0, 0), (256, 3), (4096, 2), (48, 1)):
+        dev.set_plan(tile_cost, 0, stages)
+        np.testing.assert_array_equal(ck.spmv_csr3(m, x), want)
+        plan = dev.plan()
+        assert plan["sliced"] == int(layout == 1)
+        yd = torch.full_like(xd, float("nan"))
+        nt = plan["n_tiles"]
+        cut = nt // 3
+        for t0, t1 in ((0, cut), (cut, nt)):
+            dev.spmv_tiles_ptr(xd.data_ptr(), yd.data_ptr(), t0, t1,
+                               torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(yd.cpu().numpy(), want)

@@ -26,6 +26,7 @@ GATHER = tuple(int(t) for t in os.environ.get('SWEEP_GATHER', '0,1').split(','))
 DTYPES = tuple(getattr(torch, d) for d in os.environ.get('SWEEP_DTYPES', 'float64,float32').split(','))
 VARIANTS = os.environ.get('SWEEP_VARIANTS', '')
 CTAS_LIST = tuple(int(t) for t in os.environ.get('SWEEP_CTAS', '3').split(','))
+LAYOUTS = tuple(int(t) for t in os.environ.get('SWEEP_LAYOUT', '0').split(','))
 
 
 def median_ms(fn, reps=20):
@@ -67,10 +68,12 @@ def main():
                     dims = ck.BlockDims(int(k), 1, 1)
                 dev.set_plan(0, 0, 0)
                 dev.set_schedule(0, 0)
+                dev.set_layout(0)
                 want = ck.spmv_device(m, xd, yd, dims=dims, variant=variant_i).clone()
-                for g, CTAS in [(g, c) for g in (GATHER if vb == 8 else (0,))
-                                for c in CTAS_LIST]:
+                for g, CTAS, LAY in [(g, c, la) for g in (GATHER if vb == 8 else (0,))
+                                     for c in CTAS_LIST for la in LAYOUTS]:
                   dev.set_schedule(g, CTAS)
+                  dev.set_layout(LAY)
                   for t in TILES:
                     for s in STAGES:
                         try:
@@ -83,12 +86,13 @@ def main():
                         gbs = spmv_bytes(n, n, nnz, vb) / (ms * 1e-3) / 1e9
                         rec = {"config": cfg, "dtype": str(dtype)[6:], "variant": variant_i,
                                "nx": dims.x if variant_i == "strided" else 0,
-                               "gather": g, "ctas": CTAS, "tile_cost": t, "stages": s, "ms": round(ms, 4),
+                               "gather": g, "ctas": CTAS, "layout": LAY, "tile_cost": t, "stages": s, "ms": round(ms, 4),
                                "gbs": round(gbs, 1), "bitwise_equal": same}
                         print(json.dumps(rec), flush=True)
                         out.append(rec)
             dev.set_plan(0, 0, 0)
-            dev.set_schedule(0, 0)
+            dev.set_schedule(2, 0)
+            dev.set_layout(0)
         del m, dev
         torch.cuda.empty_cache()
     os.makedirs("gpurun_out", exist_ok=True)
