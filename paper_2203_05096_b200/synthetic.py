@@ -152,6 +152,11 @@ def config_arrays(name: str, values: str = "laplacian"):
     """CSR arrays of a named config; C5 goes through ``csr_from_arrays``."""
     kind, shape, points = CONFIGS[name]
     if kind == "stencil":
+        from . import _native as nat
+        if values == "laplacian" and nat.device_count() > 0:
+            # generated in HBM (bitwise the host generator) and downloaded
+            rp, ci, va, _, _ = device_stencil(shape, points).download()
+            return len(rp) - 1, rp, ci, va
         return stencil_arrays(shape, points, values=values)
     from .format import csr_from_arrays
     rows, cols, vals = irregular_triplets(shape)

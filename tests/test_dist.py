@@ -325,3 +325,32 @@ def test_dist_cg_over_gloo(world):
     want, rr = _numpy_cg(shape, b, iters)
     np.testing.assert_allclose(x, want, rtol=1e-9, atol=1e-12)
     assert all(abs(t[3] - rr) <= 1e-9 * max(rr, 1e-300) + 1e-300 for t in results)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("config", ["C2", "C4"])
+def test_bench_multi_gpu_path_one_rank(config):
+    """bench.py's torchrun path (NCCL process group, slab partition, halo
+    exchange code, distributed CG) end to end with one rank (CSRK_DIST=1):
+    the JSON line has the contract's keys and the weak / strong labels."""
+    import json
+    import subprocess
+    import sys
+
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    port = _free_port()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=1",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), "bench.py", "--gpus", "1",
+           "--steps", "3", "--warmup", "3", "--config", config]
+    if config == "C4":
+        cmd += ["--side", "96", "--iters", "10"]
+    env = dict(os.environ, CSRK_DIST="1")
+    out = subprocess.run(cmd, cwd=repo, env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    for key in ("metric", "value", "unit", "n_gpus", "ms_per_step", "scaling", "e2e",
+                "roofline", "gpu_launches", "clocks"):
+        assert key in line, key
+    assert line["n_gpus"] == 1 and line["value"] > 0
+    assert line["scaling"] == ("weak" if config == "C2" else "strong")
+    assert line["e2e"]["h2d_bytes_per_step"] > 0
