@@ -311,7 +311,7 @@ def _mixed_rows_matrix(rng, n):
 
 
 @pytest.mark.parametrize("gather,ctas", [(0, 0), (1, 0), (2, 0), (0, 1), (1, 2), (2, 3),
-                                         (0, 4), (1, 8)])
+                                         (0, 4), (1, 8), (2, 2)])
 def test_schedules_do_not_change_bits(gather, ctas):
     """Gather mode x CTAs/SM x tile plan: y is the oracle's bit for bit in
     both orders (f64) and within 1e-5 of |A||x| (f32)."""
@@ -328,7 +328,7 @@ def test_schedules_do_not_change_bits(gather, ctas):
     scale = O.abs_row_dot(rp, ci, va, x)
     dev = m.device()
     dev.set_schedule(gather, ctas)
-    for tile_cost, stages in ((0, 0), (256, 3), (4096, 2)):
+    for tile_cost, stages in ((0, 0), (256, 3), (4096, 2), (700, 1)):
         dev.set_plan(tile_cost, 0, stages)
         plan = dev.plan()
         assert plan["gather_first"] == gather
