@@ -81,6 +81,7 @@ struct TilePlan {
   int layout = 0;         // serial f64 layout: 0 CSR, 1 sliced tiles
   uint64_t gen = 0;       // bumped whenever tile_row is rebuilt
   uint32_t *tile_row = nullptr;  // device, n_tiles + 1
+  uint32_t *tile_ptr = nullptr;  // device, n_tiles + 1 (same allocation): row_ptr[tile_row]
 };
 
 }  // namespace csrk

@@ -364,8 +364,8 @@ __global__ void __launch_bounds__(kThreads, 2)
                        const uint32_t *__restrict__ col_idx,
                        const V *__restrict__ vals, const V *__restrict__ x,
                        V *__restrict__ y, const uint32_t *__restrict__ tile_row,
-                       uint32_t n_tiles, uint32_t cap, uint32_t rcap,
-                       uint32_t stages) {
+                       const uint32_t *__restrict__ tile_ptr, uint32_t n_tiles,
+                       uint32_t cap, uint32_t rcap, uint32_t stages) {
   extern __shared__ __align__(128) unsigned char smem[];
   const Geometry geo(cap, rcap, stages, sizeof(V));
   uint64_t *full = reinterpret_cast<uint64_t *>(smem);
@@ -389,11 +389,26 @@ __global__ void __launch_bounds__(kThreads, 2)
     if (tid != 0) return;
     constexpr uint32_t VPV = Elem<V>::kPerVec;
     const uint64_t policy = evict_first_policy();
+    // the next tile's bounds (rows and their nonzero offsets, precomputed in
+    // the plan) load while this tile waits for its stage: the producer never
+    // spends a dependent global round trip between two TMA issues
+    uint32_t nr0 = 0, nr1 = 0, np0 = 0, np1 = 0;
+    if (blockIdx.x < n_tiles) {
+      nr0 = tile_row[blockIdx.x];
+      nr1 = tile_row[blockIdx.x + 1];
+      np0 = tile_ptr[blockIdx.x];
+      np1 = tile_ptr[blockIdx.x + 1];
+    }
     uint32_t i = 0;
     for (uint32_t t = blockIdx.x; t < n_tiles; t += grid, ++i) {
       const uint32_t s = i % stages;
-      const uint32_t r0 = tile_row[t], r1 = tile_row[t + 1];
-      const uint32_t p0 = row_ptr[r0], p1 = row_ptr[r1];
+      const uint32_t r0 = nr0, r1 = nr1, p0 = np0, p1 = np1;
+      if (t + grid < n_tiles) {
+        nr0 = tile_row[t + grid];
+        nr1 = tile_row[t + grid + 1];
+        np0 = tile_ptr[t + grid];
+        np1 = tile_ptr[t + grid + 1];
+      }
       if (i >= stages) mbar_wait(&empty[s], ((i / stages) + 1) & 1);
       StageMeta &md = meta[s];
       md.r0 = r0;
@@ -768,6 +783,14 @@ __global__ void tile_bounds_kernel(const uint32_t *__restrict__ row_ptr,
   tile_row[t] = group_start(sr_ptr, ssr_ptr, cut_k, lo, n_groups, n_rows);
 }
 
+// tile_ptr[t] = row_ptr[tile_row[t]]: the first nonzero of every tile
+__global__ void tile_ptr_kernel(const uint32_t *__restrict__ row_ptr,
+                                const uint32_t *__restrict__ tile_row, int64_t n_tiles,
+                                uint32_t *__restrict__ tile_ptr) {
+  const int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (t <= n_tiles) tile_ptr[t] = row_ptr[tile_row[t]];
+}
+
 // max column read by the rows of each chunk [row_cut[c], row_cut[c+1])
 __global__ void chunk_max_col_kernel(const uint32_t *__restrict__ row_ptr,
                                      const uint32_t *__restrict__ col_idx,
@@ -849,7 +872,7 @@ int launch_stream(const csrk_matrix *m, const V *vals, const V *x, V *y,
   if (grid > count) grid = count;
   if (grid < 1) return CSRK_OK;
   kern<<<static_cast<unsigned>(grid), kThreads, smem, stream>>>(
-      m->row_ptr, m->col_idx, vals, x, y, pl.tile_row + t0,
+      m->row_ptr, m->col_idx, vals, x, y, pl.tile_row + t0, pl.tile_ptr + t0,
       static_cast<uint32_t>(count), geo.cap, geo.rcap, geo.stages);
   CSRK_CUDA_TRY(cudaGetLastError());
   return CSRK_OK;
@@ -1037,12 +1060,17 @@ int ensure_plan(csrk_matrix *m, int64_t tile_cost, int64_t cap, int64_t stages,
   if (m->plan.tile_row) {
     CSRK_CUDA_TRY(cudaFree(m->plan.tile_row));
     m->plan.tile_row = nullptr;
+    m->plan.tile_ptr = nullptr;
   }
-  CSRK_CUDA_TRY(cudaMalloc(&m->plan.tile_row, (n_tiles + 1) * sizeof(uint32_t)));
+  // one allocation: tile_row[n_tiles + 1] then tile_ptr[n_tiles + 1]
+  CSRK_CUDA_TRY(cudaMalloc(&m->plan.tile_row, 2 * (n_tiles + 1) * sizeof(uint32_t)));
+  m->plan.tile_ptr = m->plan.tile_row + (n_tiles + 1);
   const int64_t blocks = (n_tiles + 1 + 255) / 256;
   tile_bounds_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(
       m->row_ptr, m->sr_ptr, m->ssr_ptr, cut_k, n_cuts, m->n_rows, pitch,
       n_tiles, m->plan.tile_row);
+  tile_ptr_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(
+      m->row_ptr, m->plan.tile_row, n_tiles, m->plan.tile_ptr);
   CSRK_CUDA_TRY(cudaGetLastError());
   m->pipe.plan_tiles = -1;  // host-pipeline cuts index the old tiles
   ++m->plan.gen;            // and the sliced copy belongs to the old plan
