@@ -230,6 +230,17 @@ int csrk_coo_to_csr(int device, int64_t n_rows, int64_t n_cols, int64_t count,
                     const int64_t *rows, const int64_t *cols, const double *vals,
                     csrk_matrix **out);
 
+/* Entry lines of a coordinate Matrix Market body (everything after the size
+ * line), parsed on all host cores: rows / cols 0-based, vals (1.0 for
+ * pattern files).  The loop of read_matrix_market (io.py:96-206) for large
+ * files; strict -- a line outside the plain grammar, an out-of-range index,
+ * a skew-symmetric diagonal or a count other than n_entries returns
+ * CSRK_EINVAL, and the caller re-reads the body with the reference's loop
+ * for the exact error. */
+int csrk_mm_parse(const char *buf, int64_t len, int64_t n_entries, int with_value,
+                  int64_t n_rows, int64_t n_cols, int skew, int64_t *rows, int64_t *cols,
+                  double *vals);
+
 /* Synthetic stencil generator writing canonical CSR on the device
  * (SURVEY.md §8(d)); shape = {nz, ny, nx} (nz = 1 for 2D), points = 5, 7, 27.
  * Produces a k = 1 handle (natural order). */

@@ -77,6 +77,8 @@ _SIGNATURES = {
     "csrk_sort_pairs": ([C.c_int, I64, P, P, C.c_int, C.c_int, P], C.c_int),
     "csrk_stencil": ([C.c_int, I64, I64, I64, C.c_int, C.POINTER(P)], C.c_int),
     "csrk_coo_to_csr": ([C.c_int, I64, I64, I64, I64P, I64P, F64P, C.POINTER(P)], C.c_int),
+    "csrk_mm_parse": ([C.c_char_p, I64, I64, C.c_int, I64, I64, C.c_int, I64P, I64P, F64P],
+                      C.c_int),
     "csrk_stencil_slab": ([C.c_int, I64, I64, I64, C.c_int, I64, I64, C.POINTER(P)],
                           C.c_int),
     "csrk_band_k": ([I64, U32P, U32P, C.c_int, F64P, C.POINTER(P)], C.c_int),
@@ -128,6 +130,11 @@ def check(rc: int) -> None:
 
 def call(name: str, *args) -> None:
     check(getattr(lib(), name)(*args))
+
+
+def call_rc(name: str, *args) -> int:
+    """Call without raising; returns the CSRK_* code."""
+    return int(getattr(lib(), name)(*args))
 
 
 def u32p(a: np.ndarray):

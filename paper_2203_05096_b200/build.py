@@ -24,7 +24,7 @@ LIB_DIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIB_DIR, "libcsrk_cuda.so")
 
 CUDA_SOURCES = ["abi.cu", "spmv.cu", "listing.cu", "construct.cu", "cg.cu", "sort.cu", "graph.cu", "rcm.cu", "coarsen.cu", "bandk_dev.cu"]
-CXX_SOURCES = ["bandk.cpp"]
+CXX_SOURCES = ["bandk.cpp", "mmio.cpp"]
 HEADERS = [os.path.join(CSRC, "internal.h"), os.path.join(REPO, "include", "csrk.h")]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

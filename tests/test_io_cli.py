@@ -145,3 +145,58 @@ def test_cli_commands_on_device(mtx, capsys):
     assert main(["tune", mtx, "--device", "b200", "--grid", "--grid-reps", "1"]) == 0
     out = json.loads(capsys.readouterr().out)
     assert len(out["table"]) == 64
+
+
+@pytest.mark.parametrize("field,symmetry", [("real", "general"), ("integer", "symmetric"),
+                                            ("pattern", "general"), ("real", "skew-symmetric")])
+def test_native_matrix_market_body_equals_python_loop(tmp_path, monkeypatch, field, symmetry):
+    """csrk_mm_parse (all host cores) parses large bodies to exactly what the
+    reference's line loop yields (io.py:96-206), comments and blank lines
+    included, and irregular lines fall back to the loop's exact errors."""
+    from paper_2203_05096_b200 import format as F
+    from paper_2203_05096_b200 import io as mio
+    monkeypatch.setattr(F, "DEVICE_COO_MIN", 1 << 62)  # host canonicalisation here
+    rng = np.random.default_rng(len(field) + len(symmetry))
+    n, m = 3000, 30000
+    r = rng.integers(1, n + 1, m).tolist()
+    c = rng.integers(1, n + 1, m).tolist()
+    if symmetry == "skew-symmetric":
+        c = [(ci % n) + 1 if ci == ri else ci for ri, ci in zip(r, c)]
+    v = (rng.standard_normal(m) * 10.0 ** rng.uniform(-30, 30, m)).tolist()
+    if field == "integer":
+        v = rng.integers(-9, 10, m).tolist()
+
+    def entry(k):
+        if field == "pattern":
+            return f"{r[k]} {c[k]}"
+        return f"  {r[k]}\t{c[k]}  {v[k]!r} " if k % 7 == 0 else f"{r[k]} {c[k]} {v[k]!r}"
+
+    body = [entry(k) for k in range(m)]
+    body.insert(10, "% a comment")
+    body.insert(2000, "")
+    body.insert(20000, "   % indented comment")
+    text = "\n".join([f"%%MatrixMarket matrix coordinate {field} {symmetry}", "% header",
+                      f"{n} {n} {m}"] + body) + "\n"
+    path = tmp_path / "a.mtx"
+    path.write_text(text)
+
+    def both():
+        out = []
+        for threshold in (1, 1 << 62):
+            monkeypatch.setattr(mio, "NATIVE_MIN_ENTRIES", threshold)
+            try:
+                a = mio.read_matrix_market(str(path))
+                out.append((a.row_ptr.tobytes(), a.col_idx.tobytes(), a.vals.tobytes()))
+            except mio.MatrixMarketError as e:
+                out.append(str(e))
+        return out
+
+    native, python = both()
+    assert native == python and not isinstance(native, str)
+    for k, bad in ((7000, f"{n + 1} 1 1.0"), (15000, "1 2 3 4"), (25000, "1 2 nan(7)")):
+        lines = text.split("\n")
+        lines[k] = bad
+        path.write_text("\n".join(lines))
+        native, python = both()
+        assert native == python
+        assert isinstance(native, str) and native.startswith(f"line {k + 1}:")
