@@ -88,7 +88,7 @@ int csrk_matrix_download(const csrk_matrix *m, uint32_t *row_ptr,
 int csrk_matrix_add_f32(csrk_matrix *m);
 /* Tile plan of the streaming kernel: contiguous row ranges balanced by
  * cost = nonzeros + rows (tile_cost per tile), cut only on group boundaries
- * (SSRs for k=3, SRs for k=2) when every group costs at most tile_cost / 2;
+ * (SSRs for k=3, SRs for k=2) when every group costs at most tile_cost / 8;
  * cap = stage capacity in nonzeros (larger tiles run in direct mode);
  * stages = TMA ring depth per CTA.  0 = defaults. */
 int csrk_matrix_set_plan(csrk_matrix *m, int64_t tile_cost, int64_t cap,

@@ -28,6 +28,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstdlib>
+#include <cstring>
 
 #include "internal.h"
 
@@ -1039,7 +1040,13 @@ int ensure_plan(csrk_matrix *m, int64_t tile_cost, int64_t cap, int64_t stages,
     CSRK_CUDA_TRY(cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, s));
     CSRK_CUDA_TRY(cudaStreamSynchronize(s));
     cudaFreeAsync(d, s);
-    if (static_cast<int64_t>(h) * 2 <= tile_cost) {
+    // Group-aligned cuts (the paper's block <-> SSR mapping) shrink the
+    // pitch by the largest group so every tile fits its stage; beyond an
+    // eighth of a tile that costs more than the alignment is worth
+    // (natural-order 7-point 256^3 with 64-row SSRs: 6.27 TB/s aligned,
+    // 6.71 TB/s cut on rows, profiles/r01_sched_sweep.txt), so large groups
+    // are cut on rows -- results do not depend on the cuts.
+    if (static_cast<int64_t>(h) * 8 <= tile_cost) {
       cut_k = m->k;
       n_cuts = n_groups;
       max_group = static_cast<int64_t>(h);
