@@ -489,6 +489,21 @@ def main(argv=None):
         if rank == 0:
             print(msg, file=sys.stderr, flush=True)
 
+    # libraries may write to the process's stdout (NCCL prints its version
+    # line at communicator creation): keep fd 1 for the one JSON line
+    saved = os.dup(1)
+    os.dup2(2, 1)
+    try:
+        line = _run(args, log)
+    finally:
+        sys.stdout.flush()
+        os.dup2(saved, 1)
+        os.close(saved)
+    if rank == 0 and line is not None:
+        print(json.dumps(line), flush=True)
+
+
+def _run(args, log):
     if args.impl == "reference":
         line = run_reference(args, log)
     elif args.config == "C4" and int(os.environ.get("WORLD_SIZE", "1")) == 1 and \
@@ -496,8 +511,7 @@ def main(argv=None):
         line = run_loop(args, log)
     else:
         line = run_ours(args, log)
-    if rank == 0 and line is not None:
-        print(json.dumps(line), flush=True)
+    return line
 
 
 if __name__ == "__main__":
