@@ -288,6 +288,9 @@ def run_ours(args, log):
                    "ssrs_target": params.ssrs, "srs_target": params.srs,
                    "n_sr": m.num_super_rows, "n_ssr": m.num_ssr,
                    "kernel": f"csrk_stream_kernel ({variant})",
+                   "plan": {k: v for k, v in m.device().plan().items()
+                            if k in ("tile_cost", "stages", "n_tiles", "group_aligned",
+                                     "gather_first", "ctas_per_sm")},
                    "parallelism": "1 GPU",
                    "l2": ("inputs larger than L2 (algorithmic %.2f GB per step vs 126 MB "
                           "L2); no flush" % (algo_bytes / 1e9)) if not flush else
