@@ -354,3 +354,27 @@ def test_bench_multi_gpu_path_one_rank(config):
     assert line["n_gpus"] == 1 and line["value"] > 0
     assert line["scaling"] == ("weak" if config == "C2" else "strong")
     assert line["e2e"]["h2d_bytes_per_step"] > 0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("chunks", [1, 3, 8])
+def test_slab_host_pipeline_bitwise(chunks):
+    """SlabSpMV.step_host (chunked H2D / interior tiles / D2H on three
+    streams) gives the bits of the device-resident step (one rank)."""
+    shape = (40, 48, 56)
+    op = D.SlabSpMV(shape, 7, 0, 1)
+    lay = op.lay
+    x = torch.from_numpy(np.random.default_rng(chunks).uniform(-1, 1, lay.n_own))
+    x_local = torch.zeros(lay.n_cols, dtype=torch.float64, device="cuda")
+    y = torch.empty(lay.n_own, dtype=torch.float64, device="cuda")
+    x_local[lay.own_off:lay.own_off + lay.n_own] = x.cuda()
+    op.compute(x_local, y)
+    torch.cuda.synchronize()
+    want = y.cpu().numpy().copy()
+    x_pin = x.clone().pin_memory()
+    y_pin = torch.full((lay.n_own,), float("nan"), dtype=torch.float64).pin_memory()
+    x_local.zero_()
+    for _ in range(2):
+        op.step_host(x_pin, y_pin, x_local, y, chunks=chunks)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(y_pin.numpy(), want)
