@@ -292,7 +292,7 @@ __device__ __forceinline__ double subwarp_tree(double acc) {
 }
 
 // rows [r0, r1) with staged (or global) arrays; `srp(r)` yields row_ptr[r]
-template <typename V, int NX, bool PROD = false, typename RowPtr>
+template <typename V, int NX, bool PROD = false, int LB = 4, typename RowPtr>
 __device__ __forceinline__ void compute_rows(uint32_t r0, uint32_t r1,
                                              const V *__restrict__ sv,
                                              const uint32_t *__restrict__ sc,
@@ -319,7 +319,7 @@ __device__ __forceinline__ void compute_rows(uint32_t r0, uint32_t r1,
         if constexpr (PROD)
           acc = lane_products<NX, V>(sv, srp(r), srp(r + 1), lane);
         else
-          acc = lane_partial<NX, 4, V>(sv, sc, srp(r), srp(r + 1), lane, x);
+          acc = lane_partial<NX, LB, V>(sv, sc, srp(r), srp(r + 1), lane, x);
       }
       acc = subwarp_tree<P>(acc);
       if (r < r1 && lane == 0) y[r] = Elem<V>::out(acc);
@@ -359,7 +359,7 @@ __device__ void compute_direct(uint32_t r0, uint32_t r1,
   }
 }
 
-template <typename V, int NX, bool GF>
+template <typename V, int NX, bool GF, int LB = 4>
 __global__ void __launch_bounds__(kThreads, 2)
     csrk_stream_kernel(const uint32_t *__restrict__ row_ptr,
                        const uint32_t *__restrict__ col_idx,
@@ -458,8 +458,8 @@ __global__ void __launch_bounds__(kThreads, 2)
         // generic-proxy writes to the stage precede the next TMA fill of it
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       } else {
-        compute_rows<V, NX>(md.r0, md.r1, sv, sc, [&](uint32_t r) { return sr[r]; },
-                            x, y, ct);
+        compute_rows<V, NX, false, LB>(md.r0, md.r1, sv, sc,
+                                       [&](uint32_t r) { return sr[r]; }, x, y, ct);
       }
     } else {
       compute_direct<V, NX>(md.r0, md.r1, row_ptr, col_idx, vals, x, y, ct);
@@ -816,14 +816,14 @@ __global__ void chunk_max_col_kernel(const uint32_t *__restrict__ row_ptr,
   }
 }
 
-template <typename V, int NX, bool GF>
+template <typename V, int NX, bool GF, int LB = 4>
 int launch_stream(const csrk_matrix *m, const V *vals, const V *x, V *y,
                   cudaStream_t stream, int64_t t0, int64_t t1) {
   const TilePlan &pl = m->plan;
   const Geometry geo(static_cast<uint32_t>(pl.cap), static_cast<uint32_t>(pl.rcap),
                      static_cast<uint32_t>(pl.stages), sizeof(V));
   const size_t smem = geo.total_bytes();
-  auto kern = csrk_stream_kernel<V, NX, GF>;
+  auto kern = csrk_stream_kernel<V, NX, GF, LB>;
   // attribute + occupancy queries cost host time per launch; cache them per
   // instantiation and shared-memory size (the chunked host pipeline launches
   // the kernel many times per SpMV)
@@ -937,10 +937,17 @@ template <typename V, bool GF>
 int dispatch_nx(const csrk_matrix *m, int variant, int nx, const V *vals,
                 const V *x, V *y, cudaStream_t s, int64_t t0, int64_t t1) {
   if (variant == CSRK_SERIAL) return launch_stream<V, 0, GF>(m, vals, x, y, s, t0, t1);
+  // Lanes gather LB of their strided elements per batch: 8 when a lane holds
+  // >= 5 of its row's nonzeros on average (27-point rows with nx = 4: C3
+  // 5.81 -> 6.06 TB/s), 4 for short rows (C2 / C5 lose with 8: registers)
+  int p = 1;
+  while (p < nx) p <<= 1;
+  const bool wide = m->plan.mean_row / p >= 5.0;
   switch (nx) {
-#define CSRK_NX_CASE(N) \
-  case N:               \
-    return launch_stream<V, N, GF>(m, vals, x, y, s, t0, t1);
+#define CSRK_NX_CASE(N)                                          \
+  case N:                                                        \
+    return wide ? launch_stream<V, N, GF, 8>(m, vals, x, y, s, t0, t1) \
+                : launch_stream<V, N, GF, 4>(m, vals, x, y, s, t0, t1);
     CSRK_NX_CASE(1)
     CSRK_NX_CASE(2)
     CSRK_NX_CASE(3)
