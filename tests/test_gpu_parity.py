@@ -454,3 +454,25 @@ def test_sliced_layout_bitwise(layout, kind):
                                torch.cuda.current_stream().cuda_stream)
         torch.cuda.synchronize()
         np.testing.assert_array_equal(yd.cpu().numpy(), want)
+
+
+def test_tile_range_and_layout_argument_checks():
+    """The C-ABI rejects bad tile ranges and layouts with ValueError."""
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(12)
+    a = random_csr(rng, 2000, 2000, 0.004)
+    dev = a.device()
+    dev.set_plan(64, 0, 2)
+    nt = dev.plan()["n_tiles"]
+    x = torch.zeros(2000, dtype=torch.float64, device="cuda")
+    y = torch.zeros_like(x)
+    s = torch.cuda.current_stream().cuda_stream
+    with pytest.raises(ValueError, match="tile range"):
+        dev.spmv_tiles_ptr(x.data_ptr(), y.data_ptr(), 0, nt + 1, s)
+    with pytest.raises(ValueError, match="tile range"):
+        dev.spmv_tiles_ptr(x.data_ptr(), y.data_ptr(), 3, 2, s)
+    dev.spmv_tiles_ptr(x.data_ptr(), y.data_ptr(), 2, 2, s)  # empty range: no-op
+    with pytest.raises(ValueError, match="layout"):
+        dev.set_layout(2)
+    tr = dev.tile_rows()
+    assert tr[0] == 0 and tr[-1] == 2000 and len(tr) == nt + 1 and np.all(np.diff(tr) >= 0)
