@@ -57,6 +57,7 @@ static void release(csrk_matrix *m) {
   cudaFree(m->sr_ptr);
   cudaFree(m->ssr_ptr);
   cudaFree(m->plan.tile_row);
+  cudaFree(m->plan.long_rows);
   csrk::free_sliced(m);
   cudaFree(m->x_stage);
   cudaFree(m->y_stage);

@@ -22,6 +22,7 @@ constexpr int64_t kDefaultTileCost = 2048;  // nonzeros + rows per tile
 constexpr int64_t kDefaultStages = 2;       // TMA ring depth per CTA (plan sweep)
 constexpr int64_t kDefaultCtasPerSm = 3;    // resident streaming CTAs per SM
 constexpr int kGatherAuto = 2;
+constexpr int64_t kLongRow = 128;  // rows longer than this are summed a warp each
 
 // Auto schedule (round-1 plan sweeps, profiles/r01_sched_sweep.txt):
 //  * regular rows: 3 CTAs per SM in f64, 4 in f32 (half the bytes per
@@ -82,6 +83,8 @@ struct TilePlan {
   uint64_t gen = 0;       // bumped whenever tile_row is rebuilt
   uint32_t *tile_row = nullptr;  // device, n_tiles + 1
   uint32_t *tile_ptr = nullptr;  // device, n_tiles + 1 (same allocation): row_ptr[tile_row]
+  uint32_t *long_rows = nullptr;  // rows longer than kLongRow (any order)
+  int64_t n_long = 0;
 };
 
 }  // namespace csrk

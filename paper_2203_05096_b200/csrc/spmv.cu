@@ -292,18 +292,23 @@ __device__ __forceinline__ double subwarp_tree(double acc) {
 }
 
 // rows [r0, r1) with staged (or global) arrays; `srp(r)` yields row_ptr[r]
+// Rows longer than `long_len` nonzeros are skipped: the long-row kernel
+// (below) sums them with a whole warp each.
 template <typename V, int NX, bool PROD = false, int LB = 4, typename RowPtr>
 __device__ __forceinline__ void compute_rows(uint32_t r0, uint32_t r1,
                                              const V *__restrict__ sv,
                                              const uint32_t *__restrict__ sc,
                                              RowPtr srp, const V *__restrict__ x,
-                                             V *__restrict__ y, int ct) {
+                                             V *__restrict__ y, int ct,
+                                             uint32_t long_len = 0xffffffffu) {
   if constexpr (NX == 0) {
     for (uint32_t r = r0 + ct; r < r1; r += kConsumers) {
+      const uint32_t s = srp(r), e = srp(r + 1);
+      if (e - s > long_len) continue;
       if constexpr (PROD)
-        y[r] = Elem<V>::out(row_products<V>(sv, srp(r), srp(r + 1)));
+        y[r] = Elem<V>::out(row_products<V>(sv, s, e));
       else
-        y[r] = Elem<V>::out(row_serial<8, V>(sv, sc, srp(r), srp(r + 1), x));
+        y[r] = Elem<V>::out(row_serial<8, V>(sv, sc, s, e, x));
     }
   } else {
     constexpr int P = pow2_ceil(NX);
@@ -315,14 +320,19 @@ __device__ __forceinline__ void compute_rows(uint32_t r0, uint32_t r1,
     for (uint32_t base = r0 + warp_first; base < r1; base += kSubs) {
       const uint32_t r = base + (sub - warp_first);
       double acc = 0.0;
-      if (r < r1) {
-        if constexpr (PROD)
-          acc = lane_products<NX, V>(sv, srp(r), srp(r + 1), lane);
-        else
-          acc = lane_partial<NX, LB, V>(sv, sc, srp(r), srp(r + 1), lane, x);
+      bool mine = r < r1;
+      if (mine) {
+        const uint32_t s = srp(r), e = srp(r + 1);
+        mine = e - s <= long_len;
+        if (mine) {
+          if constexpr (PROD)
+            acc = lane_products<NX, V>(sv, s, e, lane);
+          else
+            acc = lane_partial<NX, LB, V>(sv, sc, s, e, lane, x);
+        }
       }
       acc = subwarp_tree<P>(acc);
-      if (r < r1 && lane == 0) y[r] = Elem<V>::out(acc);
+      if (mine && lane == 0) y[r] = Elem<V>::out(acc);
     }
   }
 }
@@ -335,11 +345,12 @@ __device__ void compute_direct(uint32_t r0, uint32_t r1,
                                const uint32_t *__restrict__ col_idx,
                                const V *__restrict__ vals,
                                const V *__restrict__ x, V *__restrict__ y,
-                               int ct) {
+                               int ct, uint32_t long_len = 0xffffffffu) {
   if constexpr (NX == 0) {
     const int lane = ct & 31, warp = ct >> 5;
     for (uint32_t r = r0 + warp; r < r1; r += kConsumerWarps) {
       const uint32_t s = row_ptr[r], e = row_ptr[r + 1];
+      if (e - s > long_len) continue;
       double acc = 0.0;
       for (uint32_t p0 = s; p0 < e; p0 += 32) {
         const uint32_t p = p0 + lane;
@@ -355,7 +366,7 @@ __device__ void compute_direct(uint32_t r0, uint32_t r1,
     }
   } else {
     compute_rows<V, NX>(r0, r1, vals, col_idx,
-                        [&](uint32_t r) { return row_ptr[r]; }, x, y, ct);
+                        [&](uint32_t r) { return row_ptr[r]; }, x, y, ct, long_len);
   }
 }
 
@@ -366,7 +377,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                        const V *__restrict__ vals, const V *__restrict__ x,
                        V *__restrict__ y, const uint32_t *__restrict__ tile_row,
                        const uint32_t *__restrict__ tile_ptr, uint32_t n_tiles,
-                       uint32_t cap, uint32_t rcap, uint32_t stages) {
+                       uint32_t cap, uint32_t rcap, uint32_t stages, uint32_t long_len) {
   extern __shared__ __align__(128) unsigned char smem[];
   const Geometry geo(cap, rcap, stages, sizeof(V));
   uint64_t *full = reinterpret_cast<uint64_t *>(smem);
@@ -454,19 +465,120 @@ __global__ void __launch_bounds__(kThreads, 2)
         gather_products<V>(svw, sc, sr[md.r0], sr[md.r1], x, ct);
         asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory");
         compute_rows<V, NX, true>(md.r0, md.r1, sv, sc,
-                                  [&](uint32_t r) { return sr[r]; }, x, y, ct);
+                                  [&](uint32_t r) { return sr[r]; }, x, y, ct, long_len);
         // generic-proxy writes to the stage precede the next TMA fill of it
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       } else {
         compute_rows<V, NX, false, LB>(md.r0, md.r1, sv, sc,
-                                       [&](uint32_t r) { return sr[r]; }, x, y, ct);
+                                       [&](uint32_t r) { return sr[r]; }, x, y, ct,
+                                       long_len);
       }
     } else {
-      compute_direct<V, NX>(md.r0, md.r1, row_ptr, col_idx, vals, x, y, ct);
+      compute_direct<V, NX>(md.r0, md.r1, row_ptr, col_idx, vals, x, y, ct, long_len);
     }
     __syncwarp();
     if ((ct & 31) == 0) mbar_arrive(&empty[s]);
   }
+}
+
+// ---- long rows -------------------------------------------------------------
+//
+// Power-law matrices (the paper's failure mode) put rows of
+// thousands of nonzeros into single tiles: a tile then occupies one thread
+// (serial order) or one sub-warp (strided order) of its CTA for the whole
+// row while the rest of the CTA -- and the tiles queued behind it -- wait.
+// Rows longer than kLongRow are listed when the plan is built, skipped by the
+// streaming kernel, and summed here with a whole warp each, spread over the
+// GPU: the serial order gathers 128 products per step in parallel and lane 0
+// adds them left to right (the reference's chain, bit for bit); the strided
+// order runs its nx lane chains and the halving tree as the streaming kernel
+// does.  Rows outside [rows_lo, rows_hi) (a tile-range launch) are skipped.
+
+template <typename V, int NX>
+__global__ void __launch_bounds__(256)
+    long_rows_kernel(const uint32_t *__restrict__ row_ptr, const uint32_t *__restrict__ col_idx,
+                     const V *__restrict__ vals, const V *__restrict__ x, V *__restrict__ y,
+                     const uint32_t *__restrict__ long_rows, int64_t n_long,
+                     const uint32_t *__restrict__ rows_lo, const uint32_t *__restrict__ rows_hi) {
+  constexpr int kChunk = 128;
+  __shared__ double buf[8][kChunk];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint32_t lo = *rows_lo, hi = *rows_hi;
+  const int64_t warps = int64_t(gridDim.x) * 8;
+  for (int64_t i = blockIdx.x * int64_t(8) + w; i < n_long; i += warps) {
+    const uint32_t r = long_rows[i];
+    if (r < lo || r >= hi) continue;
+    const uint32_t s = row_ptr[r], e = row_ptr[r + 1];
+    if constexpr (NX == 0) {
+      // the next chunk's gathers are issued before lane 0 walks the current
+      // one, so their latency hides behind the ordered adds
+      constexpr int K = kChunk / 32;
+      double v[K], xv[K];
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const uint32_t p = s + k * 32 + lane;
+        const uint32_t q = p < e ? p : e - 1;
+        v[k] = static_cast<double>(vals[q]);
+        xv[k] = Elem<V>::load_x(x, col_idx[q]);
+      }
+      double acc = 0.0;
+      for (uint32_t p0 = s; p0 < e; p0 += kChunk) {
+        double prod[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) prod[k] = __dmul_rn(v[k], xv[k]);
+        if (p0 + kChunk < e) {
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            const uint32_t p = p0 + kChunk + k * 32 + lane;
+            const uint32_t q = p < e ? p : e - 1;
+            v[k] = static_cast<double>(vals[q]);
+            xv[k] = Elem<V>::load_x(x, col_idx[q]);
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < K; ++k) buf[w][k * 32 + lane] = prod[k];
+        __syncwarp();
+        if (lane == 0) {
+          const uint32_t cnt = e - p0 < uint32_t(kChunk) ? e - p0 : uint32_t(kChunk);
+          for (uint32_t j = 0; j < cnt; ++j) acc = __dadd_rn(acc, buf[w][j]);
+        }
+        __syncwarp();
+      }
+      if (lane == 0) y[r] = Elem<V>::out(acc);
+    } else {
+      constexpr int P = pow2_ceil(NX);
+      double acc = lane < P ? lane_partial<NX, 8, V>(vals, col_idx, s, e, lane, x) : 0.0;
+      acc = subwarp_tree<P>(acc);
+      if (lane == 0) y[r] = Elem<V>::out(acc);
+    }
+  }
+}
+
+__global__ void long_rows_list_kernel(const uint32_t *__restrict__ row_ptr, int64_t n_rows,
+                                      uint32_t min_len, uint32_t *__restrict__ out,
+                                      unsigned long long *__restrict__ count) {
+  for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r < n_rows;
+       r += int64_t(gridDim.x) * blockDim.x)
+    if (row_ptr[r + 1] - row_ptr[r] > min_len) {
+      const unsigned long long k = atomicAdd(count, 1ull);
+      if (out) out[k] = static_cast<uint32_t>(r);
+    }
+}
+
+template <typename V, int NX>
+int launch_long_rows(const csrk_matrix *m, const V *vals, const V *x, V *y, cudaStream_t stream,
+                     int64_t t0, int64_t t1) {
+  const TilePlan &pl = m->plan;
+  if (t1 < 0 || t1 > pl.n_tiles) t1 = pl.n_tiles;
+  if (t0 < 0) t0 = 0;
+  int64_t blocks = (pl.n_long + 7) / 8;
+  if (blocks > int64_t(m->sm_count) * 8) blocks = int64_t(m->sm_count) * 8;
+  if (blocks < 1) return CSRK_OK;
+  long_rows_kernel<V, NX><<<static_cast<unsigned>(blocks), 256, 0, stream>>>(
+      m->row_ptr, m->col_idx, vals, x, y, pl.long_rows, pl.n_long, pl.tile_row + t0,
+      pl.tile_row + t1);
+  CSRK_CUDA_TRY(cudaGetLastError());
+  return CSRK_OK;
 }
 
 // ---- sliced tiles (serial order) -----------------------------------------
@@ -874,7 +986,8 @@ int launch_stream(const csrk_matrix *m, const V *vals, const V *x, V *y,
   if (grid < 1) return CSRK_OK;
   kern<<<static_cast<unsigned>(grid), kThreads, smem, stream>>>(
       m->row_ptr, m->col_idx, vals, x, y, pl.tile_row + t0, pl.tile_ptr + t0,
-      static_cast<uint32_t>(count), geo.cap, geo.rcap, geo.stages);
+      static_cast<uint32_t>(count), geo.cap, geo.rcap, geo.stages,
+      m->plan.n_long > 0 ? static_cast<uint32_t>(kLongRow) : 0xffffffffu);
   CSRK_CUDA_TRY(cudaGetLastError());
   return CSRK_OK;
 }
@@ -934,8 +1047,55 @@ int launch_sliced(const csrk_matrix *m, const double *x, double *y, cudaStream_t
 }
 
 template <typename V, bool GF>
+int dispatch_main(const csrk_matrix *m, int variant, int nx, const V *vals,
+                  const V *x, V *y, cudaStream_t s, int64_t t0, int64_t t1);
+
+template <typename V>
+int dispatch_long(const csrk_matrix *m, int variant, int nx, const V *vals, const V *x, V *y,
+                  cudaStream_t s, int64_t t0, int64_t t1) {
+  if (m->plan.n_long == 0) return CSRK_OK;
+  if (variant == CSRK_SERIAL) return launch_long_rows<V, 0>(m, vals, x, y, s, t0, t1);
+  switch (nx) {
+#define CSRK_LONG_CASE(N) \
+  case N:                 \
+    return launch_long_rows<V, N>(m, vals, x, y, s, t0, t1);
+    CSRK_LONG_CASE(1)
+    CSRK_LONG_CASE(2)
+    CSRK_LONG_CASE(3)
+    CSRK_LONG_CASE(4)
+    CSRK_LONG_CASE(5)
+    CSRK_LONG_CASE(6)
+    CSRK_LONG_CASE(7)
+    CSRK_LONG_CASE(8)
+    CSRK_LONG_CASE(9)
+    CSRK_LONG_CASE(10)
+    CSRK_LONG_CASE(11)
+    CSRK_LONG_CASE(12)
+    CSRK_LONG_CASE(13)
+    CSRK_LONG_CASE(14)
+    CSRK_LONG_CASE(15)
+    CSRK_LONG_CASE(16)
+    CSRK_LONG_CASE(20)
+    CSRK_LONG_CASE(24)
+    CSRK_LONG_CASE(28)
+    CSRK_LONG_CASE(32)
+#undef CSRK_LONG_CASE
+    default:
+      return CSRK_OK;  // (the main dispatch reports the unsupported nx)
+  }
+}
+
+template <typename V, bool GF>
 int dispatch_nx(const csrk_matrix *m, int variant, int nx, const V *vals,
                 const V *x, V *y, cudaStream_t s, int64_t t0, int64_t t1) {
+  const int rc = dispatch_main<V, GF>(m, variant, nx, vals, x, y, s, t0, t1);
+  if (rc != CSRK_OK) return rc;
+  return dispatch_long<V>(m, variant, nx, vals, x, y, s, t0, t1);
+}
+
+template <typename V, bool GF>
+int dispatch_main(const csrk_matrix *m, int variant, int nx, const V *vals,
+                  const V *x, V *y, cudaStream_t s, int64_t t0, int64_t t1) {
   if (variant == CSRK_SERIAL) return launch_stream<V, 0, GF>(m, vals, x, y, s, t0, t1);
   // Lanes gather LB of their strided elements per batch: 8 when a lane holds
   // >= 5 of its row's nonzeros on average (27-point rows with nx = 4: C3
@@ -1027,6 +1187,26 @@ int ensure_plan(csrk_matrix *m, int64_t tile_cost, int64_t cap, int64_t stages,
     m->plan.mean_row = mean;
     m->plan.row_var = static_cast<double>(h) / static_cast<double>(m->n_rows) - mean * mean;
     m->plan.row_stats = true;
+    // rows longer than kLongRow: listed once for the long-row kernel
+    unsigned long long *dn = nullptr, hn = 0;
+    CSRK_CUDA_TRY(cudaMallocAsync(&dn, sizeof(hn), s));
+    CSRK_CUDA_TRY(cudaMemsetAsync(dn, 0, sizeof(hn), s));
+    long_rows_list_kernel<<<148 * 8, 256, 0, s>>>(m->row_ptr, m->n_rows,
+                                                   static_cast<uint32_t>(kLongRow), nullptr, dn);
+    CSRK_CUDA_TRY(cudaGetLastError());
+    CSRK_CUDA_TRY(cudaMemcpyAsync(&hn, dn, sizeof(hn), cudaMemcpyDeviceToHost, s));
+    CSRK_CUDA_TRY(cudaStreamSynchronize(s));
+    if (hn > 0) {
+      CSRK_CUDA_TRY(cudaMalloc(&m->plan.long_rows, hn * sizeof(uint32_t)));
+      CSRK_CUDA_TRY(cudaMemsetAsync(dn, 0, sizeof(hn), s));
+      long_rows_list_kernel<<<148 * 8, 256, 0, s>>>(m->row_ptr, m->n_rows,
+                                                     static_cast<uint32_t>(kLongRow),
+                                                     m->plan.long_rows, dn);
+      CSRK_CUDA_TRY(cudaGetLastError());
+      CSRK_CUDA_TRY(cudaStreamSynchronize(s));
+    }
+    cudaFreeAsync(dn, s);
+    m->plan.n_long = static_cast<int64_t>(hn);
   }
   const int64_t n_groups = m->k == 3 ? m->n_ssr : (m->k == 2 ? m->n_sr : m->n_rows);
   // cut on group boundaries when every group is small against a tile
