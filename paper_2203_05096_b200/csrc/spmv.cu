@@ -509,46 +509,51 @@ __global__ void __launch_bounds__(256)
     const uint32_t r = long_rows[i];
     if (r < lo || r >= hi) continue;
     const uint32_t s = row_ptr[r], e = row_ptr[r + 1];
+    // every lane gathers the products of a 128-entry chunk (the next chunk's
+    // gathers issued before the current one is walked, so their latency
+    // hides behind the ordered adds); the chains then walk the chunk from
+    // shared memory: lane 0 alone in the serial order, lanes 0..nx-1 their
+    // strided subsequences (position mod nx) in the strided order
+    constexpr int K = kChunk / 32;
+    constexpr int L = NX == 0 ? 1 : NX;
+    double v[K], xv[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const uint32_t p = s + k * 32 + lane;
+      const uint32_t q = p < e ? p : e - 1;
+      v[k] = static_cast<double>(vals[q]);
+      xv[k] = Elem<V>::load_x(x, col_idx[q]);
+    }
+    double acc = 0.0;
+    for (uint32_t p0 = s; p0 < e; p0 += kChunk) {
+      double prod[K];
+#pragma unroll
+      for (int k = 0; k < K; ++k) prod[k] = __dmul_rn(v[k], xv[k]);
+      if (p0 + kChunk < e) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          const uint32_t p = p0 + kChunk + k * 32 + lane;
+          const uint32_t q = p < e ? p : e - 1;
+          v[k] = static_cast<double>(vals[q]);
+          xv[k] = Elem<V>::load_x(x, col_idx[q]);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < K; ++k) buf[w][k * 32 + lane] = prod[k];
+      __syncwarp();
+      if (lane < L) {
+        const uint32_t cnt = e - p0 < uint32_t(kChunk) ? e - p0 : uint32_t(kChunk);
+        const uint32_t off = (p0 - s) % L;  // position of chunk entry 0 modulo nx
+        for (uint32_t j = (lane + L - off) % L; j < cnt; j += L)
+          acc = __dadd_rn(acc, buf[w][j]);
+      }
+      __syncwarp();
+    }
     if constexpr (NX == 0) {
-      // the next chunk's gathers are issued before lane 0 walks the current
-      // one, so their latency hides behind the ordered adds
-      constexpr int K = kChunk / 32;
-      double v[K], xv[K];
-#pragma unroll
-      for (int k = 0; k < K; ++k) {
-        const uint32_t p = s + k * 32 + lane;
-        const uint32_t q = p < e ? p : e - 1;
-        v[k] = static_cast<double>(vals[q]);
-        xv[k] = Elem<V>::load_x(x, col_idx[q]);
-      }
-      double acc = 0.0;
-      for (uint32_t p0 = s; p0 < e; p0 += kChunk) {
-        double prod[K];
-#pragma unroll
-        for (int k = 0; k < K; ++k) prod[k] = __dmul_rn(v[k], xv[k]);
-        if (p0 + kChunk < e) {
-#pragma unroll
-          for (int k = 0; k < K; ++k) {
-            const uint32_t p = p0 + kChunk + k * 32 + lane;
-            const uint32_t q = p < e ? p : e - 1;
-            v[k] = static_cast<double>(vals[q]);
-            xv[k] = Elem<V>::load_x(x, col_idx[q]);
-          }
-        }
-#pragma unroll
-        for (int k = 0; k < K; ++k) buf[w][k * 32 + lane] = prod[k];
-        __syncwarp();
-        if (lane == 0) {
-          const uint32_t cnt = e - p0 < uint32_t(kChunk) ? e - p0 : uint32_t(kChunk);
-          for (uint32_t j = 0; j < cnt; ++j) acc = __dadd_rn(acc, buf[w][j]);
-        }
-        __syncwarp();
-      }
       if (lane == 0) y[r] = Elem<V>::out(acc);
     } else {
       constexpr int P = pow2_ceil(NX);
-      double acc = lane < P ? lane_partial<NX, 8, V>(vals, col_idx, s, e, lane, x) : 0.0;
-      acc = subwarp_tree<P>(acc);
+      acc = subwarp_tree<P>(lane < NX ? acc : 0.0);
       if (lane == 0) y[r] = Elem<V>::out(acc);
     }
   }

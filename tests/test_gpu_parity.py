@@ -140,7 +140,7 @@ def _long_row_matrix(rng, n, long_len, n_long=2):
     return ck.csr_from_arrays(n, n, rows, cols, rng.uniform(-1.0, 1.0, len(rows)))
 
 
-@pytest.mark.parametrize("long_len", [33, 5000, 40000])
+@pytest.mark.parametrize("long_len", [33, 129, 300, 5000, 40000])
 def test_long_rows_pack_and_spmv(long_len):
     """Rows longer than a warp / the shared stage: the device pack sorts them
     (bitonic paths) and the streaming kernel's long-row path keeps the
