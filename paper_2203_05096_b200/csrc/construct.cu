@@ -679,7 +679,7 @@ int group_uniform(csrk_matrix *m, int64_t srs, int64_t ssrs) {
   const int64_t tc = m->plan.tile_cost, cap = m->plan.cap, st = m->plan.stages;
   cudaFree(m->plan.tile_row);
   m->plan.tile_row = nullptr;
-  m->plan.tile_ptr = nullptr;
+  m->plan.tile_ptr = m->plan.tile_long = nullptr;
   m->pipe.plan_tiles = -1;
   CSRK_TRY(ensure_plan(m, tc, cap, st, m->stream));
   CSRK_CUDA_TRY(cudaStreamSynchronize(m->stream));

@@ -34,8 +34,12 @@ constexpr int64_t kLongRow = 128;  // rows longer than this are summed a warp ea
 inline int auto_ctas(double row_var, int value_bytes) {
   return row_var > 10.0 ? 2 : (value_bytes == 4 ? 4 : 3);
 }
-inline bool auto_gather(int variant, double mean_row) {
-  return variant == CSRK_SERIAL && mean_row > 16.0;
+// Gather first in the serial order when rows are long (C3: 27-nonzero rows)
+// or their lengths spread wider than their mean (a thread per row then waits
+// on the longest row of its warp; power-law rows, mean 9.8 / variance 238:
+// 1.67 -> 2.36 TB/s), inline otherwise (C5: mean 10 / variance 30 loses 2 %).
+inline bool auto_gather(int variant, double mean_row, double row_var) {
+  return variant == CSRK_SERIAL && (mean_row > 16.0 || row_var > mean_row * mean_row);
 }
 
 // Tile cost for a launch in the STRIDED order: the 256 consumer threads
@@ -83,9 +87,23 @@ struct TilePlan {
   uint64_t gen = 0;       // bumped whenever tile_row is rebuilt
   uint32_t *tile_row = nullptr;  // device, n_tiles + 1
   uint32_t *tile_ptr = nullptr;  // device, n_tiles + 1 (same allocation): row_ptr[tile_row]
-  uint32_t *long_rows = nullptr;  // rows longer than kLongRow (any order)
+  // rows longer than kLongRow: n_long row indices in the long-row kernel's
+  // work order (longest first), then n_long (start, end) nonzero ranges in
+  // row order -- the holes the streaming kernel does not stage -- then the
+  // n_long rows in row order
+  uint32_t *long_rows = nullptr;
+  uint32_t *tile_long = nullptr;  // n_tiles + 1 (tile_row's allocation): first hole per tile
   int64_t n_long = 0;
 };
+
+// the holes (uint2 pairs) follow the work order at an 8-byte boundary
+inline const uint2 *long_holes(const TilePlan &pl) {
+  return reinterpret_cast<const uint2 *>(pl.long_rows + ((pl.n_long + 1) & ~int64_t(1)));
+}
+// and the long rows in row order after the holes
+inline const uint32_t *long_rows_asc(const TilePlan &pl) {
+  return reinterpret_cast<const uint32_t *>(long_holes(pl) + pl.n_long);
+}
 
 }  // namespace csrk
 

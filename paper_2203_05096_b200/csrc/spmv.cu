@@ -164,7 +164,7 @@ struct StageMeta {
   uint32_t ca0;     // first staged col_idx element
   uint32_t ra0;     // first staged row_ptr element
   uint32_t mode;    // kStaged or kDirect
-  uint32_t pad0, pad1;
+  uint32_t h0, h1;  // the tile's long rows: holes[h0 .. h1) (not staged)
 };
 
 // ---- per-row arithmetic ---------------------------------------------------
@@ -259,6 +259,41 @@ __device__ __forceinline__ void gather_products(V *__restrict__ sv,
     for (int j = 0; j < U; ++j) {
       const uint32_t q = p + j * kConsumers;
       if (q < q1) sv[q] = __dmul_rn(static_cast<double>(sv[q]), xv[j]);
+    }
+  }
+}
+
+// gather_products for a tile with long rows: their nonzeros (the holes,
+// ascending [start, end) pairs) were not staged and are not touched
+template <typename V>
+__device__ __forceinline__ void gather_products_holes(V *__restrict__ sv,
+                                                      const uint32_t *__restrict__ sc,
+                                                      uint32_t q0, uint32_t q1,
+                                                      const V *__restrict__ x, int ct,
+                                                      const uint2 *__restrict__ holes,
+                                                      uint32_t h, uint32_t h1) {
+  constexpr int U = 8;
+  uint2 hb = h < h1 ? holes[h] : make_uint2(0xffffffffu, 0xffffffffu);
+  for (uint32_t p = q0 + ct; p < q1; p += kConsumers * U) {
+    uint32_t c[U];
+    bool ok[U];
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      const uint32_t q = p + j * kConsumers;
+      while (q >= hb.y) {
+        ++h;
+        hb = h < h1 ? holes[h] : make_uint2(0xffffffffu, 0xffffffffu);
+      }
+      ok[j] = q < q1 && q < hb.x;
+      c[j] = ok[j] ? sc[q] : 0u;
+    }
+    double xv[U];
+#pragma unroll
+    for (int j = 0; j < U; ++j) xv[j] = Elem<V>::load_x(x, c[j]);
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      const uint32_t q = p + j * kConsumers;
+      if (ok[j]) sv[q] = __dmul_rn(static_cast<double>(sv[q]), xv[j]);
     }
   }
 }
@@ -377,7 +412,9 @@ __global__ void __launch_bounds__(kThreads, 2)
                        const V *__restrict__ vals, const V *__restrict__ x,
                        V *__restrict__ y, const uint32_t *__restrict__ tile_row,
                        const uint32_t *__restrict__ tile_ptr, uint32_t n_tiles,
-                       uint32_t cap, uint32_t rcap, uint32_t stages, uint32_t long_len) {
+                       uint32_t cap, uint32_t rcap, uint32_t stages, uint32_t long_len,
+                       const uint32_t *__restrict__ tile_long,
+                       const uint2 *__restrict__ holes) {
   extern __shared__ __align__(128) unsigned char smem[];
   const Geometry geo(cap, rcap, stages, sizeof(V));
   uint64_t *full = reinterpret_cast<uint64_t *>(smem);
@@ -404,41 +441,73 @@ __global__ void __launch_bounds__(kThreads, 2)
     // the next tile's bounds (rows and their nonzero offsets, precomputed in
     // the plan) load while this tile waits for its stage: the producer never
     // spends a dependent global round trip between two TMA issues
-    uint32_t nr0 = 0, nr1 = 0, np0 = 0, np1 = 0;
+    uint32_t nr0 = 0, nr1 = 0, np0 = 0, np1 = 0, nh0 = 0, nh1 = 0;
     if (blockIdx.x < n_tiles) {
       nr0 = tile_row[blockIdx.x];
       nr1 = tile_row[blockIdx.x + 1];
       np0 = tile_ptr[blockIdx.x];
       np1 = tile_ptr[blockIdx.x + 1];
+      if (tile_long) {
+        nh0 = tile_long[blockIdx.x];
+        nh1 = tile_long[blockIdx.x + 1];
+      }
     }
     uint32_t i = 0;
     for (uint32_t t = blockIdx.x; t < n_tiles; t += grid, ++i) {
       const uint32_t s = i % stages;
-      const uint32_t r0 = nr0, r1 = nr1, p0 = np0, p1 = np1;
+      const uint32_t r0 = nr0, r1 = nr1, p0 = np0, p1 = np1, h0 = nh0, h1 = nh1;
       if (t + grid < n_tiles) {
         nr0 = tile_row[t + grid];
         nr1 = tile_row[t + grid + 1];
         np0 = tile_ptr[t + grid];
         np1 = tile_ptr[t + grid + 1];
+        if (tile_long) {
+          nh0 = tile_long[t + grid];
+          nh1 = tile_long[t + grid + 1];
+        }
       }
       if (i >= stages) mbar_wait(&empty[s], ((i / stages) + 1) & 1);
       StageMeta &md = meta[s];
       md.r0 = r0;
       md.r1 = r1;
-      if (p1 - p0 <= cap && r1 - r0 <= rcap) {
+      md.h0 = h0;
+      md.h1 = h1;
+      if (p1 - p0 <= cap && r1 - r0 <= rcap && !(r1 - r0 == 1 && h1 > h0)) {
         unsigned char *st = stage0 + s * geo.stage_bytes;
-        const uint32_t va0 = p0 & ~(VPV - 1), va1 = round_up(p1, VPV);
-        const uint32_t ca0 = p0 & ~3u, ca1 = round_up(p1, 4);
+        const uint32_t va0 = p0 & ~(VPV - 1);
+        const uint32_t ca0 = p0 & ~3u;
         const uint32_t ra0 = r0 & ~3u, ra1 = round_up(r1 + 1, 4);
-        const uint32_t vb = (va1 - va0) * static_cast<uint32_t>(sizeof(V));
-        const uint32_t cb = (ca1 - ca0) * 4u, rb = (ra1 - ra0) * 4u;
+        const uint32_t rb = (ra1 - ra0) * 4u;
         md.va0 = va0;
         md.ca0 = ca0;
         md.ra0 = ra0;
         md.mode = kStaged;
-        mbar_arrive_expect_tx(&full[s], vb + cb + rb);
-        if (vb) tma_bulk_load(st + geo.v_off, vals + va0, vb, &full[s], policy);
-        if (cb) tma_bulk_load(st + geo.c_off, col_idx + ca0, cb, &full[s], policy);
+        // the tile's nonzeros minus its long rows (holes longer than 128
+        // entries, so the 16-byte-rounded segments never overlap); one
+        // segment [p0, p1) without long rows
+        uint32_t tx = rb;
+        for (uint32_t pass = 0; pass < 2; ++pass) {
+          uint32_t a = p0;
+          for (uint32_t h = h0; h <= h1; ++h) {
+            const uint2 hb = h < h1 ? holes[h] : make_uint2(p1, p1);
+            if (hb.x > a) {
+              const uint32_t v0 = a & ~(VPV - 1), v1 = round_up(hb.x, VPV);
+              const uint32_t c0 = a & ~3u, c1 = round_up(hb.x, 4);
+              const uint32_t vb = (v1 - v0) * static_cast<uint32_t>(sizeof(V));
+              const uint32_t cb = (c1 - c0) * 4u;
+              if (pass == 0) {
+                tx += vb + cb;
+              } else {
+                tma_bulk_load(st + geo.v_off + (v0 - va0) * sizeof(V), vals + v0, vb,
+                              &full[s], policy);
+                tma_bulk_load(st + geo.c_off + (c0 - ca0) * 4u, col_idx + c0, cb, &full[s],
+                              policy);
+              }
+            }
+            a = hb.y;
+          }
+          if (pass == 0) mbar_arrive_expect_tx(&full[s], tx);
+        }
         tma_bulk_load(st + geo.r_off, row_ptr + ra0, rb, &full[s], policy);
       } else {
         md.mode = kDirect;
@@ -462,7 +531,10 @@ __global__ void __launch_bounds__(kThreads, 2)
       const uint32_t *sr = reinterpret_cast<const uint32_t *>(st + geo.r_off) - md.ra0;
       if constexpr (GF) {
         V *svw = const_cast<V *>(sv);
-        gather_products<V>(svw, sc, sr[md.r0], sr[md.r1], x, ct);
+        if (md.h1 > md.h0)
+          gather_products_holes<V>(svw, sc, sr[md.r0], sr[md.r1], x, ct, holes, md.h0, md.h1);
+        else
+          gather_products<V>(svw, sc, sr[md.r0], sr[md.r1], x, ct);
         asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory");
         compute_rows<V, NX, true>(md.r0, md.r1, sv, sc,
                                   [&](uint32_t r) { return sr[r]; }, x, y, ct, long_len);
@@ -568,6 +640,48 @@ __global__ void long_rows_list_kernel(const uint32_t *__restrict__ row_ptr, int6
       const unsigned long long k = atomicAdd(count, 1ull);
       if (out) out[k] = static_cast<uint32_t>(r);
     }
+}
+
+// keys of the long-row list: row order (the holes) or longest first, ties by
+// row (the long-row kernel's work order: the longest chains start first)
+__global__ void long_keys_kernel(const uint32_t *__restrict__ row_ptr,
+                                 const uint32_t *__restrict__ rows, int64_t n, int by_len,
+                                 uint64_t *__restrict__ keys, uint32_t *__restrict__ vals) {
+  for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < n;
+       k += int64_t(gridDim.x) * blockDim.x) {
+    const uint32_t r = rows[k];
+    const uint32_t len = row_ptr[r + 1] - row_ptr[r];
+    keys[k] = by_len ? (uint64_t(0xffffffffu - len) << 32) | r : uint64_t(r);
+    vals[k] = r;
+  }
+}
+
+__global__ void holes_kernel(const uint32_t *__restrict__ row_ptr,
+                             const uint32_t *__restrict__ rows, int64_t n,
+                             uint2 *__restrict__ holes) {
+  for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < n;
+       k += int64_t(gridDim.x) * blockDim.x) {
+    const uint32_t r = rows[k];
+    holes[k] = make_uint2(row_ptr[r], row_ptr[r + 1]);
+  }
+}
+
+// first hole at or past each tile's first nonzero
+__global__ void tile_long_kernel(const uint32_t *__restrict__ tile_ptr, int64_t n_tiles,
+                                 const uint2 *__restrict__ holes, int64_t n_long,
+                                 uint32_t *__restrict__ tile_long) {
+  const int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (t > n_tiles) return;
+  const uint32_t p = tile_ptr[t];
+  int64_t lo = 0, hi = n_long;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) / 2;
+    if (holes[mid].x >= p)
+      hi = mid;
+    else
+      lo = mid + 1;
+  }
+  tile_long[t] = static_cast<uint32_t>(lo);
 }
 
 template <typename V, int NX>
@@ -680,7 +794,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       StageMeta &md = meta[s];
       md.r0 = r0;
       md.r1 = r1;
-      md.pad0 = q1 - q0;  // slices of the tile
+      md.h0 = q1 - q0;  // slices of the tile
       if (e1 - e0 <= cap && (q1 - q0) * 32 <= rcap) {
         unsigned char *st = stage0 + s * geo.stage_bytes;
         const uint32_t n_e = static_cast<uint32_t>(e1 - e0);   // a multiple of 32
@@ -721,7 +835,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       const uint32_t *sm = reinterpret_cast<const uint32_t *>(st + geo.r_off);
       const uint32_t *si =
           reinterpret_cast<const uint32_t *>(st + geo.s_off) + (s_base[t] - md.va0);
-      for (uint32_t q = warp; q < md.pad0; q += kConsumerWarps) {
+      for (uint32_t q = warp; q < md.h0; q += kConsumerWarps) {
         const uint32_t info = si[q];
         const uint32_t m = sm[q * 32 + lane];
         const double acc = slice_row<8>(sv, sc, (info >> 16) * 32,
@@ -992,7 +1106,9 @@ int launch_stream(const csrk_matrix *m, const V *vals, const V *x, V *y,
   kern<<<static_cast<unsigned>(grid), kThreads, smem, stream>>>(
       m->row_ptr, m->col_idx, vals, x, y, pl.tile_row + t0, pl.tile_ptr + t0,
       static_cast<uint32_t>(count), geo.cap, geo.rcap, geo.stages,
-      m->plan.n_long > 0 ? static_cast<uint32_t>(kLongRow) : 0xffffffffu);
+      m->plan.n_long > 0 ? static_cast<uint32_t>(kLongRow) : 0xffffffffu,
+      m->plan.n_long > 0 ? pl.tile_long + t0 : nullptr,
+      long_holes(pl));
   CSRK_CUDA_TRY(cudaGetLastError());
   return CSRK_OK;
 }
@@ -1144,6 +1260,64 @@ int dispatch_main(const csrk_matrix *m, int variant, int nx, const V *vals,
 
 }  // namespace
 
+namespace {
+
+// Long rows and the cuts.  A row longer than the pitch pulls every cut that
+// falls inside it onto the row after it: those tiles are empty (power-law,
+// 2 M rows, max row 20 k: 17 k of 27 k tiles), and each still cost the
+// producer a stage round trip.  A tile whose nonzeros (long rows included)
+// exceed the stage ran in direct mode, its short rows read from global
+// memory a thread each.  So, with long rows present: empty tiles are dropped,
+// and a tile too big for its stage is cut around its long rows -- the
+// pieces between them fit (their cost is at most the tile's), and a tile of
+// one long row is left to the long-row kernel.  Host work on n_tiles and
+// n_long sized arrays, once per plan.
+int recut_long(csrk_matrix *m, int64_t cap, int64_t *n_tiles_io, bool *split, cudaStream_t s) {
+  const int64_t n_tiles = *n_tiles_io, n_long = m->plan.n_long;
+  std::vector<uint32_t> hr(n_tiles + 1), hp(n_tiles + 1), lr(n_long);
+  CSRK_CUDA_TRY(cudaMemcpyAsync(hr.data(), m->plan.tile_row, hr.size() * sizeof(uint32_t),
+                                cudaMemcpyDeviceToHost, s));
+  CSRK_CUDA_TRY(cudaMemcpyAsync(hp.data(), m->plan.tile_ptr, hp.size() * sizeof(uint32_t),
+                                cudaMemcpyDeviceToHost, s));
+  CSRK_CUDA_TRY(cudaMemcpyAsync(lr.data(), long_rows_asc(m->plan), n_long * sizeof(uint32_t),
+                                cudaMemcpyDeviceToHost, s));
+  CSRK_CUDA_TRY(cudaStreamSynchronize(s));
+  std::vector<uint32_t> out;
+  out.reserve(n_tiles + 1);
+  int64_t k = 0;
+  for (int64_t t = 0; t < n_tiles; ++t) {
+    const uint32_t a = hr[t], b = hr[t + 1];
+    if (a == b) continue;
+    out.push_back(a);
+    if (static_cast<int64_t>(hp[t + 1] - hp[t]) <= cap) continue;
+    uint32_t last = a;
+    while (k < n_long && lr[k] < a) ++k;
+    for (; k < n_long && lr[k] < b; ++k) {
+      const uint32_t r = lr[k];
+      if (r != last) out.push_back(last = r), *split = true;
+      if (r + 1 < b) out.push_back(last = r + 1), *split = true;
+    }
+  }
+  out.push_back(static_cast<uint32_t>(m->n_rows));
+  const int64_t nt = static_cast<int64_t>(out.size()) - 1;
+  if (nt == n_tiles) return CSRK_OK;  // nothing to change
+  cudaFree(m->plan.tile_row);
+  m->plan.tile_row = m->plan.tile_ptr = m->plan.tile_long = nullptr;
+  CSRK_CUDA_TRY(cudaMalloc(&m->plan.tile_row, 3 * (nt + 1) * sizeof(uint32_t)));
+  m->plan.tile_ptr = m->plan.tile_row + (nt + 1);
+  m->plan.tile_long = m->plan.tile_ptr + (nt + 1);
+  CSRK_CUDA_TRY(cudaMemcpyAsync(m->plan.tile_row, out.data(), out.size() * sizeof(uint32_t),
+                                cudaMemcpyHostToDevice, s));
+  tile_ptr_kernel<<<static_cast<unsigned>((nt + 1 + 255) / 256), 256, 0, s>>>(
+      m->row_ptr, m->plan.tile_row, nt, m->plan.tile_ptr);
+  CSRK_CUDA_TRY(cudaGetLastError());
+  CSRK_CUDA_TRY(cudaStreamSynchronize(s));  // `out` is pageable host memory
+  *n_tiles_io = nt;
+  return CSRK_OK;
+}
+
+}  // namespace
+
 int ensure_plan(csrk_matrix *m, int64_t tile_cost, int64_t cap, int64_t stages,
                 cudaStream_t s) {
   if (tile_cost <= 0) tile_cost = kDefaultTileCost;
@@ -1202,11 +1376,41 @@ int ensure_plan(csrk_matrix *m, int64_t tile_cost, int64_t cap, int64_t stages,
     CSRK_CUDA_TRY(cudaMemcpyAsync(&hn, dn, sizeof(hn), cudaMemcpyDeviceToHost, s));
     CSRK_CUDA_TRY(cudaStreamSynchronize(s));
     if (hn > 0) {
-      CSRK_CUDA_TRY(cudaMalloc(&m->plan.long_rows, hn * sizeof(uint32_t)));
+      const int64_t n = static_cast<int64_t>(hn);
+      CSRK_CUDA_TRY(cudaMalloc(&m->plan.long_rows, (4 * n + 1) * sizeof(uint32_t)));
+      m->plan.n_long = n;
       CSRK_CUDA_TRY(cudaMemsetAsync(dn, 0, sizeof(hn), s));
       long_rows_list_kernel<<<148 * 8, 256, 0, s>>>(m->row_ptr, m->n_rows,
                                                      static_cast<uint32_t>(kLongRow),
                                                      m->plan.long_rows, dn);
+      CSRK_CUDA_TRY(cudaGetLastError());
+      // holes in row order, then the work order
+      uint64_t *keys = nullptr, *tk = nullptr;
+      uint32_t *vals = nullptr, *tv = nullptr;
+      keep_async_pool();
+      CSRK_CUDA_TRY(cudaMallocAsync(&keys, 2 * n * sizeof(uint64_t), s));
+      CSRK_CUDA_TRY(cudaMallocAsync(&vals, 2 * n * sizeof(uint32_t), s));
+      tk = keys + n;
+      tv = vals + n;
+      const unsigned gb = static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 148 * 8));
+      int rc = CSRK_OK;
+      for (int by_len = 0; by_len < 2 && rc == CSRK_OK; ++by_len) {
+        long_keys_kernel<<<gb, 256, 0, s>>>(m->row_ptr, m->plan.long_rows, n, by_len, keys,
+                                            vals);
+        rc = radix_sort_pairs(keys, vals, tk, tv, n, 0, by_len ? 64 : 32, s);
+        if (rc == CSRK_OK && !by_len) {
+          holes_kernel<<<gb, 256, 0, s>>>(m->row_ptr, vals, n,
+                                          const_cast<uint2 *>(long_holes(m->plan)));
+          CSRK_CUDA_TRY(cudaMemcpyAsync(const_cast<uint32_t *>(long_rows_asc(m->plan)), vals,
+                                        n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+        }
+      }
+      if (rc == CSRK_OK)
+        CSRK_CUDA_TRY(cudaMemcpyAsync(m->plan.long_rows, vals, n * sizeof(uint32_t),
+                                      cudaMemcpyDeviceToDevice, s));
+      cudaFreeAsync(keys, s);
+      cudaFreeAsync(vals, s);
+      CSRK_TRY(rc);
       CSRK_CUDA_TRY(cudaGetLastError());
       CSRK_CUDA_TRY(cudaStreamSynchronize(s));
     }
@@ -1251,7 +1455,7 @@ int ensure_plan(csrk_matrix *m, int64_t tile_cost, int64_t cap, int64_t stages,
   // (cap - tile_cost) covers the row that crosses a boundary.
   const int64_t pitch = cut_k == 1 ? tile_cost : tile_cost - max_group;
   const int64_t total_cost = m->nnz + m->n_rows;
-  const int64_t n_tiles = (total_cost + pitch - 1) / pitch;
+  int64_t n_tiles = (total_cost + pitch - 1) / pitch;
   if (n_tiles > 0x7fffffffLL) {
     set_error("too many tiles (%lld)", static_cast<long long>(n_tiles));
     return CSRK_EINVAL;
@@ -1259,17 +1463,28 @@ int ensure_plan(csrk_matrix *m, int64_t tile_cost, int64_t cap, int64_t stages,
   if (m->plan.tile_row) {
     CSRK_CUDA_TRY(cudaFree(m->plan.tile_row));
     m->plan.tile_row = nullptr;
-    m->plan.tile_ptr = nullptr;
+    m->plan.tile_ptr = m->plan.tile_long = nullptr;
   }
-  // one allocation: tile_row[n_tiles + 1] then tile_ptr[n_tiles + 1]
-  CSRK_CUDA_TRY(cudaMalloc(&m->plan.tile_row, 2 * (n_tiles + 1) * sizeof(uint32_t)));
+  // one allocation: tile_row, tile_ptr, tile_long (n_tiles + 1 each)
+  CSRK_CUDA_TRY(cudaMalloc(&m->plan.tile_row, 3 * (n_tiles + 1) * sizeof(uint32_t)));
   m->plan.tile_ptr = m->plan.tile_row + (n_tiles + 1);
-  const int64_t blocks = (n_tiles + 1 + 255) / 256;
+  m->plan.tile_long = m->plan.tile_ptr + (n_tiles + 1);
+  int64_t blocks = (n_tiles + 1 + 255) / 256;
   tile_bounds_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(
       m->row_ptr, m->sr_ptr, m->ssr_ptr, cut_k, n_cuts, m->n_rows, pitch,
       n_tiles, m->plan.tile_row);
   tile_ptr_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(
       m->row_ptr, m->plan.tile_row, n_tiles, m->plan.tile_ptr);
+  CSRK_CUDA_TRY(cudaGetLastError());
+  bool split = false;
+  if (m->plan.n_long > 0) {
+    CSRK_TRY(recut_long(m, cap, &n_tiles, &split, s));
+    blocks = (n_tiles + 1 + 255) / 256;
+  }
+  if (m->plan.n_long > 0)
+    tile_long_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(
+        m->plan.tile_ptr, n_tiles, long_holes(m->plan),
+        m->plan.n_long, m->plan.tile_long);
   CSRK_CUDA_TRY(cudaGetLastError());
   m->pipe.plan_tiles = -1;  // host-pipeline cuts index the old tiles
   ++m->plan.gen;            // and the sliced copy belongs to the old plan
@@ -1278,7 +1493,7 @@ int ensure_plan(csrk_matrix *m, int64_t tile_cost, int64_t cap, int64_t stages,
   m->plan.rcap = rcap;
   m->plan.stages = stages;
   m->plan.n_tiles = n_tiles;
-  m->plan.group_aligned = cut_k != 1 || m->k == 1;
+  m->plan.group_aligned = (cut_k != 1 || m->k == 1) && !split;
   return CSRK_OK;
 }
 
@@ -1427,7 +1642,7 @@ int launch_spmv(const csrk_matrix *m, int value_type, int variant, int nx,
       return launch_sliced(m, static_cast<const double *>(x), static_cast<double *>(y),
                            stream, t0, t1);
     const int g = m->plan.gather_first;
-    if (g == 1 || (g == kGatherAuto && auto_gather(variant, m->plan.mean_row)))
+    if (g == 1 || (g == kGatherAuto && auto_gather(variant, m->plan.mean_row, m->plan.row_var)))
       return dispatch_nx<double, true>(m, variant, nx, m->vals64,
                                        static_cast<const double *>(x),
                                        static_cast<double *>(y), stream, t0, t1);

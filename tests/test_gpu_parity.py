@@ -301,13 +301,46 @@ def test_plan_geometry_checks():
 
 
 def _mixed_rows_matrix(rng, n):
-    """Rows of 0..60 nonzeros (mean > 16, variance >> 10) plus a few long
-    rows: exercises every schedule's inline, gather-first and direct paths."""
+    """Rows of 0..60 nonzeros (mean > 16, variance >> 10) plus long rows of
+    129..1500 nonzeros (holes inside staged tiles) and 3000: exercises every
+    schedule's inline, gather-first, direct and long-row paths."""
     lens = rng.integers(0, 61, n)
+    lens[rng.choice(n, 60, replace=False)] = rng.integers(129, 1500, 60)
     lens[rng.choice(n, 5, replace=False)] = 3000
     rows = np.repeat(np.arange(n), lens)
     cols = rng.integers(0, n, len(rows))
     return ck.csr_from_arrays(n, n, rows, cols, rng.uniform(-1.0, 1.0, len(rows)))
+
+
+@pytest.mark.parametrize("tile_cost,stages", [(0, 0), (256, 3), (1153, 2), (4096, 2)])
+def test_long_row_tile_cuts(tile_cost, stages):
+    """With long rows present the plan has no empty tiles, and a tile whose
+    nonzeros exceed its stage is one (long) row -- the cuts around long rows
+    (spmv.cu recut_long) -- while both orders keep the oracle's bits."""
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(tile_cost + stages)
+    n = 40000
+    lens = rng.integers(0, 20, n)
+    lens[rng.choice(n, 300, replace=False)] = rng.integers(129, 6000, 300)
+    rows = np.repeat(np.arange(n), lens)
+    a = ck.csr_from_arrays(n, n, rows, rng.integers(0, n, len(rows)),
+                           rng.uniform(-1.0, 1.0, len(rows)))
+    m = ck.pack_csrk(a, ck.Permutation.identity(n), [[1] * n, [n]])
+    dev = m.device()
+    dev.set_plan(tile_cost, 0, stages)
+    plan = dev.plan()
+    tr = dev.tile_rows().astype(np.int64)
+    assert tr[0] == 0 and tr[-1] == n and len(tr) == plan["n_tiles"] + 1
+    assert np.all(np.diff(tr) > 0)
+    rp = a.row_ptr.astype(np.int64)
+    big = rp[tr[1:]] - rp[tr[:-1]] > plan["cap"]
+    assert np.all(np.diff(tr)[big] == 1)
+    x = rng.uniform(-1.0, 1.0, n)
+    np.testing.assert_array_equal(ck.spmv_csr3(m, x), O.spmv_serial(a.row_ptr, a.col_idx,
+                                                                    a.vals, x))
+    for nx in (4, 8):
+        np.testing.assert_array_equal(ck.spmv_gpu35(m, x, ck.BlockDims(nx, 1, 1)),
+                                      O.spmv_strided(a.row_ptr, a.col_idx, a.vals, x, nx))
 
 
 @pytest.mark.parametrize("gather,ctas", [(0, 0), (1, 0), (2, 0), (0, 1), (1, 2), (2, 3),

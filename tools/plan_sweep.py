@@ -48,7 +48,12 @@ def main():
     configs = sys.argv[1:] or ["C2", "C3", "C5"]
     out = []
     for cfg in configs:
-        a, m, xp, params, _ = bench.build_matrix(cfg, lambda s: print(s, file=sys.stderr))
+        if cfg.startswith("PL"):  # power-law rows, 2 M rows, max row length PL<len>
+            from powerlaw_probe import build_powerlaw
+            a, m, _, params = build_powerlaw(2_000_000, int(cfg[2:]))
+            xp = np.random.default_rng(0).uniform(-1.0, 1.0, a.n_rows)
+        else:
+            a, m, xp, params, _ = bench.build_matrix(cfg, lambda s: print(s, file=sys.stderr))
         n, nnz = a.n_rows, a.nnz
         variant = "strided" if params.kernel_variant.value == "cuda35" else "serial"
         dev = m.device()

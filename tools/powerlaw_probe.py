@@ -38,22 +38,32 @@ def med(fn, reps=20):
     return float(np.median(ts))
 
 
-n = int(sys.argv[1]) if len(sys.argv) > 1 else 2_000_000
-for max_len in [int(v) for v in (sys.argv[2:] or ["1000", "20000"])]:
+def build_powerlaw(n, max_len):
+    """(csr, csrk matrix, stats, tuned params) of one power-law case."""
     r, c, v = powerlaw_triplets(n, max_len)
     a = ck.csr_from_arrays(n, n, r, c, v)
     st = ck.compute_stats(a)
     p = ck.tune_gpu(st, ck.b200_profile())
     res = ck.band_k(a, 3, [p.srs, p.ssrs])
-    m = ck.pack_csrk(a, res.perm, res.level_group_sizes)
-    x = torch.rand(n, dtype=torch.float64, device="cuda")
-    y = torch.empty_like(x)
-    byts = spmv_bytes(n, n, a.nnz, 8)
-    print(f"max_len {max_len}: nnz {a.nnz} rd {st.rdensity:.2f} var {st.variance:.1f} "
-          f"max_row {st.max_row_nnz} tuned {p.kernel_variant.value} {p.block_dims}", flush=True)
-    for variant, nx in [("serial", 0), ("strided", 4), ("strided", 8), ("strided", 16),
-                        ("strided", 32)]:
-        dims = ck.BlockDims(max(nx, 1), 1, 1)
-        ms = med(lambda: ck.spmv_device(m, x, y, dims=dims, variant=variant))
-        print(f"  {variant:8s} nx {nx:2d}: {ms * 1e3:8.1f} us  {byts / ms / 1e6:6.0f} GB/s",
-              flush=True)
+    return a, ck.pack_csrk(a, res.perm, res.level_group_sizes), st, p
+
+
+def main():
+    n = int(sys.argv[1]) if len(sys.argv) > 1 else 2_000_000
+    for max_len in [int(v) for v in (sys.argv[2:] or ["1000", "20000"])]:
+        a, m, st, p = build_powerlaw(n, max_len)
+        x = torch.rand(n, dtype=torch.float64, device="cuda")
+        y = torch.empty_like(x)
+        byts = spmv_bytes(n, n, a.nnz, 8)
+        print(f"max_len {max_len}: nnz {a.nnz} rd {st.rdensity:.2f} var {st.variance:.1f} "
+              f"max_row {st.max_row_nnz} tuned {p.kernel_variant.value} {p.block_dims}", flush=True)
+        for variant, nx in [("serial", 0), ("strided", 4), ("strided", 8), ("strided", 16),
+                            ("strided", 32)]:
+            dims = ck.BlockDims(max(nx, 1), 1, 1)
+            ms = med(lambda: ck.spmv_device(m, x, y, dims=dims, variant=variant))
+            print(f"  {variant:8s} nx {nx:2d}: {ms * 1e3:8.1f} us  {byts / ms / 1e6:6.0f} GB/s",
+                  flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -4,8 +4,10 @@ import json
 import sys
 
 t = collections.defaultdict(dict)
-for line in open(sys.argv[1]):
-    r = json.loads(line)
+text = open(sys.argv[1]).read()
+recs = json.loads(text) if text.lstrip().startswith("[") else \
+    [json.loads(line) for line in text.splitlines() if line.startswith("{")]
+for r in recs:
     key = (r["config"], r["dtype"], r["variant"] + ("%d" % r["nx"] if r.get("nx") else ""),
            "G%d" % r["gather"], "C%d" % r.get("ctas", 0), "L%d" % r.get("layout", 2))
     t[key]["T%dS%d" % (r["tile_cost"], r["stages"])] = (r["gbs"], r["bitwise_equal"])
