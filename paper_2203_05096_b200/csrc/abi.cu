@@ -66,6 +66,9 @@ static void release(csrk_matrix *m) {
   if (m->pipe.h2d) cudaStreamDestroy(m->pipe.h2d);
   if (m->pipe.comp) cudaStreamDestroy(m->pipe.comp);
   if (m->pipe.d2h) cudaStreamDestroy(m->pipe.d2h);
+  if (m->long_fork) cudaEventDestroy(m->long_fork);
+  if (m->long_join) cudaEventDestroy(m->long_join);
+  if (m->long_stream) cudaStreamDestroy(m->long_stream);
   if (m->ev0) cudaEventDestroy(m->ev0);
   if (m->ev1) cudaEventDestroy(m->ev1);
   if (m->stream) cudaStreamDestroy(m->stream);

@@ -146,6 +146,9 @@ struct csrk_matrix {
   } pipe;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // the long-row kernel's side stream (forked from / joined to the caller's)
+  cudaStream_t long_stream = nullptr;
+  cudaEvent_t long_fork = nullptr, long_join = nullptr;
   void *x_stage = nullptr, *y_stage = nullptr;
   size_t x_stage_bytes = 0, y_stage_bytes = 0;
 };

@@ -684,6 +684,16 @@ __global__ void tile_long_kernel(const uint32_t *__restrict__ tile_ptr, int64_t 
   tile_long[t] = static_cast<uint32_t>(lo);
 }
 
+// blocks of 8 warps per SM beside the streaming kernel's CTAs
+// (CSRK_LONG_BLOCKS overrides, for sweeps)
+int64_t long_blocks_per_sm() {
+  static const int64_t v = [] {
+    const char *e = std::getenv("CSRK_LONG_BLOCKS");
+    return e ? std::max<int64_t>(1, std::atoll(e)) : int64_t(8);
+  }();
+  return v;
+}
+
 template <typename V, int NX>
 int launch_long_rows(const csrk_matrix *m, const V *vals, const V *x, V *y, cudaStream_t stream,
                      int64_t t0, int64_t t1) {
@@ -691,7 +701,8 @@ int launch_long_rows(const csrk_matrix *m, const V *vals, const V *x, V *y, cuda
   if (t1 < 0 || t1 > pl.n_tiles) t1 = pl.n_tiles;
   if (t0 < 0) t0 = 0;
   int64_t blocks = (pl.n_long + 7) / 8;
-  if (blocks > int64_t(m->sm_count) * 8) blocks = int64_t(m->sm_count) * 8;
+  if (blocks > int64_t(m->sm_count) * long_blocks_per_sm())
+    blocks = int64_t(m->sm_count) * long_blocks_per_sm();
   if (blocks < 1) return CSRK_OK;
   long_rows_kernel<V, NX><<<static_cast<unsigned>(blocks), 256, 0, stream>>>(
       m->row_ptr, m->col_idx, vals, x, y, pl.long_rows, pl.n_long, pl.tile_row + t0,
@@ -1206,12 +1217,41 @@ int dispatch_long(const csrk_matrix *m, int variant, int nx, const V *vals, cons
   }
 }
 
+// In the strided order with nx <= 8 the long-row kernel runs beside the
+// streaming kernel: forked onto a side stream after the streaming kernel is
+// queued (the persistent CTAs are resident first and the long-row warps fill
+// the SMs' remaining slots) and joined back before the caller's stream
+// continues.  Power-law, 2 M rows, max row 20 k: nx = 4 514 -> 337 us,
+// nx = 8 549 -> 353 us.  The serial order (one chain per warp: it wants
+// every warp slot) and nx >= 16 lose beside the streaming kernel (602 ->
+// 721, 596 -> 702 us) and queue behind it (profiles/r01_powerlaw_probe.txt).
+// CSRK_LONG_SERIAL=1 queues every order behind it.
 template <typename V, bool GF>
 int dispatch_nx(const csrk_matrix *m, int variant, int nx, const V *vals,
                 const V *x, V *y, cudaStream_t s, int64_t t0, int64_t t1) {
-  const int rc = dispatch_main<V, GF>(m, variant, nx, vals, x, y, s, t0, t1);
-  if (rc != CSRK_OK) return rc;
-  return dispatch_long<V>(m, variant, nx, vals, x, y, s, t0, t1);
+  static const bool serial_long = [] {
+    const char *e = std::getenv("CSRK_LONG_SERIAL");
+    return e && e[0] == '1';
+  }();
+  if (m->plan.n_long == 0 || serial_long || variant == CSRK_SERIAL || nx > 8) {
+    const int rc = dispatch_main<V, GF>(m, variant, nx, vals, x, y, s, t0, t1);
+    if (rc != CSRK_OK) return rc;
+    return dispatch_long<V>(m, variant, nx, vals, x, y, s, t0, t1);
+  }
+  csrk_matrix *mm = const_cast<csrk_matrix *>(m);  // lazily created side stream
+  if (!mm->long_stream) {
+    CSRK_CUDA_TRY(cudaStreamCreateWithFlags(&mm->long_stream, cudaStreamNonBlocking));
+    CSRK_CUDA_TRY(cudaEventCreateWithFlags(&mm->long_fork, cudaEventDisableTiming));
+    CSRK_CUDA_TRY(cudaEventCreateWithFlags(&mm->long_join, cudaEventDisableTiming));
+  }
+  CSRK_CUDA_TRY(cudaEventRecord(mm->long_fork, s));
+  CSRK_CUDA_TRY(cudaStreamWaitEvent(mm->long_stream, mm->long_fork, 0));
+  int rc = dispatch_main<V, GF>(m, variant, nx, vals, x, y, s, t0, t1);
+  if (rc == CSRK_OK)
+    rc = dispatch_long<V>(m, variant, nx, vals, x, y, mm->long_stream, t0, t1);
+  CSRK_CUDA_TRY(cudaEventRecord(mm->long_join, mm->long_stream));
+  CSRK_CUDA_TRY(cudaStreamWaitEvent(s, mm->long_join, 0));
+  return rc;
 }
 
 template <typename V, bool GF>
