@@ -29,12 +29,19 @@ CTAS_LIST = tuple(int(t) for t in os.environ.get('SWEEP_CTAS', '3').split(','))
 LAYOUTS = tuple(int(t) for t in os.environ.get('SWEEP_LAYOUT', '0').split(','))
 
 
+FLUSH = None
+if os.environ.get("SWEEP_FLUSH") == "1":  # write 256 MB (> L2) before every timed launch
+    FLUSH = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
+
+
 def median_ms(fn, reps=20):
     for _ in range(3):
         fn()
     torch.cuda.synchronize()
     ts = []
     for _ in range(reps):
+        if FLUSH is not None:
+            FLUSH.fill_(1.0)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
         fn()
