@@ -100,3 +100,55 @@ def test_device_stencil_uniform_groups():
     # the C4 analytic check: Laplacian row sums are 7 - row length
     y1 = dev.spmv_host(np.ones(dev.n_rows))
     np.testing.assert_array_equal(y1, 7.0 - np.diff(rp.astype(np.int64)))
+
+
+def _arrowhead(n=6000, hubs=(0, 1500, 4000), step=3):
+    """SPD, diagonally dominant, with dense hub rows / columns: rows longer
+    than 128 nonzeros go to the long-row kernel (and, strided nx <= 8, its
+    side stream) inside the CG / power loops."""
+    rows, cols, vals = [np.arange(n)], [np.arange(n)], [np.full(n, 10.0)]
+    for h in hubs:
+        c = np.arange(0, n, step)
+        c = c[c != h]
+        rows += [np.full(len(c), h), c]
+        cols += [c, np.full(len(c), h)]
+        vals += [np.full(len(c), 1e-3), np.full(len(c), 1e-3)]
+    a = ck.csr_from_arrays(n, n, np.concatenate(rows), np.concatenate(cols),
+                           np.concatenate(vals))
+    res = ck.band_k(a, 3, [4, 8])
+    return a, res, ck.pack_csrk(a, res.perm, res.level_group_sizes)
+
+
+@pytest.mark.parametrize("variant,nx", [("serial", 0), ("strided", 4), ("strided", 16)])
+def test_long_rows_in_cg_graph_and_power(variant, nx):
+    a, res, m = _arrowhead()
+    rp, ci, va = m.base.row_ptr, m.base.col_idx, m.base.vals
+    assert np.diff(rp).max() > 128
+    n = a.n_rows
+    dims = ck.BlockDims(max(nx, 1), 1, 1)
+    b = torch.from_numpy(np.random.default_rng(4).uniform(-1, 1, n)).cuda()
+    x_eager, info = cg.cg(m, b, iters=30, dims=dims, variant=variant)
+    x = torch.zeros_like(b)
+    scratch = tuple(torch.empty_like(b) for _ in range(3))
+
+    def loop(stream):
+        x.zero_()
+        cg.cg(m, b, x, iters=30, dims=dims, variant=variant, stream=stream,
+              scratch=scratch, sync=False)
+
+    g = cg.GraphedLoop(loop)
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(x, x_eager)
+    resid = b.cpu().numpy() - O.spmv_serial(rp, ci, va, x.cpu().numpy())
+    assert np.linalg.norm(resid) < 1e-8 * np.linalg.norm(b.cpu().numpy())
+    # power iterations: bit for bit the oracle's order
+    x0 = np.random.default_rng(5).uniform(0.5, 1.5, n)
+    xp = torch.from_numpy(x0.copy()).cuda()
+    cg.power_iterations(m, xp, iters=4, dims=dims, variant=variant)
+    v = x0.copy()
+    for _ in range(4):
+        yv = (O.spmv_serial(rp, ci, va, v) if variant == "serial"
+              else O.spmv_strided(rp, ci, va, v, nx))
+        v = yv * (1.0 / np.abs(yv).max())
+    np.testing.assert_array_equal(xp.cpu().numpy(), v)
