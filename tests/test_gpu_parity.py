@@ -408,6 +408,31 @@ def test_pipeline_shapes_bitwise(monkeypatch, shape, d2h, xcut):
         np.testing.assert_array_equal(y_pin, want)
 
 
+@pytest.mark.parametrize("shape", ["u3", "r12"])
+def test_pipeline_with_long_rows(monkeypatch, shape):
+    """The pinned host pipeline's chunked tile-range launches with long rows
+    (each chunk's long rows, the side stream for nx = 4): the oracle's bits."""
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(11)
+    n = 1_200_000  # > 1 M rows: the pinned pipeline engages
+    lens = rng.integers(0, 12, n)
+    lens[rng.choice(n, 500, replace=False)] = rng.integers(129, 3000, 500)
+    rows = np.repeat(np.arange(n), lens)
+    a = ck.csr_from_arrays(n, n, rows, np.minimum(n - 1, rows + rng.integers(0, 5000, len(rows))),
+                           rng.uniform(-1.0, 1.0, len(rows)))
+    m = ck.pack_csrk(a, ck.Permutation.identity(n), [[1] * n, [n]])
+    monkeypatch.setenv("CSRK_PIPE_SHAPE", shape)
+    x_pin = torch.empty(n, dtype=torch.float64, pin_memory=True).numpy()
+    y_pin = torch.empty(n, dtype=torch.float64, pin_memory=True).numpy()
+    x_pin[:] = rng.uniform(-1.0, 1.0, n)
+    y_pin[:] = np.nan
+    ck.spmv_csr3(m, x_pin, out=y_pin)
+    np.testing.assert_array_equal(y_pin, O.spmv_serial(a.row_ptr, a.col_idx, a.vals, x_pin))
+    y_pin[:] = np.nan
+    ck.spmv_gpu35(m, x_pin, ck.BlockDims(4, 1, 1), out=y_pin)
+    np.testing.assert_array_equal(y_pin, O.spmv_strided(a.row_ptr, a.col_idx, a.vals, x_pin, 4))
+
+
 def test_auto_plan_follows_the_order():
     """An automatic plan re-tiles for strided launches whose rows would leave
     a pass mostly empty (27-nonzero rows, nx = 4), keeps 2048 for the serial
