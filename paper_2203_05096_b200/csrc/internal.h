@@ -38,8 +38,15 @@ inline int auto_ctas(double row_var, int value_bytes) {
 // or their lengths spread wider than their mean (a thread per row then waits
 // on the longest row of its warp; power-law rows, mean 9.8 / variance 238:
 // 1.67 -> 2.36 TB/s), inline otherwise (C5: mean 10 / variance 30 loses 2 %).
-inline bool auto_gather(int variant, double mean_row, double row_var) {
-  return variant == CSRK_SERIAL && (mean_row > 16.0 || row_var > mean_row * mean_row);
+// In the strided order gather first when rows are shorter than the
+// sub-warp (most lanes would idle through the inline batches): C2 nx = 8
+// 2.30 -> 2.86 TB/s, C5 nx = 16 1.18 -> 1.36, C1 nx = 32 0.44 -> 0.65; rows
+// at least a sub-warp long keep inline gathers (C3 nx = 8 5.33 vs 4.07).
+inline bool auto_gather(int variant, int nx, double mean_row, double row_var) {
+  if (variant == CSRK_SERIAL) return mean_row > 16.0 || row_var > mean_row * mean_row;
+  int p = 1;
+  while (p < nx) p <<= 1;
+  return mean_row < p;
 }
 
 // Tile cost for a launch in the STRIDED order: the 256 consumer threads

@@ -1682,7 +1682,7 @@ int launch_spmv(const csrk_matrix *m, int value_type, int variant, int nx,
       return launch_sliced(m, static_cast<const double *>(x), static_cast<double *>(y),
                            stream, t0, t1);
     const int g = m->plan.gather_first;
-    if (g == 1 || (g == kGatherAuto && auto_gather(variant, m->plan.mean_row, m->plan.row_var)))
+    if (g == 1 || (g == kGatherAuto && auto_gather(variant, nx, m->plan.mean_row, m->plan.row_var)))
       return dispatch_nx<double, true>(m, variant, nx, m->vals64,
                                        static_cast<const double *>(x),
                                        static_cast<double *>(y), stream, t0, t1);
