@@ -1238,19 +1238,14 @@ int dispatch_nx(const csrk_matrix *m, int variant, int nx, const V *vals,
     if (rc != CSRK_OK) return rc;
     return dispatch_long<V>(m, variant, nx, vals, x, y, s, t0, t1);
   }
-  csrk_matrix *mm = const_cast<csrk_matrix *>(m);  // lazily created side stream
-  if (!mm->long_stream) {
-    CSRK_CUDA_TRY(cudaStreamCreateWithFlags(&mm->long_stream, cudaStreamNonBlocking));
-    CSRK_CUDA_TRY(cudaEventCreateWithFlags(&mm->long_fork, cudaEventDisableTiming));
-    CSRK_CUDA_TRY(cudaEventCreateWithFlags(&mm->long_join, cudaEventDisableTiming));
-  }
-  CSRK_CUDA_TRY(cudaEventRecord(mm->long_fork, s));
-  CSRK_CUDA_TRY(cudaStreamWaitEvent(mm->long_stream, mm->long_fork, 0));
+  // (side stream and events created with the long-row list, ensure_plan)
+  CSRK_CUDA_TRY(cudaEventRecord(m->long_fork, s));
+  CSRK_CUDA_TRY(cudaStreamWaitEvent(m->long_stream, m->long_fork, 0));
   int rc = dispatch_main<V, GF>(m, variant, nx, vals, x, y, s, t0, t1);
   if (rc == CSRK_OK)
-    rc = dispatch_long<V>(m, variant, nx, vals, x, y, mm->long_stream, t0, t1);
-  CSRK_CUDA_TRY(cudaEventRecord(mm->long_join, mm->long_stream));
-  CSRK_CUDA_TRY(cudaStreamWaitEvent(s, mm->long_join, 0));
+    rc = dispatch_long<V>(m, variant, nx, vals, x, y, m->long_stream, t0, t1);
+  CSRK_CUDA_TRY(cudaEventRecord(m->long_join, m->long_stream));
+  CSRK_CUDA_TRY(cudaStreamWaitEvent(s, m->long_join, 0));
   return rc;
 }
 
@@ -1419,6 +1414,11 @@ int ensure_plan(csrk_matrix *m, int64_t tile_cost, int64_t cap, int64_t stages,
       const int64_t n = static_cast<int64_t>(hn);
       CSRK_CUDA_TRY(cudaMalloc(&m->plan.long_rows, (4 * n + 1) * sizeof(uint32_t)));
       m->plan.n_long = n;
+      if (!m->long_stream) {  // the long-row kernel's side stream (dispatch_nx)
+        CSRK_CUDA_TRY(cudaStreamCreateWithFlags(&m->long_stream, cudaStreamNonBlocking));
+        CSRK_CUDA_TRY(cudaEventCreateWithFlags(&m->long_fork, cudaEventDisableTiming));
+        CSRK_CUDA_TRY(cudaEventCreateWithFlags(&m->long_join, cudaEventDisableTiming));
+      }
       CSRK_CUDA_TRY(cudaMemsetAsync(dn, 0, sizeof(hn), s));
       long_rows_list_kernel<<<148 * 8, 256, 0, s>>>(m->row_ptr, m->n_rows,
                                                      static_cast<uint32_t>(kLongRow),
