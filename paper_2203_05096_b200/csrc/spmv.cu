@@ -1307,35 +1307,78 @@ namespace {
 // pieces between them fit (their cost is at most the tile's), and a tile of
 // one long row is left to the long-row kernel.  Host work on n_tiles and
 // n_long sized arrays, once per plan.
-int recut_long(csrk_matrix *m, int64_t cap, int64_t *n_tiles_io, bool *split, cudaStream_t s) {
+int recut_long(csrk_matrix *m, int64_t tile_cost, int64_t cap, int64_t rcap,
+               int64_t *n_tiles_io, bool *split, cudaStream_t s) {
   const int64_t n_tiles = *n_tiles_io, n_long = m->plan.n_long;
   std::vector<uint32_t> hr(n_tiles + 1), hp(n_tiles + 1), lr(n_long);
+  std::vector<uint2> holes(n_long);
   CSRK_CUDA_TRY(cudaMemcpyAsync(hr.data(), m->plan.tile_row, hr.size() * sizeof(uint32_t),
                                 cudaMemcpyDeviceToHost, s));
   CSRK_CUDA_TRY(cudaMemcpyAsync(hp.data(), m->plan.tile_ptr, hp.size() * sizeof(uint32_t),
                                 cudaMemcpyDeviceToHost, s));
   CSRK_CUDA_TRY(cudaMemcpyAsync(lr.data(), long_rows_asc(m->plan), n_long * sizeof(uint32_t),
                                 cudaMemcpyDeviceToHost, s));
+  CSRK_CUDA_TRY(cudaMemcpyAsync(holes.data(), long_holes(m->plan), n_long * sizeof(uint2),
+                                cudaMemcpyDeviceToHost, s));
   CSRK_CUDA_TRY(cudaStreamSynchronize(s));
-  std::vector<uint32_t> out;
-  out.reserve(n_tiles + 1);
+  // 1. pieces: the base tiles minus empty ones, those too big for a stage
+  //    cut around their long rows; pc = first nonzero of each cut
+  std::vector<uint32_t> cut, pc;
+  cut.reserve(n_tiles + 1);
+  pc.reserve(n_tiles + 1);
   int64_t k = 0;
   for (int64_t t = 0; t < n_tiles; ++t) {
     const uint32_t a = hr[t], b = hr[t + 1];
     if (a == b) continue;
-    out.push_back(a);
+    cut.push_back(a);
+    pc.push_back(hp[t]);
     if (static_cast<int64_t>(hp[t + 1] - hp[t]) <= cap) continue;
     uint32_t last = a;
     while (k < n_long && lr[k] < a) ++k;
     for (; k < n_long && lr[k] < b; ++k) {
       const uint32_t r = lr[k];
-      if (r != last) out.push_back(last = r), *split = true;
-      if (r + 1 < b) out.push_back(last = r + 1), *split = true;
+      if (r != last) cut.push_back(last = r), pc.push_back(holes[k].x);
+      if (r + 1 < b) cut.push_back(last = r + 1), pc.push_back(holes[k].y);
     }
   }
+  cut.push_back(static_cast<uint32_t>(m->n_rows));
+  pc.push_back(hp[n_tiles]);
+  // 2. greedy merge of consecutive pieces while the tile still fits a stage
+  //    (nonzeros incl. long rows <= cap, rows <= rcap) and its staged cost
+  //    (nonzeros excl. long rows + rows) stays within the tile cost: the
+  //    pieces between long rows join up again instead of each costing the
+  //    producer a stage round trip (power-law 20 k: 35 k -> fewer tiles)
+  std::vector<uint32_t> out;
+  out.reserve(cut.size());
+  const size_t np = cut.size() - 1;
+  size_t h = 0;  // holes cursor (row order)
+  auto long_nnz = [&](uint32_t a, uint32_t b) {  // nonzeros of long rows in [a, b)
+    int64_t sum = 0;
+    while (h < static_cast<size_t>(n_long) && lr[h] < a) ++h;
+    for (size_t q = h; q < static_cast<size_t>(n_long) && lr[q] < b; ++q)
+      sum += holes[q].y - holes[q].x;
+    return sum;
+  };
+  size_t st = 0;
+  int64_t lsum = long_nnz(cut[0], cut[1]);
+  out.push_back(cut[0]);
+  for (size_t j = 1; j < np; ++j) {
+    const int64_t lj = long_nnz(cut[j], cut[j + 1]);
+    const int64_t span = static_cast<int64_t>(pc[j + 1]) - pc[st];
+    const int64_t rows = static_cast<int64_t>(cut[j + 1]) - cut[st];
+    if (span <= cap && rows <= rcap && span - lsum - lj + rows <= tile_cost) {
+      lsum += lj;  // piece j joins the current tile
+      continue;
+    }
+    out.push_back(cut[j]);
+    st = j;
+    lsum = lj;
+  }
   out.push_back(static_cast<uint32_t>(m->n_rows));
+  if (out.size() == hr.size() && std::equal(out.begin(), out.end(), hr.begin()))
+    return CSRK_OK;  // nothing to change
+  *split = true;
   const int64_t nt = static_cast<int64_t>(out.size()) - 1;
-  if (nt == n_tiles) return CSRK_OK;  // nothing to change
   cudaFree(m->plan.tile_row);
   m->plan.tile_row = m->plan.tile_ptr = m->plan.tile_long = nullptr;
   CSRK_CUDA_TRY(cudaMalloc(&m->plan.tile_row, 3 * (nt + 1) * sizeof(uint32_t)));
@@ -1518,7 +1561,7 @@ int ensure_plan(csrk_matrix *m, int64_t tile_cost, int64_t cap, int64_t stages,
   CSRK_CUDA_TRY(cudaGetLastError());
   bool split = false;
   if (m->plan.n_long > 0) {
-    CSRK_TRY(recut_long(m, cap, &n_tiles, &split, s));
+    CSRK_TRY(recut_long(m, tile_cost, cap, rcap, &n_tiles, &split, s));
     blocks = (n_tiles + 1 + 255) / 256;
   }
   if (m->plan.n_long > 0)
