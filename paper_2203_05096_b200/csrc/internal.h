@@ -88,6 +88,7 @@ struct TilePlan {
   int gather_first = kGatherAuto;
   int ctas_per_sm = 0;
   double mean_row = 0.0, row_var = 0.0;
+  double mean_short = 0.0;  // mean length of the rows the streaming kernel sums (<= kLongRow)
   bool row_stats = false;
   bool auto_tile = true;  // tile cost follows the launch's order (auto_tile_cost)
   int layout = 0;         // serial f64 layout: 0 CSR, 1 sliced tiles

@@ -585,7 +585,9 @@ __global__ void __launch_bounds__(256)
     // gathers issued before the current one is walked, so their latency
     // hides behind the ordered adds); the chains then walk the chunk from
     // shared memory: lane 0 alone in the serial order, lanes 0..nx-1 their
-    // strided subsequences (position mod nx) in the strided order
+    // strided subsequences (position mod nx) in the strided order.  (A
+    // register walk by shuffles measured slower: 64-bit shuffles are two
+    // instructions each -- serial 517 -> 788 us on the 20 k power-law case.)
     constexpr int K = kChunk / 32;
     constexpr int L = NX == 0 ? 1 : NX;
     double v[K], xv[K];
@@ -615,9 +617,23 @@ __global__ void __launch_bounds__(256)
       __syncwarp();
       if (lane < L) {
         const uint32_t cnt = e - p0 < uint32_t(kChunk) ? e - p0 : uint32_t(kChunk);
-        const uint32_t off = (p0 - s) % L;  // position of chunk entry 0 modulo nx
-        for (uint32_t j = (lane + L - off) % L; j < cnt; j += L)
-          acc = __dadd_rn(acc, buf[w][j]);
+        if (kChunk % L == 0 && cnt == uint32_t(kChunk)) {
+          // full chunk (entry 0 at position 0 mod nx): the loads of a group
+          // are independent of the chain, so they issue ahead of its adds
+          constexpr int kPer = kChunk / L, kGroup = kPer < 16 ? kPer : 16;
+#pragma unroll
+          for (int g = 0; g < kPer; g += kGroup) {
+            double t[kGroup];
+#pragma unroll
+            for (int q = 0; q < kGroup; ++q) t[q] = buf[w][(g + q) * L + lane];
+#pragma unroll
+            for (int q = 0; q < kGroup; ++q) acc = __dadd_rn(acc, t[q]);
+          }
+        } else {
+          const uint32_t off = (p0 - s) % L;  // position of chunk entry 0 modulo nx
+          for (uint32_t j = (lane + L - off) % L; j < cnt; j += L)
+            acc = __dadd_rn(acc, buf[w][j]);
+        }
       }
       __syncwarp();
     }
@@ -664,6 +680,16 @@ __global__ void holes_kernel(const uint32_t *__restrict__ row_ptr,
     const uint32_t r = rows[k];
     holes[k] = make_uint2(row_ptr[r], row_ptr[r + 1]);
   }
+}
+
+__global__ void hole_sum_kernel(const uint2 *__restrict__ holes, int64_t n,
+                                unsigned long long *__restrict__ sum) {
+  unsigned long long acc = 0;
+  for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < n;
+       k += int64_t(gridDim.x) * blockDim.x)
+    acc += holes[k].y - holes[k].x;
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(sum, acc);
 }
 
 // first hole at or past each tile's first nonzero
@@ -1058,6 +1084,22 @@ __global__ void chunk_max_col_kernel(const uint32_t *__restrict__ row_ptr,
   }
 }
 
+// Whether the long-row kernel runs beside the streaming kernel (see
+// dispatch_nx): strided order with nx <= 8, unless CSRK_LONG_SERIAL=1.
+bool long_beside(const csrk_matrix *m, int variant, int nx) {
+  static const bool serial_long = [] {
+    const char *e = std::getenv("CSRK_LONG_SERIAL");
+    return e && e[0] == '1';
+  }();
+  return m->plan.n_long > 0 && !serial_long && variant == CSRK_STRIDED && nx <= 8;
+}
+// shared memory the streaming kernel's carveout leaves for long-row blocks
+// beside it (their 8 KB buffers; without the room they could not co-reside
+// and took SMs the persistent CTAs then waited for -- 2.1 -> 1.1 TB/s at
+// some tile sizes on the power-law case)
+constexpr int kBesideBlocks = 2;
+constexpr size_t kLongBlockSmem = 8 * 128 * sizeof(double) + 1024;
+
 template <typename V, int NX, bool GF, int LB = 4>
 int launch_stream(const csrk_matrix *m, const V *vals, const V *x, V *y,
                   cudaStream_t stream, int64_t t0, int64_t t1) {
@@ -1069,15 +1111,18 @@ int launch_stream(const csrk_matrix *m, const V *vals, const V *x, V *y,
   // attribute + occupancy queries cost host time per launch; cache them per
   // instantiation and shared-memory size (the chunked host pipeline launches
   // the kernel many times per SpMV)
-  static thread_local size_t cached_smem = 0;
+  static thread_local size_t cached_smem = 0, cached_extra = 0;
   static thread_local int cached_per_sm = 0, cached_ctas = 0;
   static thread_local int cached_device = -1;
   int cur_dev = 0;
   CSRK_CUDA_TRY(cudaGetDevice(&cur_dev));
   const int ctas = pl.ctas_per_sm > 0 ? pl.ctas_per_sm
                                       : auto_ctas(pl.row_var, static_cast<int>(sizeof(V)));
+  const size_t extra =
+      long_beside(m, NX == 0 ? CSRK_SERIAL : CSRK_STRIDED, NX) ? kBesideBlocks * kLongBlockSmem : 0;
   int per_sm = 0;
-  if (cached_smem == smem && cached_device == cur_dev && cached_ctas == ctas) {
+  if (cached_smem == smem && cached_device == cur_dev && cached_ctas == ctas &&
+      cached_extra == extra) {
     per_sm = cached_per_sm;
   } else {
     CSRK_CUDA_TRY(cudaFuncSetAttribute(
@@ -1091,7 +1136,7 @@ int launch_stream(const csrk_matrix *m, const V *vals, const V *x, V *y,
     CSRK_CUDA_TRY(cudaDeviceGetAttribute(&smem_sm,
                                          cudaDevAttrMaxSharedMemoryPerMultiprocessor,
                                          cur_dev));
-    const double need = static_cast<double>(ctas) * (smem + 1024);
+    const double need = static_cast<double>(ctas) * (smem + 1024) + static_cast<double>(extra);
     int pct = static_cast<int>(need * 100.0 / smem_sm + 0.999);
     pct = pct < 1 ? 1 : (pct > 100 ? 100 : pct);
     CSRK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
@@ -1099,6 +1144,7 @@ int launch_stream(const csrk_matrix *m, const V *vals, const V *x, V *y,
     CSRK_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads,
                                                                 smem));
     if (per_sm > ctas) per_sm = ctas;
+    cached_extra = extra;
     cached_smem = smem;
     cached_per_sm = per_sm;
     cached_ctas = ctas;
@@ -1229,11 +1275,7 @@ int dispatch_long(const csrk_matrix *m, int variant, int nx, const V *vals, cons
 template <typename V, bool GF>
 int dispatch_nx(const csrk_matrix *m, int variant, int nx, const V *vals,
                 const V *x, V *y, cudaStream_t s, int64_t t0, int64_t t1) {
-  static const bool serial_long = [] {
-    const char *e = std::getenv("CSRK_LONG_SERIAL");
-    return e && e[0] == '1';
-  }();
-  if (m->plan.n_long == 0 || serial_long || variant == CSRK_SERIAL || nx > 8) {
+  if (!long_beside(m, variant, nx)) {
     const int rc = dispatch_main<V, GF>(m, variant, nx, vals, x, y, s, t0, t1);
     if (rc != CSRK_OK) return rc;
     return dispatch_long<V>(m, variant, nx, vals, x, y, s, t0, t1);
@@ -1258,7 +1300,7 @@ int dispatch_main(const csrk_matrix *m, int variant, int nx, const V *vals,
   // 5.81 -> 6.06 TB/s), 4 for short rows (C2 / C5 lose with 8: registers)
   int p = 1;
   while (p < nx) p <<= 1;
-  const bool wide = m->plan.mean_row / p >= 5.0;
+  const bool wide = m->plan.mean_short / p >= 5.0;
   switch (nx) {
 #define CSRK_NX_CASE(N)                                          \
   case N:                                                        \
@@ -1442,6 +1484,7 @@ int ensure_plan(csrk_matrix *m, int64_t tile_cost, int64_t cap, int64_t stages,
     cudaFreeAsync(d, s);
     const double mean = static_cast<double>(m->nnz) / static_cast<double>(m->n_rows);
     m->plan.mean_row = mean;
+    m->plan.mean_short = mean;
     m->plan.row_var = static_cast<double>(h) / static_cast<double>(m->n_rows) - mean * mean;
     m->plan.row_stats = true;
     // rows longer than kLongRow: listed once for the long-row kernel
@@ -1491,11 +1534,20 @@ int ensure_plan(csrk_matrix *m, int64_t tile_cost, int64_t cap, int64_t stages,
       if (rc == CSRK_OK)
         CSRK_CUDA_TRY(cudaMemcpyAsync(m->plan.long_rows, vals, n * sizeof(uint32_t),
                                       cudaMemcpyDeviceToDevice, s));
+      unsigned long long hl = 0;
+      if (rc == CSRK_OK) {  // the short rows' mean length (strided schedule choices)
+        CSRK_CUDA_TRY(cudaMemsetAsync(dn, 0, sizeof(hn), s));
+        hole_sum_kernel<<<gb, 256, 0, s>>>(long_holes(m->plan), n, dn);
+        CSRK_CUDA_TRY(cudaMemcpyAsync(&hl, dn, sizeof(hl), cudaMemcpyDeviceToHost, s));
+      }
       cudaFreeAsync(keys, s);
       cudaFreeAsync(vals, s);
       CSRK_TRY(rc);
       CSRK_CUDA_TRY(cudaGetLastError());
       CSRK_CUDA_TRY(cudaStreamSynchronize(s));
+      if (m->n_rows > n)
+        m->plan.mean_short = static_cast<double>(m->nnz - static_cast<int64_t>(hl)) /
+                             static_cast<double>(m->n_rows - n);
     }
     cudaFreeAsync(dn, s);
     m->plan.n_long = static_cast<int64_t>(hn);
@@ -1684,7 +1736,7 @@ int prepare_plan(const csrk_matrix *cm, int value_type, int variant, int nx) {
     if (sliced_wanted(m, value_type, variant)) CSRK_TRY(ensure_sliced(m, m->stream));
     return CSRK_OK;
   }
-  const int64_t tc = auto_tile_cost(m->plan.mean_row, variant, nx);
+  const int64_t tc = auto_tile_cost(m->plan.mean_short, variant, nx);
   if (tc != m->plan.tile_cost) {
     const bool keep = m->plan.auto_tile;
     CSRK_TRY(ensure_plan(m, tc, 0, m->plan.stages, m->stream));
