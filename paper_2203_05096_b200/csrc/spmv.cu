@@ -1085,13 +1085,17 @@ __global__ void chunk_max_col_kernel(const uint32_t *__restrict__ row_ptr,
 }
 
 // Whether the long-row kernel runs beside the streaming kernel (see
-// dispatch_nx): strided order with nx <= 8, unless CSRK_LONG_SERIAL=1.
+// dispatch_nx): always with long rows, unless CSRK_LONG_SERIAL=1.
 bool long_beside(const csrk_matrix *m, int variant, int nx) {
   static const bool serial_long = [] {
     const char *e = std::getenv("CSRK_LONG_SERIAL");
     return e && e[0] == '1';
   }();
-  return m->plan.n_long > 0 && !serial_long && variant == CSRK_STRIDED && nx <= 8;
+  static const int max_nx = [] {  // sweep knob: widest strided order beside
+    const char *e = std::getenv("CSRK_LONG_BESIDE_NX");
+    return e ? std::atoi(e) : 32;
+  }();
+  return m->plan.n_long > 0 && !serial_long && (variant == CSRK_SERIAL || nx <= max_nx);
 }
 // shared memory the streaming kernel's carveout leaves for long-row blocks
 // beside it (their 8 KB buffers; without the room they could not co-reside
@@ -1263,15 +1267,13 @@ int dispatch_long(const csrk_matrix *m, int variant, int nx, const V *vals, cons
   }
 }
 
-// In the strided order with nx <= 8 the long-row kernel runs beside the
-// streaming kernel: forked onto a side stream after the streaming kernel is
-// queued (the persistent CTAs are resident first and the long-row warps fill
-// the SMs' remaining slots) and joined back before the caller's stream
-// continues.  Power-law, 2 M rows, max row 20 k: nx = 4 514 -> 337 us,
-// nx = 8 549 -> 353 us.  The serial order (one chain per warp: it wants
-// every warp slot) and nx >= 16 lose beside the streaming kernel (602 ->
-// 721, 596 -> 702 us) and queue behind it (profiles/r01_powerlaw_probe.txt).
-// CSRK_LONG_SERIAL=1 queues every order behind it.
+// The long-row kernel runs beside the streaming kernel: forked onto a side
+// stream after the streaming kernel is queued (the persistent CTAs are
+// resident first; their carveout leaves room for two long-row blocks per SM,
+// launch_stream) and joined back before the caller's stream continues.
+// Power-law, 2 M rows, max row 20 k, queued -> beside: serial 503 -> 397 us,
+// nx = 4 447 -> 335, nx = 32 654 -> 560 (profiles/r01_powerlaw_probe.txt).
+// CSRK_LONG_SERIAL=1 queues it behind the streaming kernel instead.
 template <typename V, bool GF>
 int dispatch_nx(const csrk_matrix *m, int variant, int nx, const V *vals,
                 const V *x, V *y, cudaStream_t s, int64_t t0, int64_t t1) {
