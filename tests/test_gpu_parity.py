@@ -341,6 +341,14 @@ def test_long_row_tile_cuts(tile_cost, stages):
     for nx in (4, 8):
         np.testing.assert_array_equal(ck.spmv_gpu35(m, x, ck.BlockDims(nx, 1, 1)),
                                       O.spmv_strided(a.row_ptr, a.col_idx, a.vals, x, nx))
+    # fp32 (16-byte segments of 4 values around the holes), odd lane counts
+    want = O.spmv_serial(a.row_ptr, a.col_idx, a.vals, x)
+    scale = O.abs_row_dot(a.row_ptr, a.col_idx, a.vals, x)
+    xd = torch.from_numpy(x).cuda().float()
+    for variant, nx in (("serial", 1), ("strided", 3), ("strided", 12)):
+        y32 = ck.spmv_device(m, xd, dims=ck.BlockDims(nx, 1, 1), variant=variant)
+        torch.cuda.synchronize()
+        assert np.all(np.abs(y32.cpu().double().numpy() - want) <= 1e-5 * scale)  # empty rows: 0
 
 
 @pytest.mark.parametrize("gather,ctas", [(0, 0), (1, 0), (2, 0), (0, 1), (1, 2), (2, 3),
