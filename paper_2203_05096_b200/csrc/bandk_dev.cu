@@ -54,11 +54,17 @@ inline unsigned nbk(int64_t n, int threads = 256) {
 constexpr int64_t kInf64 = 0x7fffffffffffffffLL;
 
 template <typename T>
-struct DV {
+struct DV {  // stream-ordered scratch from the kept pool (keep_async_pool)
   T *p = nullptr;
-  ~DV() { cudaFree(p); }
-  cudaError_t alloc(int64_t n) { return cudaMalloc(&p, (n > 0 ? n : 1) * sizeof(T)); }
-  void release() { p = nullptr; }
+  cudaStream_t st = nullptr;
+  ~DV() {
+    if (p) cudaFreeAsync(p, st);
+  }
+  cudaError_t alloc(int64_t n, cudaStream_t s) {
+    keep_async_pool();
+    st = s;
+    return cudaMallocAsync(&p, (n > 0 ? n : 1) * sizeof(T), s);
+  }
 };
 
 __global__ void inv64_kernel(const int64_t *__restrict__ fwd, int64_t n,
@@ -236,10 +242,10 @@ int make_level(const int32_t *f2c, int64_t n_fine, int64_t n_coarse, Level &lv,
   DV<uint64_t> keys, tk;
   DV<uint32_t> tv;
   DV<int64_t> cnt;
-  CSRK_CUDA_TRY(keys.alloc(n_fine));
-  CSRK_CUDA_TRY(tk.alloc(n_fine));
-  CSRK_CUDA_TRY(tv.alloc(n_fine));
-  CSRK_CUDA_TRY(cnt.alloc(n_coarse));
+  CSRK_CUDA_TRY(keys.alloc(n_fine, s));
+  CSRK_CUDA_TRY(tk.alloc(n_fine, s));
+  CSRK_CUDA_TRY(tv.alloc(n_fine, s));
+  CSRK_CUDA_TRY(cnt.alloc(n_coarse, s));
   CSRK_CUDA_TRY(cudaMalloc(&lv.mem, (n_fine > 0 ? n_fine : 1) * sizeof(uint32_t)));
   CSRK_CUDA_TRY(cudaMalloc(&lv.mptr, (n_coarse + 1) * sizeof(int64_t)));
   member_keys_kernel<<<nbk(n_fine), 256, 0, s>>>(f2c, n_fine, keys.p, lv.mem);
@@ -262,25 +268,25 @@ int expand_level_dev(const csrk_dgraph *g, const Level &lv, const int64_t *seq_c
   DV<int32_t> cand, queue;
   DV<int8_t> state;
   DV<int> flag;
-  CSRK_CUDA_TRY(bsize.alloc(nb));
-  CSRK_CUDA_TRY(off.alloc(nb + 1));
-  CSRK_CUDA_TRY(blk.alloc(n));
-  CSRK_CUDA_TRY(pos_a.alloc(n));
-  CSRK_CUDA_TRY(pos_b.alloc(n));
-  CSRK_CUDA_TRY(outside.alloc(n));
-  CSRK_CUDA_TRY(anchor.alloc(n));
-  CSRK_CUDA_TRY(krank.alloc(n));
-  CSRK_CUDA_TRY(tv.alloc(n));
-  CSRK_CUDA_TRY(keys.alloc(n));
-  CSRK_CUDA_TRY(tk.alloc(n));
-  CSRK_CUDA_TRY(cand.alloc(n));
-  CSRK_CUDA_TRY(queue.alloc(n));
-  CSRK_CUDA_TRY(state.alloc(n));
-  CSRK_CUDA_TRY(flag.alloc(1));
+  CSRK_CUDA_TRY(bsize.alloc(nb, s));
+  CSRK_CUDA_TRY(off.alloc(nb + 1, s));
+  CSRK_CUDA_TRY(blk.alloc(n, s));
+  CSRK_CUDA_TRY(pos_a.alloc(n, s));
+  CSRK_CUDA_TRY(pos_b.alloc(n, s));
+  CSRK_CUDA_TRY(outside.alloc(n, s));
+  CSRK_CUDA_TRY(anchor.alloc(n, s));
+  CSRK_CUDA_TRY(krank.alloc(n, s));
+  CSRK_CUDA_TRY(tv.alloc(n, s));
+  CSRK_CUDA_TRY(keys.alloc(n, s));
+  CSRK_CUDA_TRY(tk.alloc(n, s));
+  CSRK_CUDA_TRY(cand.alloc(n, s));
+  CSRK_CUDA_TRY(queue.alloc(n, s));
+  CSRK_CUDA_TRY(state.alloc(n, s));
+  CSRK_CUDA_TRY(flag.alloc(1, s));
   CSRK_CUDA_TRY(cudaMemsetAsync(state.p, 0, n, s));
   // key ranks (degree, weight, index)
   DV<uint32_t> order;
-  CSRK_CUDA_TRY(order.alloc(n));
+  CSRK_CUDA_TRY(order.alloc(n, s));
   key_rank_keys_kernel<<<nbk(n), 256, 0, s>>>(g->ptr, g->nw, n, keys.p, order.p);
   CSRK_TRY(radix_sort_pairs(keys.p, order.p, tk.p, tv.p, n, 0, 64, s));
   scatter_rank_kernel<<<nbk(n), 256, 0, s>>>(order.p, n, krank.p);

@@ -144,10 +144,17 @@ __global__ void inv_kernel(const int64_t *__restrict__ fwd, int64_t n,
 }
 
 template <typename T>
-struct DB {
+struct DB {  // stream-ordered scratch from the kept pool (keep_async_pool)
   T *p = nullptr;
-  ~DB() { cudaFree(p); }
-  cudaError_t alloc(int64_t n) { return cudaMalloc(&p, (n > 0 ? n : 1) * sizeof(T)); }
+  cudaStream_t st = nullptr;
+  ~DB() {
+    if (p) cudaFreeAsync(p, st);
+  }
+  cudaError_t alloc(int64_t n, cudaStream_t s) {
+    keep_async_pool();
+    st = s;
+    return cudaMallocAsync(&p, (n > 0 ? n : 1) * sizeof(T), s);
+  }
 };
 
 }  // namespace
@@ -167,15 +174,15 @@ int graph_match_dev(const csrk_dgraph *g, int32_t *match, int *iters, cudaStream
   DB<uint32_t> vals, tvals, rank;
   DB<int32_t> choice;
   DB<int> flag;
-  CSRK_CUDA_TRY(keys.alloc(n));
-  CSRK_CUDA_TRY(tkeys.alloc(n));
-  CSRK_CUDA_TRY(vals.alloc(n));
-  CSRK_CUDA_TRY(tvals.alloc(n));
-  CSRK_CUDA_TRY(rank.alloc(n));
-  CSRK_CUDA_TRY(ta.alloc(n));
-  CSRK_CUDA_TRY(tb.alloc(n));
-  CSRK_CUDA_TRY(choice.alloc(n));
-  CSRK_CUDA_TRY(flag.alloc(1));
+  CSRK_CUDA_TRY(keys.alloc(n, s));
+  CSRK_CUDA_TRY(tkeys.alloc(n, s));
+  CSRK_CUDA_TRY(vals.alloc(n, s));
+  CSRK_CUDA_TRY(tvals.alloc(n, s));
+  CSRK_CUDA_TRY(rank.alloc(n, s));
+  CSRK_CUDA_TRY(ta.alloc(n, s));
+  CSRK_CUDA_TRY(tb.alloc(n, s));
+  CSRK_CUDA_TRY(choice.alloc(n, s));
+  CSRK_CUDA_TRY(flag.alloc(1, s));
   deg_key_kernel<<<nb(n), 256, 0, s>>>(g->ptr, n, keys.p, vals.p);
   CSRK_TRY(radix_sort_pairs(keys.p, vals.p, tkeys.p, tvals.p, n, 0, 32, s));
   vrank_kernel<<<nb(n), 256, 0, s>>>(vals.p, n, rank.p);
@@ -228,7 +235,7 @@ int graph_coarsen_dev(const csrk_dgraph *g, double target, int32_t *f2c, csrk_dg
     if (n == 0 || !(static_cast<double>(total) / static_cast<double>(n) < target)) break;
     if (!first) {
       DB<int64_t> band, inv;
-      if (band.alloc(n) != cudaSuccess || inv.alloc(n) != cudaSuccess) return CSRK_ENOMEM;
+      if (band.alloc(n, s) != cudaSuccess || inv.alloc(n, s) != cudaSuccess) return CSRK_ENOMEM;
       rc = graph_wbo_dev(cur_g(), band.p, s);
       if (rc != CSRK_OK) break;
       inv_kernel<<<nb(n), 256, 0, s>>>(band.p, n, inv.p);
@@ -243,8 +250,8 @@ int graph_coarsen_dev(const csrk_dgraph *g, double target, int32_t *f2c, csrk_dg
     first = false;
     DB<int32_t> match, new_id;
     DB<int64_t> flag, pos;
-    if (match.alloc(n) != cudaSuccess || new_id.alloc(n) != cudaSuccess ||
-        flag.alloc(n) != cudaSuccess || pos.alloc(n + 1) != cudaSuccess)
+    if (match.alloc(n, s) != cudaSuccess || new_id.alloc(n, s) != cudaSuccess ||
+        flag.alloc(n, s) != cudaSuccess || pos.alloc(n + 1, s) != cudaSuccess)
       return CSRK_ENOMEM;
     int sweeps = 0;
     rc = graph_match_dev(cur_g(), match.p, &sweeps, s);

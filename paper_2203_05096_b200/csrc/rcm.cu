@@ -381,10 +381,17 @@ __global__ void cm_init_kernel(const uint32_t *__restrict__ roots, int64_t n_com
 }
 
 template <typename T>
-struct DBuf {
+struct DBuf {  // stream-ordered scratch from the kept pool (keep_async_pool)
   T *p = nullptr;
-  ~DBuf() { cudaFree(p); }
-  cudaError_t alloc(int64_t n) { return cudaMalloc(&p, (n > 0 ? n : 1) * sizeof(T)); }
+  cudaStream_t st = nullptr;
+  ~DBuf() {
+    if (p) cudaFreeAsync(p, st);
+  }
+  cudaError_t alloc(int64_t n, cudaStream_t s) {
+    keep_async_pool();
+    st = s;
+    return cudaMallocAsync(&p, (n > 0 ? n : 1) * sizeof(T), s);
+  }
 };
 
 
@@ -411,26 +418,26 @@ int graph_wbo_dev(const csrk_dgraph *g, int64_t *fwd_dev, cudaStream_t s) {
   DBuf<int8_t> active;
   DBuf<int> counter;
   DBuf<int64_t> coff, csize, csize_off;
-  CSRK_CUDA_TRY(keys.alloc(n));
-  CSRK_CUDA_TRY(tkeys.alloc(n));
-  CSRK_CUDA_TRY(vals.alloc(n));
-  CSRK_CUDA_TRY(tvals.alloc(n));
-  CSRK_CUDA_TRY(krank.alloc(n));
-  CSRK_CUDA_TRY(by_key.alloc(n));
-  CSRK_CUDA_TRY(claim.alloc(n));
-  CSRK_CUDA_TRY(lastmin.alloc(n));
-  CSRK_CUDA_TRY(minrank.alloc(n));
-  CSRK_CUDA_TRY(label.alloc(n));
-  CSRK_CUDA_TRY(size.alloc(n));
-  CSRK_CUDA_TRY(depth.alloc(n));
-  CSRK_CUDA_TRY(frontier.alloc(n));
-  CSRK_CUDA_TRY(next.alloc(n));
-  CSRK_CUDA_TRY(pos.alloc(n));
-  CSRK_CUDA_TRY(ecc.alloc(n));
-  CSRK_CUDA_TRY(crank.alloc(n));
-  CSRK_CUDA_TRY(qlen.alloc(n));
-  CSRK_CUDA_TRY(counter.alloc(4));
-  CSRK_CUDA_TRY(coff.alloc(n + 1));
+  CSRK_CUDA_TRY(keys.alloc(n, s));
+  CSRK_CUDA_TRY(tkeys.alloc(n, s));
+  CSRK_CUDA_TRY(vals.alloc(n, s));
+  CSRK_CUDA_TRY(tvals.alloc(n, s));
+  CSRK_CUDA_TRY(krank.alloc(n, s));
+  CSRK_CUDA_TRY(by_key.alloc(n, s));
+  CSRK_CUDA_TRY(claim.alloc(n, s));
+  CSRK_CUDA_TRY(lastmin.alloc(n, s));
+  CSRK_CUDA_TRY(minrank.alloc(n, s));
+  CSRK_CUDA_TRY(label.alloc(n, s));
+  CSRK_CUDA_TRY(size.alloc(n, s));
+  CSRK_CUDA_TRY(depth.alloc(n, s));
+  CSRK_CUDA_TRY(frontier.alloc(n, s));
+  CSRK_CUDA_TRY(next.alloc(n, s));
+  CSRK_CUDA_TRY(pos.alloc(n, s));
+  CSRK_CUDA_TRY(ecc.alloc(n, s));
+  CSRK_CUDA_TRY(crank.alloc(n, s));
+  CSRK_CUDA_TRY(qlen.alloc(n, s));
+  CSRK_CUDA_TRY(counter.alloc(4, s));
+  CSRK_CUDA_TRY(coff.alloc(n + 1, s));
   phase("alloc");
 
   // 1. key ranks: stable sort of (degree, weight) keeps index order on ties;
@@ -464,12 +471,12 @@ int graph_wbo_dev(const csrk_dgraph *g, int64_t *fwd_dev, cudaStream_t s) {
   // roots in component order (-size, root); vals keeps them
   CSRK_TRY(radix_sort_pairs(keys.p, vals.p, tkeys.p, tvals.p, n_comp, 0, 64, s));
   const uint32_t *roots = vals.p;
-  CSRK_CUDA_TRY(csize.alloc(n_comp));
-  CSRK_CUDA_TRY(csize_off.alloc(n_comp + 1));
-  CSRK_CUDA_TRY(start.alloc(n_comp));
-  CSRK_CUDA_TRY(best_node.alloc(n_comp));
-  CSRK_CUDA_TRY(best_ecc.alloc(n_comp));
-  CSRK_CUDA_TRY(active.alloc(n_comp));
+  CSRK_CUDA_TRY(csize.alloc(n_comp, s));
+  CSRK_CUDA_TRY(csize_off.alloc(n_comp + 1, s));
+  CSRK_CUDA_TRY(start.alloc(n_comp, s));
+  CSRK_CUDA_TRY(best_node.alloc(n_comp, s));
+  CSRK_CUDA_TRY(best_ecc.alloc(n_comp, s));
+  CSRK_CUDA_TRY(active.alloc(n_comp, s));
   comp_sizes_kernel<<<nblocks(n_comp), 256, 0, s>>>(roots, n_comp, size.p, csize.p);
   CSRK_TRY(exclusive_scan_i64(csize.p, n_comp, csize_off.p, s));
   comp_layout_kernel<<<nblocks(n_comp), 256, 0, s>>>(roots, n_comp, size.p, csize_off.p,
@@ -482,7 +489,7 @@ int graph_wbo_dev(const csrk_dgraph *g, int64_t *fwd_dev, cudaStream_t s) {
                                                  best_node.p, best_ecc.p, active.p);
   constexpr int kBfsBatch = 8;  // even: the frontier ends each batch in `frontier`
   DBuf<int> lsize;
-  CSRK_CUDA_TRY(lsize.alloc(kBfsBatch + 1));
+  CSRK_CUDA_TRY(lsize.alloc(kBfsBatch + 1, s));
   const unsigned bfs_grid = nblocks(n) < 148 * 8 ? nblocks(n) : 148 * 8;
   int64_t n_active = n_comp;
   while (n_active > 0) {
@@ -534,10 +541,10 @@ int graph_wbo_dev(const csrk_dgraph *g, int64_t *fwd_dev, cudaStream_t s) {
                                                  frontier.p);
   DBuf<int64_t> cnt, off, lvl_start;
   DBuf<int32_t> big;
-  CSRK_CUDA_TRY(cnt.alloc(n));
-  CSRK_CUDA_TRY(off.alloc(n + 1));
-  CSRK_CUDA_TRY(lvl_start.alloc(n));
-  CSRK_CUDA_TRY(big.alloc(n));
+  CSRK_CUDA_TRY(cnt.alloc(n, s));
+  CSRK_CUDA_TRY(off.alloc(n + 1, s));
+  CSRK_CUDA_TRY(lvl_start.alloc(n, s));
+  CSRK_CUDA_TRY(big.alloc(n, s));
   int64_t fsize = n_comp;
   for (;;) {
     cm_claim_kernel<<<nblocks(fsize), 256, 0, s>>>(g->ptr, g->idx, frontier.p, fsize, pos.p,
