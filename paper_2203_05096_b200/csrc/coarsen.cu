@@ -53,14 +53,18 @@ __global__ void vrank_kernel(const uint32_t *__restrict__ order, int64_t n,
 }
 
 // one Jacobi sweep: choices from `taken_prev`, new claims into `taken_next`
+// (all free on entry); `reset` -- the array the next sweep claims into, read
+// by nobody in this one -- is set free on the way
 __global__ void match_sweep_kernel(const int64_t *__restrict__ ptr,
                                    const int32_t *__restrict__ idx,
                                    const int32_t *__restrict__ ew,
                                    const uint32_t *__restrict__ rank, int64_t n,
                                    const uint64_t *__restrict__ taken_prev,
                                    uint64_t *__restrict__ taken_next,
+                                   uint64_t *__restrict__ reset,
                                    int32_t *__restrict__ choice) {
   GS(v, n) {
+    reset[v] = kFree;
     const uint32_t rv = rank[v];
     int32_t best = -1;
     if ((taken_prev[v] >> 32) >= rv) {  // v is free at its turn
@@ -87,13 +91,11 @@ __global__ void match_sweep_kernel(const int64_t *__restrict__ ptr,
   }
 }
 
-// compare the previous and new "taken by" arrays, then reset the previous
-// one to free so it can receive the next sweep's claims
-__global__ void diff_reset_kernel(uint64_t *__restrict__ a, const uint64_t *__restrict__ b,
-                                  int64_t n, int *__restrict__ changed) {
+// did the sweep change the "taken by" array?
+__global__ void diff_kernel(const uint64_t *__restrict__ a, const uint64_t *__restrict__ b,
+                            int64_t n, int *__restrict__ changed) {
   GS(i, n) {
     if (a[i] != b[i]) *changed = 1;
-    a[i] = kFree;
   }
 }
 
@@ -170,7 +172,7 @@ void graph_free_dev(csrk_dgraph *g);
 int graph_match_dev(const csrk_dgraph *g, int32_t *match, int *iters, cudaStream_t s) {
   const int64_t n = g->n;
   if (n == 0) return CSRK_OK;
-  DB<uint64_t> keys, tkeys, ta, tb;
+  DB<uint64_t> keys, tkeys, ta, tb, tc;
   DB<uint32_t> vals, tvals, rank;
   DB<int32_t> choice;
   DB<int> flag;
@@ -181,6 +183,7 @@ int graph_match_dev(const csrk_dgraph *g, int32_t *match, int *iters, cudaStream
   CSRK_CUDA_TRY(rank.alloc(n, s));
   CSRK_CUDA_TRY(ta.alloc(n, s));
   CSRK_CUDA_TRY(tb.alloc(n, s));
+  CSRK_CUDA_TRY(tc.alloc(n, s));
   CSRK_CUDA_TRY(choice.alloc(n, s));
   CSRK_CUDA_TRY(flag.alloc(1, s));
   deg_key_kernel<<<nb(n), 256, 0, s>>>(g->ptr, n, keys.p, vals.p);
@@ -188,17 +191,25 @@ int graph_match_dev(const csrk_dgraph *g, int32_t *match, int *iters, cudaStream
   vrank_kernel<<<nb(n), 256, 0, s>>>(vals.p, n, rank.p);
   fill_u64_kernel<<<nb(n), 256, 0, s>>>(ta.p, n, kFree);
   fill_u64_kernel<<<nb(n), 256, 0, s>>>(tb.p, n, kFree);
+  fill_u64_kernel<<<nb(n), 256, 0, s>>>(tc.p, n, kFree);
   // sweeps run in batches of 8 with one host check per batch: sweeps past
-  // the fixed point change nothing, and only the batch's last sweep decides
+  // the fixed point change nothing, and only the batch's last sweep decides.
+  // Three "taken by" arrays rotate (read, claimed into, reset for the next
+  // sweep), so no pass of its own resets one between sweeps.
   constexpr int kBatch = 8;
   int it = 0;
   for (;;) {
     for (int j = 0; j < kBatch; ++j, ++it) {
       match_sweep_kernel<<<nb(n), 256, 0, s>>>(g->ptr, g->idx, g->ew, rank.p, n, ta.p, tb.p,
-                                               choice.p);
-      if (j == kBatch - 1) CSRK_CUDA_TRY(cudaMemsetAsync(flag.p, 0, sizeof(int), s));
-      diff_reset_kernel<<<nb(n), 256, 0, s>>>(ta.p, tb.p, n, flag.p);
-      std::swap(ta.p, tb.p);
+                                               tc.p, choice.p);
+      if (j == kBatch - 1) {
+        CSRK_CUDA_TRY(cudaMemsetAsync(flag.p, 0, sizeof(int), s));
+        diff_kernel<<<nb(n), 256, 0, s>>>(ta.p, tb.p, n, flag.p);
+      }
+      uint64_t *t = ta.p;  // (read, claim, reset) <- (claim, reset, read)
+      ta.p = tb.p;
+      tb.p = tc.p;
+      tc.p = t;
     }
     int h = 0;
     CSRK_CUDA_TRY(cudaMemcpyAsync(&h, flag.p, sizeof(int), cudaMemcpyDeviceToHost, s));
