@@ -590,28 +590,33 @@ __global__ void __launch_bounds__(256)
     // instructions each -- serial 517 -> 788 us on the 20 k power-law case.)
     constexpr int K = kChunk / 32;
     constexpr int L = NX == 0 ? 1 : NX;
-    double v[K], xv[K];
+    // D chunks in flight: the longest row's chain is the kernel's critical
+    // path, and with one chunk of look-ahead each step waited out most of a
+    // load latency (power-law 20 k, serial: 349 us for 474 MB)
+    constexpr int D = 3;
+    double v[D][K], xv[D][K];
+    auto load = [&](double(&vv)[K], double(&xx)[K], uint32_t c0) {
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-      const uint32_t p = s + k * 32 + lane;
-      const uint32_t q = p < e ? p : e - 1;
-      v[k] = static_cast<double>(vals[q]);
-      xv[k] = Elem<V>::load_x(x, col_idx[q]);
-    }
+      for (int k = 0; k < K; ++k) {
+        const uint32_t p = c0 + k * 32 + lane;
+        const uint32_t q = p < e ? p : e - 1;
+        vv[k] = static_cast<double>(vals[q]);
+        xx[k] = Elem<V>::load_x(x, col_idx[q]);
+      }
+    };
+#pragma unroll
+    for (int d = 0; d < D; ++d)
+      if (s + d * kChunk < e) load(v[d], xv[d], s + d * kChunk);
     double acc = 0.0;
-    for (uint32_t p0 = s; p0 < e; p0 += kChunk) {
+    for (uint32_t base = s; base < e; base += D * kChunk)
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      const uint32_t p0 = base + d * kChunk;
+      if (p0 >= e) break;
       double prod[K];
 #pragma unroll
-      for (int k = 0; k < K; ++k) prod[k] = __dmul_rn(v[k], xv[k]);
-      if (p0 + kChunk < e) {
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-          const uint32_t p = p0 + kChunk + k * 32 + lane;
-          const uint32_t q = p < e ? p : e - 1;
-          v[k] = static_cast<double>(vals[q]);
-          xv[k] = Elem<V>::load_x(x, col_idx[q]);
-        }
-      }
+      for (int k = 0; k < K; ++k) prod[k] = __dmul_rn(v[d][k], xv[d][k]);
+      if (p0 + D * kChunk < e) load(v[d], xv[d], p0 + D * kChunk);
 #pragma unroll
       for (int k = 0; k < K; ++k) buf[w][k * 32 + lane] = prod[k];
       __syncwarp();
