@@ -419,29 +419,139 @@ def run_loop(args, log):
     }
 
 
+REF_DIR = os.path.join(REPO, "baseline", "_ref")
+REF_CACHE = os.path.join(REPO, "baseline", "_cache")
+B200_PROFILE = os.path.join(REPO, "paper_2203_05096_b200", "data", "b200.json")
+
+
+def _import_reference():
+    """The UNMODIFIED reference package installed at baseline/_ref (pip
+    --target of /root/reference/pkg).  The repo root leaves sys.path first so
+    its `csrk` alias of this package cannot shadow it; nothing of this repo's
+    package (and none of its .so files) is imported on this arm."""
+    if not os.path.isfile(os.path.join(REF_DIR, "csrk", "__init__.py")):
+        return None
+    sys.path[:] = [REF_DIR] + [p for p in sys.path
+                               if os.path.abspath(p or os.getcwd()) != REPO]
+    for k in [k for k in sys.modules if k == "csrk" or k.startswith("csrk.")]:
+        del sys.modules[k]
+    import csrk
+    if not os.path.abspath(csrk.__file__).startswith(REF_DIR):
+        raise RuntimeError(f"reference import resolved to {csrk.__file__}")
+    return csrk
+
+
+def _load_synthetic():
+    """The numpy-only input generator (paper_2203_05096_b200/synthetic.py),
+    loaded by file path so the package (and its CUDA library) stays out of
+    this process -- the same generator the golden script feeds the reference."""
+    import importlib.util
+
+    spec = importlib.util.spec_from_file_location(
+        "_csrk_synthetic", os.path.join(REPO, "paper_2203_05096_b200", "synthetic.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
+
+
+def reference_matrix(ref, cfg: str, log):
+    """The config's CSR-k built entirely by the reference: CsrMatrix /
+    csr_from_arrays, compute_stats, tune_gpu with the B200 profile JSON (the
+    reference's own plugin mechanism, tuning.py:518), band_k, pack_csrk,
+    permute_vector.  band_k takes minutes at C2 / C3 / C5 in pure Python, so
+    its result (perm.fwd and the level sizes, written by this same code on a
+    previous run) is reused from baseline/_cache when the input digest
+    matches."""
+    import hashlib
+
+    syn = _load_synthetic()
+    t0 = time.perf_counter()
+    kind, shape, points = syn.CONFIGS[cfg]
+    if kind == "stencil":
+        n, rp, ci, va = syn.stencil_arrays(shape, points)
+        a = ref.CsrMatrix(n, n, rp, ci, va)
+    else:
+        rows, cols, vals = syn.irregular_triplets(shape)
+        a = ref.csr_from_arrays(shape, shape, rows, cols, vals)
+        n = a.n_rows
+    t_gen = time.perf_counter() - t0
+    stats = ref.compute_stats(a)
+    params = ref.tune_gpu(stats, ref.load_profile(B200_PROFILE))
+    targets = [params.srs, params.ssrs]
+    h = hashlib.sha256()
+    for arr in (a.row_ptr, a.col_idx, a.vals):
+        h.update(np.ascontiguousarray(arr).tobytes())
+    tag = h.hexdigest()[:16]
+    path = os.path.join(REF_CACHE, f"{cfg}_k3_{targets[0]}_{targets[1]}_{tag}.npz")
+    t0 = time.perf_counter()
+    cached = os.path.exists(path)
+    if cached:
+        z = np.load(path)
+        perm = ref.Permutation.from_forward(z["fwd"])
+        groups = [z["sizes0"].tolist(), z["sizes1"].tolist()]
+    else:
+        res = ref.band_k(a, 3, targets)
+        perm, groups = res.perm, [list(g) for g in res.level_group_sizes]
+        try:
+            os.makedirs(REF_CACHE, exist_ok=True)
+            np.savez(path, fwd=perm.fwd, sizes0=np.asarray(groups[0], dtype=np.int64),
+                     sizes1=np.asarray(groups[1], dtype=np.int64))
+        except OSError:
+            pass
+    t_band = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    m = ref.pack_csrk(a, perm, groups)
+    t_pack = time.perf_counter() - t0
+    x = np.random.default_rng(0).uniform(-1.0, 1.0, n)
+    xp = ref.permute_vector(perm, x)
+    log(f"[reference] {cfg}: n={n} nnz={a.nnz} targets {targets} gen {t_gen:.1f}s "
+        f"band_k {t_band:.1f}s ({'cached perm' if cached else 'computed'}) pack {t_pack:.1f}s")
+    return a, m, x, xp, params, {"gen_s": round(t_gen, 2), "band_k_s": round(t_band, 2),
+                                 "band_k_cached": cached, "pack_s": round(t_pack, 2)}
+
+
 def run_reference(args, log):
-    """--impl reference: the reference's CPU CSR-3 algorithm (oracle port),
-    all host cores, same config / metric."""
+    """--impl reference: the reference's own CPU CSR-3 SpMV,
+    ``spmv_csr3(m, xp, workers=os.cpu_count())`` (kernels.py:209-221), from
+    the unmodified package at baseline/_ref, on the same config, metric and
+    (B200-profile) group sizes as this repo's arm.  Rank 0 only."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return None
-    import paper_2203_05096_b200 as ck  # noqa: F401  (matrix construction only)
-
-    a, m, xp, params, _ = build_matrix(args.config, log)
-    from oracle import oracle as O
-
+    ref = _import_reference()
+    if ref is None:
+        return {"impl": "reference",
+                "unavailable": "baseline/_ref/csrk is not installed (pip --target of "
+                               "/root/reference/pkg)"}
+    if args.config == "C4":
+        return {"impl": "reference",
+                "unavailable": "C4 (938 M nonzeros): the reference's csr_from_arrays / "
+                               "band_k cannot build it in host RAM and time (SURVEY.md 8(d))"}
+    a, m, x, xp, params, build_t = reference_matrix(ref, args.config, log)
     threads = os.cpu_count() or 1
-    rows = O.csr3_group_rows(m.sr_ptr, m.ssr_ptr)
-    b = m.base
     for _ in range(args.warmup):
-        O.spmv_grouped(rows, b.row_ptr, b.col_idx, b.vals, xp, threads)
+        ref.spmv_csr3(m, xp, workers=threads)
     times = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        O.spmv_grouped(rows, b.row_ptr, b.col_idx, b.vals, xp, threads)
+        ref.spmv_csr3(m, xp, workers=threads)
         times.append(time.perf_counter() - t0)
     mean = sum(times) / len(times)
-    val = round(2.0 * a.nnz / mean / 1e9, 3)
+    val = round(2.0 * a.nnz / mean / 1e9, 4)
+    extra = {}
+    if args.config == "C1":
+        # BASELINE.json names C1 the "reference CPU path": the sequential
+        # oracle spmv_csr_ref (kernels.py:97-114), one core, one call
+        t0 = time.perf_counter()
+        ref.spmv_csr_ref(a, x)
+        t_ref = time.perf_counter() - t0
+        extra["spmv_csr_ref"] = {"value": round(2.0 * a.nnz / t_ref / 1e9, 4),
+                                 "unit": "GFLOP/s", "cores": 1, "seconds": round(t_ref, 3)}
+    try:
+        cpu_model = next((ln.split(":", 1)[1].strip() for ln in open("/proc/cpuinfo")
+                          if ln.startswith("model name")), None)
+    except OSError:
+        cpu_model = None
     return {
         "impl": "reference",
         "metric": METRIC,
@@ -455,18 +565,21 @@ def run_reference(args, log):
         "scaling": "strong",
         "vs_baseline": None,
         "dtype": "f64",
-        "data": "synthetic (deterministic grid Laplacian, x ~ U[-1,1) seed 0)",
+        "data": "synthetic (deterministic grid Laplacian / irregular rows, x ~ U[-1,1) seed 0)",
         "config": {"workload": CONFIG_TEXT.get(args.config, args.config),
-                   "config_id": args.config, "n_rows": a.n_rows, "nnz": a.nnz},
+                   "config_id": args.config, "n_rows": a.n_rows, "nnz": a.nnz,
+                   "ssrs_target": params.ssrs, "srs_target": params.srs,
+                   "n_sr": m.num_super_rows, "n_ssr": m.num_ssr},
         "cpu_baseline": {"value": val, "unit": "GFLOP/s", "cores": threads,
-                         "kind": "port",
-                         "sample": f"{args.steps} whole-matrix SpMVs of the same CSR-k "
-                                   "matrix; the reference's spmv_csr3 algorithm "
-                                   "(kernels.py:209-221) restated in C + OpenMP "
-                                   "(oracle/csrk_oracle.c); the pure-Python reference "
-                                   "cannot travel to the GPU box"},
+                         "kind": "reference", "cpu_model": cpu_model,
+                         "sample": f"{args.steps} whole-matrix calls of the unmodified "
+                                   "reference csrk.spmv_csr3(m, xp, workers=os.cpu_count()) "
+                                   "(kernels.py:209-221, baseline/_ref) on the CSR-k matrix "
+                                   "the reference's own band_k + pack_csrk built"},
         "e2e": {"value": val, "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "build_seconds": build_t,
+        **extra,
     }
 
 

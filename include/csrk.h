@@ -15,6 +15,22 @@
  *   - every function returns CSRK_OK (0) or an error code; the message of
  *     the last failure on the calling thread is csrk_last_error();
  *   - CSRK_EINVAL messages reuse the reference's ValueError wording.
+ *
+ * Threading
+ *   - a matrix handle is bound to one device; calls on distinct handles are
+ *     independent;
+ *   - every entry point that plans, stages or launches on a handle holds
+ *     that handle's lock, so concurrent calls on ONE handle serialise (the
+ *     reference's kernels are reentrant -- spmv_csr2/3 under a caller's
+ *     executor, kernels.py:158-182 -- and so are these);
+ *   - the stream-ordered SpMV entry points return once the work is queued:
+ *     a caller that launches on several streams orders its own x / y
+ *     buffers; the long-row kernel runs on a side stream private to each
+ *     caller stream (forked from and joined back to it), so launches on
+ *     different streams, or on one stream under CUDA-graph capture, share
+ *     no fork / join state;
+ *   - the host-buffer entry points (csrk_spmv_host, construction) block
+ *     until their results are in host memory.
  */
 #ifndef CSRK_H
 #define CSRK_H
@@ -94,7 +110,8 @@ int csrk_matrix_add_f32(csrk_matrix *m);
 int csrk_matrix_set_plan(csrk_matrix *m, int64_t tile_cost, int64_t cap,
                          int64_t stages);
 /* out = tile_cost, cap, rcap, stages, n_tiles, group_aligned, gather mode,
- *       ctas_per_sm (the f64 value when auto), layout, sliced copy built */
+ *       ctas_per_sm (the f64 value when auto), cut mode, n_long (rows
+ *       longer than 128 nonzeros, summed by the long-row kernel) */
 int csrk_matrix_plan(const csrk_matrix *m, int64_t out[10]);
 /* Schedule of the streaming kernel (B200 tuning knobs with no reference
  * counterpart; results are bitwise identical under every setting).
@@ -107,14 +124,17 @@ int csrk_matrix_plan(const csrk_matrix *m, int64_t out[10]);
  * carveout is set to exactly what they need, and the rest of the 256 KB
  * stays L1 for the x gathers. */
 int csrk_matrix_set_schedule(csrk_matrix *m, int gather, int ctas_per_sm);
-/* Layout of serial-order f64 launches: 0 = the CSR arrays (default), 1 =
- * sliced tiles.  A sliced tile keeps the tile's rows sorted by length in
- * slices of 32 rows with element j of a slice contiguous (SELL-32 per tile),
- * built once per plan on the device (an extra copy of the values and
- * columns); each row is still summed left to right by one thread, so y is
- * bitwise the same.  Opt-in: it removes the shared-memory bank conflicts of
- * the CSR stage but measured no faster on B200. */
-int csrk_matrix_set_layout(csrk_matrix *m, int layout);
+/* Where tile cuts may fall: 0 = auto (on group boundaries -- SSRs for
+ * k=3, SRs for k=2, the paper's block <-> super-super-row mapping of
+ * Listing 3 -- when every group costs at most tile_cost / 8, else on rows),
+ * 1 = always on rows, 2 = always on group boundaries (pitch shrunk by the
+ * largest group so a tile still fits its stage).  Results are bitwise the
+ * same; this is the A/B knob of DESIGN.md §7. */
+int csrk_matrix_set_cut_mode(csrk_matrix *m, int mode);
+/* Build (or rebuild) the tile plan a launch with this value type / order /
+ * nx would use, without launching: csrk_spmv_tiles and
+ * csrk_matrix_tile_rows then index exactly that plan. */
+int csrk_matrix_prepare(csrk_matrix *m, int value_type, int variant, int nx);
 
 /* ---- SpMV ------------------------------------------------------------------
  * y = A x on device-resident x / y (already in the permuted index space, as

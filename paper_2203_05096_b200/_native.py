@@ -48,7 +48,8 @@ _SIGNATURES = {
     "csrk_matrix_set_plan": ([P, I64, I64, I64], C.c_int),
     "csrk_matrix_plan": ([P, I64P], C.c_int),
     "csrk_matrix_set_schedule": ([P, C.c_int, C.c_int], C.c_int),
-    "csrk_matrix_set_layout": ([P, C.c_int], C.c_int),
+    "csrk_matrix_set_cut_mode": ([P, C.c_int], C.c_int),
+    "csrk_matrix_prepare": ([P, C.c_int, C.c_int, C.c_int], C.c_int),
     "csrk_spmv": ([P, C.c_int, C.c_int, C.c_int, P, P, P], C.c_int),
     "csrk_spmv_tiles": ([P, C.c_int, C.c_int, C.c_int, P, P, I64, I64, P], C.c_int),
     "csrk_matrix_tile_rows": ([P, U32P], C.c_int),
@@ -282,15 +283,19 @@ class DeviceMatrix:
         (0 inline, 1 gather-first) and resident CTAs per SM (0 = default)."""
         call("csrk_matrix_set_schedule", self.ptr, int(gather), int(ctas_per_sm))
 
-    def set_layout(self, layout: int):
-        """Serial f64 layout: 0 CSR (default), 1 sliced tiles (include/csrk.h)."""
-        call("csrk_matrix_set_layout", self.ptr, int(layout))
+    def set_cut_mode(self, mode: int):
+        """Tile cuts: 0 auto, 1 rows, 2 group (SSR) boundaries (include/csrk.h)."""
+        call("csrk_matrix_set_cut_mode", self.ptr, int(mode))
+
+    def prepare(self, variant=CSRK_SERIAL, nx=1, f32=False):
+        """Build the tile plan a launch of this order would use (no launch)."""
+        call("csrk_matrix_prepare", self.ptr, CSRK_F32 if f32 else CSRK_F64, variant, nx)
 
     def plan(self) -> dict:
         out = np.zeros(10, dtype=np.int64)
         call("csrk_matrix_plan", self.ptr, i64p(out))
         keys = ("tile_cost", "cap", "rcap", "stages", "n_tiles", "group_aligned",
-                "gather_first", "ctas_per_sm", "layout", "sliced")
+                "gather_first", "ctas_per_sm", "cut_mode", "n_long")
         return {k: int(v) for k, v in zip(keys, out)}
 
     def stats(self):

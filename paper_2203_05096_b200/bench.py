@@ -20,6 +20,7 @@ Targets (TARGETS, the registration point of reference bench.py:58, 169-178):
 
 from __future__ import annotations
 
+import json
 import os
 import time
 from dataclasses import asdict, dataclass
@@ -28,7 +29,7 @@ import numpy as np
 
 from . import _native as nat
 from .format import CsrMatrix, pack_csrk, permute_vector, unpermute_vector
-from .kernels import STRIDED_NX, BlockDims, spmv_csr_ref
+from .kernels import STRIDED_NX, BlockDims, host_row_sums, spmv_csr_ref
 from .reorder import band_k
 from .tuning import (
     VOLTA,
@@ -102,6 +103,27 @@ def scaled_error(y, ref, abs_row_dot) -> float:
     return float((diff[~zero] / d[~zero]).max()) if np.any(~zero) else 0.0
 
 
+NOMINAL_HBM_GBS = 8000.0
+
+
+def measured_hbm_gbs():
+    """The measured HBM copy bandwidth of this machine, GB/s: $CSRK_HBM_GBS,
+    else MEASURED_PEAKS.json next to the package (the repo root), else None."""
+    env = os.environ.get("CSRK_HBM_GBS", "").strip()
+    if env:
+        try:
+            return float(env)
+        except ValueError:
+            return None
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                        "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            return float(json.load(fh)["hbm_gbs"])
+    except (OSError, ValueError, KeyError, TypeError):
+        return None
+
+
 def spmv_bytes(n_rows: int, n_cols: int, nnz: int, value_bytes: int = 8) -> int:
     """Algorithmic HBM bytes of one SpMV: vals + col_idx
     + row_ptr + x + y, each touched once."""
@@ -167,6 +189,16 @@ class BenchRecord:
     passed: bool
     reorder_seconds: float
     pack_seconds: float
+    # B200 extensions: algorithmic HBM bytes per
+    # multiply (spmv_bytes) over the mean time, its fraction of the nominal
+    # 8 TB/s and of the measured copy bandwidth (when known), the scaled
+    # error max |y - ref| / (|A||x|) of SURVEY.md §8(c)(3), and what the
+    # result was verified against
+    gbs: float = 0.0
+    frac_of_nominal: float = 0.0
+    frac_of_measured: float | None = None
+    scaled_error: float = 0.0
+    verified_against: str = "spmv_csr_ref (host, sequential row sums)"
 
     def to_dict(self) -> dict:
         return asdict(self)
@@ -321,9 +353,15 @@ def run_benchmark(a: CsrMatrix, matrix_id: str, target: str, *, ssrs=None, srs=N
     if perm is not None:
         y = unpermute_vector(perm, y)
     err = max_rel_error(y, ref_y)
+    scale = host_row_sums(a.row_ptr, a.col_idx, np.abs(a.vals), np.abs(x))
+    gbs = spmv_bytes(a.n_rows, a.n_cols, a.nnz, 8) / mean / 1e9 if mean > 0 else float("inf")
+    peak = measured_hbm_gbs()
     return BenchRecord(
         schema_version=SCHEMA_VERSION, matrix_id=matrix_id, kernel=target,
         tuning=tuning, warmups=warmups, reps=reps, mean_seconds=mean,
         gflops=2.0 * a.nnz / mean / 1e9 if mean > 0 else float("inf"),
         max_rel_error=err, tolerance=tolerance, passed=bool(err <= tolerance),
-        reorder_seconds=reorder_s, pack_seconds=pack_s)
+        reorder_seconds=reorder_s, pack_seconds=pack_s,
+        gbs=gbs, frac_of_nominal=gbs / NOMINAL_HBM_GBS,
+        frac_of_measured=(gbs / peak) if peak else None,
+        scaled_error=scaled_error(y, ref_y, scale))

@@ -20,6 +20,7 @@ import ctypes as C
 import numpy as np
 
 from . import _native as nat
+from .kernels import check_device_vector
 
 __all__ = ["cg", "power_iterations", "GraphedLoop", "device_handle"]
 
@@ -55,14 +56,17 @@ def cg(m, b, x=None, iters: int = 100, *, dims=None, variant: str = "serial",
     import torch
 
     dev = device_handle(m)
-    if b.dim() != 1 or b.shape[0] != dev.n_rows or not b.is_contiguous():
-        raise ValueError(f"b must be a contiguous vector of length {dev.n_rows}")
+    if dev.n_rows != dev.n_cols:
+        raise ValueError("CG requires a square matrix")
     vt = _vt(b)
+    check_device_vector(b, dev, dev.n_rows, "b")
     if vt == nat.CSRK_F32:
         dev.ensure_f32()
     if x is None:
         x = torch.zeros_like(b)
     r, p, ap = scratch if scratch is not None else (torch.empty_like(b) for _ in range(3))
+    for name, t in (("x", x), ("r", r), ("p", p), ("ap", ap)):
+        check_device_vector(t, dev, dev.n_rows, name, dtype=b.dtype)
     var, nx = _variant(dims, variant)
     stream = stream or torch.cuda.current_stream(b.device)
     sc = np.zeros(4) if sync else None
@@ -83,10 +87,14 @@ def power_iterations(m, x, iters: int = 100, *, dims=None, variant: str = "seria
     import torch
 
     dev = device_handle(m)
+    if dev.n_rows != dev.n_cols:
+        raise ValueError("power iterations require a square matrix")
     vt = _vt(x)
+    check_device_vector(x, dev, dev.n_cols, "x")
     if vt == nat.CSRK_F32:
         dev.ensure_f32()
     y = torch.empty_like(x) if y is None else y
+    check_device_vector(y, dev, dev.n_rows, "y", dtype=x.dtype)
     var, nx = _variant(dims, variant)
     stream = stream or torch.cuda.current_stream(x.device)
     nat.call("csrk_power", dev.ptr, vt, var, nx, C.c_void_p(x.data_ptr()),

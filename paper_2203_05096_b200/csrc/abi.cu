@@ -58,7 +58,6 @@ static void release(csrk_matrix *m) {
   cudaFree(m->ssr_ptr);
   cudaFree(m->plan.tile_row);
   cudaFree(m->plan.long_rows);
-  csrk::free_sliced(m);
   cudaFree(m->x_stage);
   cudaFree(m->y_stage);
   for (auto e : m->pipe.ev_x) cudaEventDestroy(e);
@@ -66,9 +65,11 @@ static void release(csrk_matrix *m) {
   if (m->pipe.h2d) cudaStreamDestroy(m->pipe.h2d);
   if (m->pipe.comp) cudaStreamDestroy(m->pipe.comp);
   if (m->pipe.d2h) cudaStreamDestroy(m->pipe.d2h);
-  if (m->long_fork) cudaEventDestroy(m->long_fork);
-  if (m->long_join) cudaEventDestroy(m->long_join);
-  if (m->long_stream) cudaStreamDestroy(m->long_stream);
+  for (auto &sd : m->sides) {
+    cudaEventDestroy(sd.fork);
+    cudaEventDestroy(sd.join);
+    cudaStreamDestroy(sd.side);
+  }
   if (m->ev0) cudaEventDestroy(m->ev0);
   if (m->ev1) cudaEventDestroy(m->ev1);
   if (m->stream) cudaStreamDestroy(m->stream);
@@ -326,6 +327,7 @@ int csrk_matrix_add_f32(csrk_matrix *m) {
     return CSRK_EINVAL;
   }
   if (m->vals32) return CSRK_OK;
+  CSRK_LOCK(m);
   CSRK_CUDA_TRY(cudaSetDevice(m->device));
   const int64_t pn = padded_nnz(m->nnz);
   CSRK_CUDA_TRY(cudaMalloc(&m->vals32, pn * sizeof(float)));
@@ -341,6 +343,7 @@ int csrk_matrix_set_plan(csrk_matrix *m, int64_t tile_cost, int64_t cap,
     set_error("null argument");
     return CSRK_EINVAL;
   }
+  CSRK_LOCK(m);
   CSRK_CUDA_TRY(cudaSetDevice(m->device));
   CSRK_TRY(ensure_plan(m, tile_cost, cap, stages, m->stream));
   m->plan.auto_tile = tile_cost <= 0;
@@ -354,6 +357,7 @@ int csrk_spmv(const csrk_matrix *m, int value_type, int variant, int nx,
     set_error("null argument");
     return CSRK_EINVAL;
   }
+  CSRK_LOCK(m);
   CSRK_CUDA_TRY(cudaSetDevice(m->device));
   CSRK_TRY(prepare_plan(m, value_type, variant, nx));
   return launch_spmv(m, value_type, variant, nx, x, y,
@@ -372,9 +376,8 @@ int csrk_spmv_tiles(const csrk_matrix *m, int value_type, int variant, int nx,
     return CSRK_EINVAL;
   }
   if (t1 == t0) return CSRK_OK;
+  CSRK_LOCK(m);
   CSRK_CUDA_TRY(cudaSetDevice(m->device));
-  if (sliced_wanted(m, value_type, variant))  // tile ranges index the current plan
-    CSRK_TRY(ensure_sliced(const_cast<csrk_matrix *>(m), m->stream));
   return launch_spmv(m, value_type, variant, nx, x, y, static_cast<cudaStream_t>(stream),
                      t0, t1);
 }
@@ -388,6 +391,7 @@ int csrk_matrix_tile_rows(const csrk_matrix *m, uint32_t *out) {
     set_error("matrix has no tile plan");
     return CSRK_EINVAL;
   }
+  CSRK_LOCK(m);
   CSRK_CUDA_TRY(cudaSetDevice(m->device));
   CSRK_CUDA_TRY(cudaMemcpy(out, m->plan.tile_row, (m->plan.n_tiles + 1) * sizeof(uint32_t),
                            cudaMemcpyDeviceToHost));
@@ -514,6 +518,7 @@ int csrk_spmv_host(csrk_matrix *m, int value_type, int variant, int nx,
     return CSRK_EINVAL;
   }
   const size_t es = value_type == CSRK_F32 ? sizeof(float) : sizeof(double);
+  CSRK_LOCK(m);
   CSRK_CUDA_TRY(cudaSetDevice(m->device));
   CSRK_TRY(prepare_plan(m, value_type, variant, nx));
   const size_t xb = static_cast<size_t>(m->n_cols) * es + 16;
@@ -657,26 +662,50 @@ int csrk_matrix_plan(const csrk_matrix *m, int64_t out[10]) {
   out[5] = m->plan.group_aligned ? 1 : 0;
   out[6] = m->plan.gather_first;
   out[7] = m->plan.ctas_per_sm ? m->plan.ctas_per_sm : auto_ctas(m->plan.row_var, 8);
-  out[8] = m->plan.layout;
-  out[9] = (m->sliced.col && m->sliced.gen == m->plan.gen) ? 1 : 0;
+  out[8] = m->plan.cut_mode;
+  out[9] = m->plan.n_long;
   return CSRK_OK;
 }
 
-int csrk_matrix_set_layout(csrk_matrix *m, int layout) {
+int csrk_matrix_set_cut_mode(csrk_matrix *m, int mode) {
   if (!m) {
     set_error("null argument");
     return CSRK_EINVAL;
   }
-  if (layout < 0 || layout > 1) {
-    set_error("layout must be 0 (CSR) or 1 (sliced tiles), got %d", layout);
+  if (mode < 0 || mode > 2) {
+    set_error("cut mode must be 0 (auto), 1 (rows) or 2 (groups), got %d", mode);
     return CSRK_EINVAL;
   }
-  m->plan.layout = layout;
-  if (layout == 0) {
-    CSRK_CUDA_TRY(cudaSetDevice(m->device));
-    CSRK_CUDA_TRY(cudaStreamSynchronize(m->stream));
-    free_sliced(m);
+  CSRK_LOCK(m);
+  if (mode == m->plan.cut_mode) return CSRK_OK;
+  m->plan.cut_mode = mode;
+  if (m->n_rows == 0) return CSRK_OK;
+  CSRK_CUDA_TRY(cudaSetDevice(m->device));
+  // rebuild the current plan with the new cuts
+  const bool keep = m->plan.auto_tile;
+  CSRK_TRY(ensure_plan(m, m->plan.tile_cost, m->plan.cap, m->plan.stages, m->stream, true));
+  m->plan.auto_tile = keep;
+  CSRK_CUDA_TRY(cudaStreamSynchronize(m->stream));
+  return CSRK_OK;
+}
+
+int csrk_matrix_prepare(csrk_matrix *m, int value_type, int variant, int nx) {
+  if (!m) {
+    set_error("null argument");
+    return CSRK_EINVAL;
   }
+  if (variant != CSRK_SERIAL && variant != CSRK_STRIDED) {
+    set_error("unknown SpMV variant %d", variant);
+    return CSRK_EINVAL;
+  }
+  if (value_type != CSRK_F64 && value_type != CSRK_F32) {
+    set_error("unknown value type %d", value_type);
+    return CSRK_EINVAL;
+  }
+  CSRK_LOCK(m);
+  CSRK_CUDA_TRY(cudaSetDevice(m->device));
+  CSRK_TRY(prepare_plan(m, value_type, variant, nx));
+  CSRK_CUDA_TRY(cudaStreamSynchronize(m->stream));
   return CSRK_OK;
 }
 
@@ -694,6 +723,7 @@ int csrk_matrix_set_schedule(csrk_matrix *m, int gather, int ctas_per_sm) {
     set_error("ctas_per_sm must be in 0..8, got %d", ctas_per_sm);
     return CSRK_EINVAL;
   }
+  CSRK_LOCK(m);
   m->plan.gather_first = gather;
   m->plan.ctas_per_sm = ctas_per_sm;
   return CSRK_OK;
@@ -722,6 +752,7 @@ int csrk_spmv_listing3(const csrk_matrix *m, int dx, int dy, const double *x,
     set_error("block holds %d threads, limit is 1024", dx * dy);
     return CSRK_EINVAL;
   }
+  CSRK_LOCK(m);
   CSRK_CUDA_TRY(cudaSetDevice(m->device));
   return launch_listing3(m, dx, dy, x, y, trace,
                          static_cast<cudaStream_t>(stream));
@@ -742,6 +773,7 @@ int csrk_spmv_listing4(const csrk_matrix *m, int dx, int dy, int dz,
     set_error("block holds %d threads, limit is 1024", dx * dy * dz);
     return CSRK_EINVAL;
   }
+  CSRK_LOCK(m);
   CSRK_CUDA_TRY(cudaSetDevice(m->device));
   return launch_listing4(m, dx, dy, dz, x, y, trace,
                          static_cast<cudaStream_t>(stream));

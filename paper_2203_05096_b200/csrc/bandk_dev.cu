@@ -491,6 +491,8 @@ extern "C" int csrk_band_k_device(const csrk_matrix *a, int k, const double *tar
   CSRK_CUDA_TRY(cudaSetDevice(a->device));
   auto *res = new csrk_bandk_result();
   const int rc = csrk::band_k_dev(a, k, targets, *res, nullptr, a->stream);
+  cudaStreamSynchronize(a->stream);
+  csrk::trim_async_pool();  // the builder's scratch goes back to the driver
   if (rc != CSRK_OK) {
     delete res;
     if (rc == CSRK_ECUDA) csrk::set_error("CUDA error in device band_k");

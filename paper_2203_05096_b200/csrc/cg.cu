@@ -290,6 +290,7 @@ int csrk_cg(const csrk_matrix *m, int value_type, int variant, int nx, const voi
     set_error("CG requires a square matrix");
     return CSRK_EINVAL;
   }
+  CSRK_LOCK(m);
   CSRK_CUDA_TRY(cudaSetDevice(m->device));
   CSRK_TRY(prepare_plan(m, value_type, variant, nx));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -310,6 +311,11 @@ int csrk_power(const csrk_matrix *m, int value_type, int variant, int nx, void *
     set_error("invalid argument to csrk_power");
     return CSRK_EINVAL;
   }
+  if (m->n_rows != m->n_cols) {  // y becomes the next x
+    set_error("power iterations require a square matrix");
+    return CSRK_EINVAL;
+  }
+  CSRK_LOCK(m);
   CSRK_CUDA_TRY(cudaSetDevice(m->device));
   CSRK_TRY(prepare_plan(m, value_type, variant, nx));
   cudaStream_t s = static_cast<cudaStream_t>(stream);

@@ -965,8 +965,10 @@ int csrk_pack(int device, int64_t n, int64_t nnz, const uint32_t *row_ptr,
     csrk::set_error("null argument");
     return CSRK_EINVAL;
   }
-  return csrk::pack_device(device, n, nnz, row_ptr, col_idx, vals, fwd, inv,
+  const int rc = csrk::pack_device(device, n, nnz, row_ptr, col_idx, vals, fwd, inv,
                            n_levels, n_sizes1, sizes1, n_sizes2, sizes2, out);
+  csrk::trim_async_pool();
+  return rc;
 }
 
 int csrk_gather_f64(int64_t n, const double *in, const int64_t *idx,
@@ -987,6 +989,7 @@ int csrk_matrix_group_uniform(csrk_matrix *m, int64_t srs, int64_t ssrs) {
     csrk::set_error("null argument");
     return CSRK_EINVAL;
   }
+  CSRK_LOCK(m);
   return csrk::group_uniform(m, srs, ssrs);
 }
 
@@ -1014,7 +1017,9 @@ int csrk_coo_to_csr(int device, int64_t n_rows, int64_t n_cols, int64_t count,
     csrk::set_error("null argument");
     return CSRK_EINVAL;
   }
-  return csrk::coo_to_csr_device(device, n_rows, n_cols, count, rows, cols, vals, out);
+  const int rc = csrk::coo_to_csr_device(device, n_rows, n_cols, count, rows, cols, vals, out);
+  csrk::trim_async_pool();
+  return rc;
 }
 
 int csrk_stencil_slab(int device, int64_t nz, int64_t ny, int64_t nx, int points,

@@ -5,6 +5,7 @@
 #include <cstdarg>
 #include <cstdint>
 #include <cstdio>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -91,7 +92,7 @@ struct TilePlan {
   double mean_short = 0.0;  // mean length of the rows the streaming kernel sums (<= kLongRow)
   bool row_stats = false;
   bool auto_tile = true;  // tile cost follows the launch's order (auto_tile_cost)
-  int layout = 0;         // serial f64 layout: 0 CSR, 1 sliced tiles
+  int cut_mode = 0;       // 0 auto, 1 rows, 2 groups (csrk_matrix_set_cut_mode)
   uint64_t gen = 0;       // bumped whenever tile_row is rebuilt
   uint32_t *tile_row = nullptr;  // device, n_tiles + 1
   uint32_t *tile_ptr = nullptr;  // device, n_tiles + 1 (same allocation): row_ptr[tile_row]
@@ -115,16 +116,6 @@ inline const uint32_t *long_rows_asc(const TilePlan &pl) {
 
 }  // namespace csrk
 
-// Sliced-tile copy of the matrix for the serial f64 kernel (SELL-32 inside
-// every tile of the plan it was built for; csrc/spmv.cu).
-struct csrk_sliced {
-  uint64_t gen = ~0ull;  // plan generation it belongs to
-  int64_t n_slices = 0, entries = 0;
-  uint32_t *col = nullptr, *meta = nullptr, *info = nullptr, *base = nullptr;
-  double *val = nullptr;
-  unsigned long long *te = nullptr;
-};
-
 struct csrk_matrix {
   int device = 0;
   int64_t n_rows = 0, n_cols = 0, nnz = 0;
@@ -137,7 +128,6 @@ struct csrk_matrix {
   uint32_t *sr_ptr = nullptr;   // n_sr + 1 (k >= 2)
   uint32_t *ssr_ptr = nullptr;  // n_ssr + 1 (k == 3)
   csrk::TilePlan plan;          // current streaming plan
-  csrk_sliced sliced;           // optional sliced copy (serial f64 launches)
   int sm_count = 0;
   // host-API staging and the overlapped host pipeline (csrk_spmv_host)
   struct Pipe {
@@ -154,9 +144,19 @@ struct csrk_matrix {
   } pipe;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-  // the long-row kernel's side stream (forked from / joined to the caller's)
-  cudaStream_t long_stream = nullptr;
-  cudaEvent_t long_fork = nullptr, long_join = nullptr;
+  // the long-row kernel's side streams: one per caller stream (forked from /
+  // joined to it), so launches on different streams -- or one being
+  // captured into a CUDA graph -- never share fork / join state
+  struct Side {
+    cudaStream_t caller = nullptr, side = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+  };
+  std::vector<Side> sides;
+  // Thread safety: every C-ABI entry point that plans, stages or launches on
+  // a matrix holds this lock (include/csrk.h "Threading"), so concurrent
+  // callers of one handle serialise instead of racing on the plan, the
+  // staging buffers and the pipeline streams.
+  mutable std::mutex mu;
   void *x_stage = nullptr, *y_stage = nullptr;
   size_t x_stage_bytes = 0, y_stage_bytes = 0;
 };
@@ -189,6 +189,18 @@ inline void keep_async_pool() {
   if (dev < 32) done.fetch_or(1u << dev, std::memory_order_relaxed);
 }
 
+// One-shot builders (device Band-k, pack, COO -> CSR) hand the scratch they
+// cached in the pool back to the driver when they finish (after their final
+// synchronisation), so cudaMalloc-based allocators -- PyTorch's caching
+// allocator, NCCL -- can use it; the raised threshold above only keeps
+// memory mapped across the level loops *inside* one build.
+inline void trim_async_pool() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
+}
+
 // padded element count for col_idx / vals allocations: room for the 16-byte
 // aligned over-read of the TMA bulk copies at both ends of a span.
 inline int64_t padded_nnz(int64_t nnz) { return ((nnz + 3) / 4) * 4 + 8; }
@@ -196,15 +208,10 @@ inline int64_t padded_rows(int64_t n_rows) { return ((n_rows + 1 + 3) / 4) * 4 +
 
 int alloc_matrix_arrays(csrk_matrix *m, bool want64, bool want32);
 int ensure_plan(csrk_matrix *m, int64_t tile_cost, int64_t cap, int64_t stages,
-                cudaStream_t s);
+                cudaStream_t s, bool force = false);
 // before a whole-matrix launch: re-plan for the launch's order when the plan
 // is automatic (cached; rebuilds only when the tile cost changes)
 int prepare_plan(const csrk_matrix *m, int value_type, int variant, int nx);
-// the sliced copy for the current plan (built when a serial f64 launch
-// uses it: layout 1)
-bool sliced_wanted(const csrk_matrix *m, int value_type, int variant);
-int ensure_sliced(csrk_matrix *m, cudaStream_t s);
-void free_sliced(csrk_matrix *m);
 int launch_spmv(const csrk_matrix *m, int value_type, int variant, int nx,
                 const void *x, void *y, cudaStream_t stream, int64_t t0 = 0,
                 int64_t t1 = -1);
@@ -232,6 +239,9 @@ int radix_sort_pairs(uint64_t *keys, uint32_t *vals, uint64_t *tmp_keys,
       return e_ == cudaErrorMemoryAllocation ? CSRK_ENOMEM : CSRK_ECUDA;    \
     }                                                                       \
   } while (0)
+
+// the per-matrix lock of the C-ABI entry points (csrk_matrix::mu)
+#define CSRK_LOCK(m) std::lock_guard<std::mutex> csrk_lock_guard_((m)->mu)
 
 #define CSRK_TRY(expr)            \
   do {                            \

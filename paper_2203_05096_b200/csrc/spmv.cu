@@ -136,16 +136,13 @@ struct Geometry {
   uint32_t v_off, c_off, r_off, s_off, stage_bytes, header_bytes;
 
   // CSR stages: vals / col_idx spans (cap) and row pointers (rcap + 1).
-  // Sliced stages: the same vals / col_idx room for the slice entries, the
-  // r region for the slice lanes' row words and an s region for the slice
-  // descriptors (at most rcap / 32 + 1 slices).
   __host__ __device__ Geometry(uint32_t cap_, uint32_t rcap_, uint32_t stages_,
-                               uint32_t vsize, bool sliced = false)
+                               uint32_t vsize)
       : cap(cap_), rcap(rcap_), stages(stages_) {
     v_elems = cap + 8;       // alignment slack at both ends
     c_elems = cap + 8;
     r_elems = rcap + 1 + 8;  // rows + 1 pointers
-    s_elems = sliced ? rcap / 32 + 1 + 8 : 0;
+    s_elems = 0;
     v_off = 0;
     c_off = round_up(v_elems * vsize, 128);
     r_off = c_off + round_up(c_elems * 4, 128);
@@ -742,247 +739,6 @@ int launch_long_rows(const csrk_matrix *m, const V *vals, const V *x, V *y, cuda
   return CSRK_OK;
 }
 
-// ---- sliced tiles (serial order) -----------------------------------------
-//
-// The CSR stage above hands each consumer thread one row, so a warp's 32
-// shared-memory loads of "element j" hit 32 unrelated addresses: bank
-// conflicts made the shared-memory wavefronts 36 % of the L1TEX data pipe on
-// C5, the same pipe that serves the x gathers.  A sliced tile stores the
-// tile's rows sorted by length (descending, ties by row) in slices of 32:
-// element j of the slice's 32 rows is contiguous (SELL-32 inside the tile),
-// so the loads are conflict-free and one warp walks one slice.  Each row is
-// still summed by one thread from its first column to its last -- the
-// reference's serial order, bit for bit.
-//
-// Measured (profiles/r01_sliced_layout.txt): on C5 the sliced kernel cuts
-// the shared wavefronts 24.3 M -> 8.6 M, the L1TEX pipe 91 % -> 63 % and the
-// instructions by 28 %, yet runs at the same speed (241 vs 233 us): with the
-// pipe relieved the kernel is bound by gather latency at the occupancy the
-// stage ring allows, and the row-sorted y stores scatter.  C2 is 4 % slower.
-// So it is an opt-in layout (csrk_matrix_set_layout 1), not the default.
-//
-// Per slice s: sinfo[s] = (entry offset from the tile start / 32) << 16 | L
-// (L = the slice's longest row); per lane: sm[32 s + lane] = (row - tile's
-// first row) << 16 | row length, 0xffffffff for lanes past the tile's rows.
-// Per tile t: slices [sbase[t], sbase[t+1]), entries [te[t], te[t+1]).
-
-constexpr uint32_t kNoLane = 0xffffffffu;
-
-template <int B>
-__device__ __forceinline__ double slice_row(const double *__restrict__ sv,
-                                            const uint32_t *__restrict__ sc, uint32_t base,
-                                            uint32_t len, uint32_t L, int lane,
-                                            const double *__restrict__ x) {
-  double acc = 0.0;
-  for (uint32_t j0 = 0; j0 < L; j0 += B) {
-    uint32_t c[B];
-    double v[B], xv[B];
-#pragma unroll
-    for (int j = 0; j < B; ++j) {
-      const uint32_t jj = j0 + j < L ? j0 + j : L - 1;
-      const uint32_t q = base + jj * 32 + lane;
-      c[j] = j0 + j < len ? sc[q] : 0u;  // spare lanes read x[0]
-      v[j] = sv[q];
-    }
-#pragma unroll
-    for (int j = 0; j < B; ++j) xv[j] = __ldg(x + c[j]);
-#pragma unroll
-    for (int j = 0; j < B; ++j)
-      if (j0 + j < len) acc = __dadd_rn(acc, __dmul_rn(v[j], xv[j]));
-  }
-  return acc;
-}
-
-__global__ void __launch_bounds__(kThreads, 2)
-    csrk_sliced_kernel(const uint32_t *__restrict__ row_ptr,
-                       const uint32_t *__restrict__ col_idx,
-                       const double *__restrict__ vals, const double *__restrict__ x,
-                       double *__restrict__ y, const uint32_t *__restrict__ tile_row,
-                       const uint32_t *__restrict__ s_col, const double *__restrict__ s_val,
-                       const uint32_t *__restrict__ s_meta,
-                       const uint32_t *__restrict__ s_info,
-                       const uint32_t *__restrict__ s_base,
-                       const unsigned long long *__restrict__ s_te, uint32_t n_tiles,
-                       uint32_t cap, uint32_t rcap, uint32_t stages) {
-  extern __shared__ __align__(128) unsigned char smem[];
-  const Geometry geo(cap, rcap, stages, sizeof(double), true);
-  uint64_t *full = reinterpret_cast<uint64_t *>(smem);
-  uint64_t *empty = full + stages;
-  StageMeta *meta = reinterpret_cast<StageMeta *>(empty + stages);
-  unsigned char *stage0 = smem + geo.header_bytes;
-
-  const int tid = threadIdx.x;
-  if (tid == 0) {
-    for (uint32_t s = 0; s < stages; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kConsumerWarps);
-    }
-    fence_barrier_init();
-  }
-  __syncthreads();
-
-  const uint32_t grid = gridDim.x;
-  if (tid < 32) {
-    // ---------------- producer warp ----------------
-    if (tid != 0) return;
-    const uint64_t policy = evict_first_policy();
-    uint32_t i = 0;
-    for (uint32_t t = blockIdx.x; t < n_tiles; t += grid, ++i) {
-      const uint32_t s = i % stages;
-      const uint32_t r0 = tile_row[t], r1 = tile_row[t + 1];
-      const uint32_t q0 = s_base[t], q1 = s_base[t + 1];
-      const unsigned long long e0 = s_te[t], e1 = s_te[t + 1];
-      if (i >= stages) mbar_wait(&empty[s], ((i / stages) + 1) & 1);
-      StageMeta &md = meta[s];
-      md.r0 = r0;
-      md.r1 = r1;
-      md.h0 = q1 - q0;  // slices of the tile
-      if (e1 - e0 <= cap && (q1 - q0) * 32 <= rcap) {
-        unsigned char *st = stage0 + s * geo.stage_bytes;
-        const uint32_t n_e = static_cast<uint32_t>(e1 - e0);   // a multiple of 32
-        const uint32_t sa0 = q0 & ~3u, sa1 = round_up(q1, 4);  // slice descriptors
-        md.va0 = sa0;
-        md.mode = kStaged;
-        const uint32_t bytes = n_e * 12u + (q1 - q0) * 128u + (sa1 - sa0) * 4u;
-        mbar_arrive_expect_tx(&full[s], bytes);
-        if (n_e) {
-          tma_bulk_load(st + geo.v_off, s_val + e0, n_e * 8u, &full[s], policy);
-          tma_bulk_load(st + geo.c_off, s_col + e0, n_e * 4u, &full[s], policy);
-        }
-        if (q1 > q0)
-          tma_bulk_load(st + geo.r_off, s_meta + static_cast<size_t>(q0) * 32,
-                        (q1 - q0) * 128u, &full[s], policy);
-        if (sa1 > sa0)
-          tma_bulk_load(st + geo.s_off, s_info + sa0, (sa1 - sa0) * 4u, &full[s], policy);
-      } else {
-        md.mode = kDirect;
-        mbar_arrive(&full[s]);
-      }
-    }
-    return;
-  }
-
-  // ---------------- consumer warps ----------------
-  const int ct = tid - 32;
-  const int lane = ct & 31, warp = ct >> 5;
-  uint32_t i = 0;
-  for (uint32_t t = blockIdx.x; t < n_tiles; t += grid, ++i) {
-    const uint32_t s = i % stages;
-    mbar_wait(&full[s], (i / stages) & 1);
-    const StageMeta md = meta[s];
-    if (md.mode == kStaged) {
-      const unsigned char *st = stage0 + s * geo.stage_bytes;
-      const double *sv = reinterpret_cast<const double *>(st + geo.v_off);
-      const uint32_t *sc = reinterpret_cast<const uint32_t *>(st + geo.c_off);
-      const uint32_t *sm = reinterpret_cast<const uint32_t *>(st + geo.r_off);
-      const uint32_t *si =
-          reinterpret_cast<const uint32_t *>(st + geo.s_off) + (s_base[t] - md.va0);
-      for (uint32_t q = warp; q < md.h0; q += kConsumerWarps) {
-        const uint32_t info = si[q];
-        const uint32_t m = sm[q * 32 + lane];
-        const double acc = slice_row<8>(sv, sc, (info >> 16) * 32,
-                                        m == kNoLane ? 0u : (m & 0xffffu), info & 0xffffu,
-                                        lane, x);
-        if (m != kNoLane) y[md.r0 + (m >> 16)] = acc;
-      }
-    } else {
-      compute_direct<double, 0>(md.r0, md.r1, row_ptr, col_idx, vals, x, y, ct);
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
-  }
-}
-
-// sliced layout construction (host side in build_sliced below)
-__global__ void tile_of_row_kernel(const uint32_t *__restrict__ tile_row, int64_t n_tiles,
-                                   const uint32_t *__restrict__ row_ptr,
-                                   uint64_t *__restrict__ keys, uint32_t *__restrict__ vals) {
-  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n_tiles;
-       t += int64_t(gridDim.x) * blockDim.x) {
-    for (uint32_t r = tile_row[t]; r < tile_row[t + 1]; ++r) {
-      uint64_t len = row_ptr[r + 1] - row_ptr[r];
-      if (len > 0xffffffull) len = 0xffffffull;
-      keys[r] = (static_cast<uint64_t>(t) << 24) | (0xffffffull - len);
-      vals[r] = r;
-    }
-  }
-}
-
-// per tile: slice count; per slice: length (the first = longest sorted row)
-__global__ void slice_count_kernel(const uint32_t *__restrict__ tile_row, int64_t n_tiles,
-                                   int64_t *__restrict__ ns) {
-  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n_tiles;
-       t += int64_t(gridDim.x) * blockDim.x)
-    ns[t] = (tile_row[t + 1] - tile_row[t] + 31) / 32;
-}
-
-__global__ void slice_len_kernel(const uint32_t *__restrict__ tile_row, int64_t n_tiles,
-                                 const int64_t *__restrict__ sbase,
-                                 const uint32_t *__restrict__ sorted_rows,
-                                 const uint32_t *__restrict__ row_ptr,
-                                 int64_t *__restrict__ slen, uint32_t *__restrict__ s_base) {
-  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t <= n_tiles;
-       t += int64_t(gridDim.x) * blockDim.x) {
-    s_base[t] = static_cast<uint32_t>(sbase[t]);
-    if (t == n_tiles) continue;
-    const uint32_t r0 = tile_row[t], r1 = tile_row[t + 1];
-    for (int64_t q = sbase[t]; q < sbase[t + 1]; ++q) {
-      const uint32_t r = sorted_rows[r0 + 32 * (q - sbase[t])];
-      slen[q] = 32 * static_cast<int64_t>(row_ptr[r + 1] - row_ptr[r]);
-    }
-    (void)r1;
-  }
-}
-
-__global__ void slice_info_kernel(const uint32_t *__restrict__ tile_row, int64_t n_tiles,
-                                  const int64_t *__restrict__ sbase,
-                                  const int64_t *__restrict__ soff,
-                                  const int64_t *__restrict__ slen,
-                                  uint32_t *__restrict__ s_info,
-                                  unsigned long long *__restrict__ s_te) {
-  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t <= n_tiles;
-       t += int64_t(gridDim.x) * blockDim.x) {
-    s_te[t] = static_cast<unsigned long long>(soff[sbase[t]]);
-    if (t == n_tiles) continue;
-    const int64_t e0 = soff[sbase[t]];
-    for (int64_t q = sbase[t]; q < sbase[t + 1]; ++q) {
-      const uint64_t rel = static_cast<uint64_t>(soff[q] - e0) / 32;
-      const uint64_t L = static_cast<uint64_t>(slen[q]) / 32;
-      s_info[q] = static_cast<uint32_t>(((rel > 0xffffu ? 0xffffu : rel) << 16) |
-                                        (L > 0xffffu ? 0xffffu : L));
-    }
-  }
-}
-
-// one thread per sorted row: its lane word and its entries
-__global__ void slice_fill_kernel(const uint32_t *__restrict__ tile_row, int64_t n_rows,
-                                  const uint64_t *__restrict__ sorted_keys,
-                                  const uint32_t *__restrict__ sorted_rows,
-                                  const int64_t *__restrict__ sbase,
-                                  const int64_t *__restrict__ soff,
-                                  const uint32_t *__restrict__ row_ptr,
-                                  const uint32_t *__restrict__ col_idx,
-                                  const double *__restrict__ vals, uint32_t *__restrict__ s_meta,
-                                  uint32_t *__restrict__ s_col, double *__restrict__ s_val) {
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n_rows;
-       i += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t t = static_cast<int64_t>(sorted_keys[i] >> 24);
-    const uint32_t r = sorted_rows[i];
-    const int64_t k = i - tile_row[t];
-    const int64_t q = sbase[t] + k / 32;
-    const int lane = static_cast<int>(k % 32);
-    const uint32_t a = row_ptr[r], len = row_ptr[r + 1] - a;
-    const uint32_t local = r - tile_row[t];
-    s_meta[q * 32 + lane] = ((local > 0xffffu ? 0xffffu : local) << 16) |
-                            (len > 0xffffu ? 0xffffu : len);
-    const int64_t e = soff[q] + lane;
-    for (uint32_t j = 0; j < len; ++j) {
-      s_col[e + static_cast<int64_t>(j) * 32] = col_idx[a + j];
-      s_val[e + static_cast<int64_t>(j) * 32] = vals[a + j];
-    }
-  }
-}
-
 // ---- tile plan -------------------------------------------------------------
 
 __device__ __forceinline__ uint32_t group_start(const uint32_t *sr_ptr,
@@ -1179,60 +935,6 @@ int launch_stream(const csrk_matrix *m, const V *vals, const V *x, V *y,
   return CSRK_OK;
 }
 
-int launch_sliced(const csrk_matrix *m, const double *x, double *y, cudaStream_t stream,
-                  int64_t t0, int64_t t1) {
-  const TilePlan &pl = m->plan;
-  const Geometry geo(static_cast<uint32_t>(pl.cap), static_cast<uint32_t>(pl.rcap),
-                     static_cast<uint32_t>(pl.stages), sizeof(double), true);
-  const size_t smem = geo.total_bytes();
-  static thread_local size_t cached_smem = 0;
-  static thread_local int cached_per_sm = 0, cached_ctas = 0, cached_device = -1;
-  int cur_dev = 0;
-  CSRK_CUDA_TRY(cudaGetDevice(&cur_dev));
-  const int ctas = pl.ctas_per_sm > 0 ? pl.ctas_per_sm : auto_ctas(pl.row_var, 8);
-  int per_sm = 0;
-  if (cached_smem == smem && cached_device == cur_dev && cached_ctas == ctas) {
-    per_sm = cached_per_sm;
-  } else {
-    CSRK_CUDA_TRY(cudaFuncSetAttribute(csrk_sliced_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem)));
-    int smem_sm = 0;
-    CSRK_CUDA_TRY(cudaDeviceGetAttribute(&smem_sm,
-                                         cudaDevAttrMaxSharedMemoryPerMultiprocessor,
-                                         cur_dev));
-    const double need = static_cast<double>(ctas) * (smem + 1024);
-    int pct = static_cast<int>(need * 100.0 / smem_sm + 0.999);
-    pct = pct < 1 ? 1 : (pct > 100 ? 100 : pct);
-    CSRK_CUDA_TRY(cudaFuncSetAttribute(csrk_sliced_kernel,
-                                       cudaFuncAttributePreferredSharedMemoryCarveout, pct));
-    CSRK_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, csrk_sliced_kernel,
-                                                                kThreads, smem));
-    if (per_sm > ctas) per_sm = ctas;
-    cached_smem = smem;
-    cached_per_sm = per_sm;
-    cached_ctas = ctas;
-    cached_device = cur_dev;
-  }
-  if (per_sm < 1) {
-    set_error("sliced kernel does not fit on an SM (%zu bytes of shared memory)", smem);
-    return CSRK_EINVAL;
-  }
-  if (t1 < 0 || t1 > pl.n_tiles) t1 = pl.n_tiles;
-  if (t0 < 0) t0 = 0;
-  const int64_t count = t1 - t0;
-  int64_t grid = static_cast<int64_t>(per_sm) * m->sm_count;
-  if (grid > count) grid = count;
-  if (grid < 1) return CSRK_OK;
-  const csrk_sliced &sl = m->sliced;
-  csrk_sliced_kernel<<<static_cast<unsigned>(grid), kThreads, smem, stream>>>(
-      m->row_ptr, m->col_idx, m->vals64, x, y, pl.tile_row + t0, sl.col, sl.val, sl.meta,
-      sl.info, sl.base + t0, sl.te + t0, static_cast<uint32_t>(count), geo.cap, geo.rcap,
-      geo.stages);
-  CSRK_CUDA_TRY(cudaGetLastError());
-  return CSRK_OK;
-}
-
 template <typename V, bool GF>
 int dispatch_main(const csrk_matrix *m, int variant, int nx, const V *vals,
                   const V *x, V *y, cudaStream_t s, int64_t t0, int64_t t1);
@@ -1279,6 +981,8 @@ int dispatch_long(const csrk_matrix *m, int variant, int nx, const V *vals, cons
 // Power-law, 2 M rows, max row 20 k, queued -> beside: serial 503 -> 397 us,
 // nx = 4 447 -> 335, nx = 32 654 -> 560 (profiles/r01_powerlaw_probe.txt).
 // CSRK_LONG_SERIAL=1 queues it behind the streaming kernel instead.
+constexpr size_t kMaxSides = 8;
+
 template <typename V, bool GF>
 int dispatch_nx(const csrk_matrix *m, int variant, int nx, const V *vals,
                 const V *x, V *y, cudaStream_t s, int64_t t0, int64_t t1) {
@@ -1287,14 +991,34 @@ int dispatch_nx(const csrk_matrix *m, int variant, int nx, const V *vals,
     if (rc != CSRK_OK) return rc;
     return dispatch_long<V>(m, variant, nx, vals, x, y, s, t0, t1);
   }
-  // (side stream and events created with the long-row list, ensure_plan)
-  CSRK_CUDA_TRY(cudaEventRecord(m->long_fork, s));
-  CSRK_CUDA_TRY(cudaStreamWaitEvent(m->long_stream, m->long_fork, 0));
+  // the caller stream's own side stream (created on first use; the caller
+  // holds the matrix lock); past kMaxSides distinct caller streams the
+  // long-row kernel queues on the caller's stream instead
+  csrk_matrix *mm = const_cast<csrk_matrix *>(m);
+  csrk_matrix::Side *sd = nullptr;
+  for (auto &c : mm->sides)
+    if (c.caller == s) sd = &c;
+  if (!sd && mm->sides.size() < kMaxSides) {
+    csrk_matrix::Side c;
+    c.caller = s;
+    CSRK_CUDA_TRY(cudaStreamCreateWithFlags(&c.side, cudaStreamNonBlocking));
+    CSRK_CUDA_TRY(cudaEventCreateWithFlags(&c.fork, cudaEventDisableTiming));
+    CSRK_CUDA_TRY(cudaEventCreateWithFlags(&c.join, cudaEventDisableTiming));
+    mm->sides.push_back(c);
+    sd = &mm->sides.back();
+  }
+  if (!sd) {
+    const int rc = dispatch_main<V, GF>(m, variant, nx, vals, x, y, s, t0, t1);
+    if (rc != CSRK_OK) return rc;
+    return dispatch_long<V>(m, variant, nx, vals, x, y, s, t0, t1);
+  }
+  CSRK_CUDA_TRY(cudaEventRecord(sd->fork, s));
+  CSRK_CUDA_TRY(cudaStreamWaitEvent(sd->side, sd->fork, 0));
   int rc = dispatch_main<V, GF>(m, variant, nx, vals, x, y, s, t0, t1);
   if (rc == CSRK_OK)
-    rc = dispatch_long<V>(m, variant, nx, vals, x, y, m->long_stream, t0, t1);
-  CSRK_CUDA_TRY(cudaEventRecord(m->long_join, m->long_stream));
-  CSRK_CUDA_TRY(cudaStreamWaitEvent(s, m->long_join, 0));
+    rc = dispatch_long<V>(m, variant, nx, vals, x, y, sd->side, t0, t1);
+  CSRK_CUDA_TRY(cudaEventRecord(sd->join, sd->side));
+  CSRK_CUDA_TRY(cudaStreamWaitEvent(s, sd->join, 0));
   return rc;
 }
 
@@ -1446,7 +1170,7 @@ int recut_long(csrk_matrix *m, int64_t tile_cost, int64_t cap, int64_t rcap,
 }  // namespace
 
 int ensure_plan(csrk_matrix *m, int64_t tile_cost, int64_t cap, int64_t stages,
-                cudaStream_t s) {
+                cudaStream_t s, bool force) {
   if (tile_cost <= 0) tile_cost = kDefaultTileCost;
   if (tile_cost < 32) tile_cost = 32;
   if (tile_cost > 65536) tile_cost = 65536;
@@ -1469,7 +1193,7 @@ int ensure_plan(csrk_matrix *m, int64_t tile_cost, int64_t cap, int64_t stages,
               geo.total_bytes());
     return CSRK_EINVAL;
   }
-  if (m->plan.tile_row && m->plan.tile_cost == tile_cost && m->plan.cap == cap &&
+  if (!force && m->plan.tile_row && m->plan.tile_cost == tile_cost && m->plan.cap == cap &&
       m->plan.rcap == rcap && m->plan.stages == stages)
     return CSRK_OK;
   if (m->sm_count == 0) {
@@ -1507,11 +1231,6 @@ int ensure_plan(csrk_matrix *m, int64_t tile_cost, int64_t cap, int64_t stages,
       const int64_t n = static_cast<int64_t>(hn);
       CSRK_CUDA_TRY(cudaMalloc(&m->plan.long_rows, (4 * n + 1) * sizeof(uint32_t)));
       m->plan.n_long = n;
-      if (!m->long_stream) {  // the long-row kernel's side stream (dispatch_nx)
-        CSRK_CUDA_TRY(cudaStreamCreateWithFlags(&m->long_stream, cudaStreamNonBlocking));
-        CSRK_CUDA_TRY(cudaEventCreateWithFlags(&m->long_fork, cudaEventDisableTiming));
-        CSRK_CUDA_TRY(cudaEventCreateWithFlags(&m->long_join, cudaEventDisableTiming));
-      }
       CSRK_CUDA_TRY(cudaMemsetAsync(dn, 0, sizeof(hn), s));
       long_rows_list_kernel<<<148 * 8, 256, 0, s>>>(m->row_ptr, m->n_rows,
                                                      static_cast<uint32_t>(kLongRow),
@@ -1584,7 +1303,8 @@ int ensure_plan(csrk_matrix *m, int64_t tile_cost, int64_t cap, int64_t stages,
     // (natural-order 7-point 256^3 with 64-row SSRs: 6.27 TB/s aligned,
     // 6.71 TB/s cut on rows, profiles/r01_sched_sweep.txt), so large groups
     // are cut on rows -- results do not depend on the cuts.
-    if (static_cast<int64_t>(h) * 8 <= tile_cost) {
+    const int mode = m->plan.cut_mode;
+    if (mode == 2 || (mode == 0 && static_cast<int64_t>(h) * 8 <= tile_cost)) {
       cut_k = m->k;
       n_cuts = n_groups;
       max_group = static_cast<int64_t>(h);
@@ -1595,7 +1315,10 @@ int ensure_plan(csrk_matrix *m, int64_t tile_cost, int64_t cap, int64_t stages,
   // Group cuts use pitch = tile_cost - largest group: every tile then fits
   // the stage.  Row cuts keep pitch = tile_cost; the stage's slack
   // (cap - tile_cost) covers the row that crosses a boundary.
-  const int64_t pitch = cut_k == 1 ? tile_cost : tile_cost - max_group;
+  // (a group larger than the tile: one group per tile, direct mode when it
+  // exceeds the stage -- reachable only with cut mode 2)
+  const int64_t pitch =
+      cut_k == 1 ? tile_cost : std::max<int64_t>(tile_cost - max_group, 1);
   const int64_t total_cost = m->nnz + m->n_rows;
   int64_t n_tiles = (total_cost + pitch - 1) / pitch;
   if (n_tiles > 0x7fffffffLL) {
@@ -1629,7 +1352,7 @@ int ensure_plan(csrk_matrix *m, int64_t tile_cost, int64_t cap, int64_t stages,
         m->plan.n_long, m->plan.tile_long);
   CSRK_CUDA_TRY(cudaGetLastError());
   m->pipe.plan_tiles = -1;  // host-pipeline cuts index the old tiles
-  ++m->plan.gen;            // and the sliced copy belongs to the old plan
+  ++m->plan.gen;
   m->plan.tile_cost = tile_cost;
   m->plan.cap = cap;
   m->plan.rcap = rcap;
@@ -1639,110 +1362,11 @@ int ensure_plan(csrk_matrix *m, int64_t tile_cost, int64_t cap, int64_t stages,
   return CSRK_OK;
 }
 
-void free_sliced(csrk_matrix *m) {
-  csrk_sliced &sl = m->sliced;
-  cudaFree(sl.col);
-  cudaFree(sl.val);
-  cudaFree(sl.meta);
-  cudaFree(sl.info);
-  cudaFree(sl.base);
-  cudaFree(sl.te);
-  sl = csrk_sliced();
-}
-
-bool sliced_wanted(const csrk_matrix *m, int value_type, int variant) {
-  if (value_type != CSRK_F64 || variant != CSRK_SERIAL || m->n_rows == 0) return false;
-  return m->plan.layout == 1 && m->plan.row_stats && m->plan.cap <= 65535;
-}
-
-namespace {
-template <typename T>
-struct TmpBuf {
-  T *p = nullptr;
-  cudaStream_t s;
-  explicit TmpBuf(cudaStream_t st) : s(st) {}
-  ~TmpBuf() {
-    if (p) cudaFreeAsync(p, s);
-  }
-  cudaError_t alloc(int64_t n) {
-    keep_async_pool();
-    return cudaMallocAsync(&p, (n > 0 ? n : 1) * sizeof(T), s);
-  }
-};
-inline unsigned grid_of(int64_t n) {
-  int64_t b = (n + 255) / 256;
-  return static_cast<unsigned>(b < 1 ? 1 : (b > 148 * 32 ? 148 * 32 : b));
-}
-}  // namespace
-
-int ensure_sliced(csrk_matrix *m, cudaStream_t s) {
-  if (m->sliced.gen == m->plan.gen && m->sliced.col) return CSRK_OK;
-  free_sliced(m);
-  const int64_t n = m->n_rows, nt = m->plan.n_tiles;
-  TmpBuf<uint64_t> keys(s), tkeys(s);
-  TmpBuf<uint32_t> rows(s), trows(s);
-  TmpBuf<int64_t> ns(s), sbase(s);
-  CSRK_CUDA_TRY(keys.alloc(n));
-  CSRK_CUDA_TRY(tkeys.alloc(n));
-  CSRK_CUDA_TRY(rows.alloc(n));
-  CSRK_CUDA_TRY(trows.alloc(n));
-  CSRK_CUDA_TRY(ns.alloc(nt));
-  CSRK_CUDA_TRY(sbase.alloc(nt + 1));
-  tile_of_row_kernel<<<grid_of(nt), 256, 0, s>>>(m->plan.tile_row, nt, m->row_ptr, keys.p,
-                                                 rows.p);
-  int tb = 1;
-  while ((int64_t(1) << tb) <= nt) ++tb;
-  CSRK_TRY(radix_sort_pairs(keys.p, rows.p, tkeys.p, trows.p, n, 0, ((24 + tb + 7) / 8) * 8,
-                            s));
-  slice_count_kernel<<<grid_of(nt), 256, 0, s>>>(m->plan.tile_row, nt, ns.p);
-  CSRK_TRY(exclusive_scan_i64(ns.p, nt, sbase.p, s));
-  int64_t n_slices = 0;
-  CSRK_CUDA_TRY(cudaMemcpyAsync(&n_slices, sbase.p + nt, sizeof(n_slices),
-                                cudaMemcpyDeviceToHost, s));
-  CSRK_CUDA_TRY(cudaStreamSynchronize(s));
-  TmpBuf<int64_t> slen(s), soff(s);
-  CSRK_CUDA_TRY(slen.alloc(n_slices));
-  CSRK_CUDA_TRY(soff.alloc(n_slices + 1));
-  csrk_sliced &sl = m->sliced;
-  CSRK_CUDA_TRY(cudaMalloc(&sl.base, (nt + 1) * sizeof(uint32_t)));
-  CSRK_CUDA_TRY(cudaMalloc(&sl.te, (nt + 1) * sizeof(unsigned long long)));
-  slice_len_kernel<<<grid_of(nt + 1), 256, 0, s>>>(m->plan.tile_row, nt, sbase.p, rows.p,
-                                                   m->row_ptr, slen.p, sl.base);
-  CSRK_TRY(exclusive_scan_i64(slen.p, n_slices, soff.p, s));
-  int64_t entries = 0;
-  CSRK_CUDA_TRY(cudaMemcpyAsync(&entries, soff.p + n_slices, sizeof(entries),
-                                cudaMemcpyDeviceToHost, s));
-  CSRK_CUDA_TRY(cudaStreamSynchronize(s));
-  // (+64: the TMA copies of a tile's slice descriptors over-read to 16 B)
-  CSRK_CUDA_TRY(cudaMalloc(&sl.col, (entries + 64) * sizeof(uint32_t)));
-  CSRK_CUDA_TRY(cudaMalloc(&sl.val, (entries + 64) * sizeof(double)));
-  CSRK_CUDA_TRY(cudaMalloc(&sl.meta, (n_slices * 32 + 64) * sizeof(uint32_t)));
-  CSRK_CUDA_TRY(cudaMalloc(&sl.info, (n_slices + 64) * sizeof(uint32_t)));
-  CSRK_CUDA_TRY(cudaMemsetAsync(sl.col, 0, (entries + 64) * sizeof(uint32_t), s));
-  CSRK_CUDA_TRY(cudaMemsetAsync(sl.val, 0, (entries + 64) * sizeof(double), s));
-  CSRK_CUDA_TRY(cudaMemsetAsync(sl.meta, 0xff, (n_slices * 32 + 64) * sizeof(uint32_t), s));
-  CSRK_CUDA_TRY(cudaMemsetAsync(sl.info, 0, (n_slices + 64) * sizeof(uint32_t), s));
-  slice_info_kernel<<<grid_of(nt + 1), 256, 0, s>>>(m->plan.tile_row, nt, sbase.p, soff.p,
-                                                    slen.p, sl.info, sl.te);
-  slice_fill_kernel<<<grid_of(n), 256, 0, s>>>(m->plan.tile_row, n, keys.p, rows.p, sbase.p,
-                                               soff.p, m->row_ptr, m->col_idx, m->vals64,
-                                               sl.meta, sl.col, sl.val);
-  CSRK_CUDA_TRY(cudaGetLastError());
-  CSRK_CUDA_TRY(cudaStreamSynchronize(s));
-  sl.n_slices = n_slices;
-  sl.entries = entries;
-  sl.gen = m->plan.gen;
-  return CSRK_OK;
-}
-
 int prepare_plan(const csrk_matrix *cm, int value_type, int variant, int nx) {
   csrk_matrix *m = const_cast<csrk_matrix *>(cm);  // the plan is a cache
   if (m->n_rows == 0) return CSRK_OK;
   if (!m->plan.row_stats) CSRK_TRY(ensure_plan(m, 0, 0, 0, m->stream));
-  if (!m->plan.auto_tile) {
-    if (sliced_wanted(m, value_type, variant)) CSRK_TRY(ensure_sliced(m, m->stream));
-    return CSRK_OK;
-  }
+  if (!m->plan.auto_tile) return CSRK_OK;
   const int64_t tc = auto_tile_cost(m->plan.mean_short, variant, nx);
   if (tc != m->plan.tile_cost) {
     const bool keep = m->plan.auto_tile;
@@ -1750,7 +1374,6 @@ int prepare_plan(const csrk_matrix *cm, int value_type, int variant, int nx) {
     m->plan.auto_tile = keep;
     CSRK_CUDA_TRY(cudaStreamSynchronize(m->stream));
   }
-  if (sliced_wanted(m, value_type, variant)) CSRK_TRY(ensure_sliced(m, m->stream));
   return CSRK_OK;
 }
 
@@ -1779,10 +1402,6 @@ int launch_spmv(const csrk_matrix *m, int value_type, int variant, int nx,
       set_error("matrix holds no float64 values");
       return CSRK_EINVAL;
     }
-    if (variant == CSRK_SERIAL && m->sliced.col && m->sliced.gen == m->plan.gen &&
-        sliced_wanted(m, value_type, variant))
-      return launch_sliced(m, static_cast<const double *>(x), static_cast<double *>(y),
-                           stream, t0, t1);
     const int g = m->plan.gather_first;
     if (g == 1 || (g == kGatherAuto && auto_gather(variant, nx, m->plan.mean_row, m->plan.row_var)))
       return dispatch_nx<double, true>(m, variant, nx, m->vals64,

@@ -42,6 +42,8 @@ __all__ = [
     "emulate_gpu_spmv35",
     "spmv_gpu35",
     "spmv_device",
+    "check_device_vector",
+    "host_row_sums",
     "STRIDED_NX",
 ]
 
@@ -105,12 +107,48 @@ def _check_x(a: CsrMatrix, x) -> np.ndarray:
     return x
 
 
+def host_row_sums(row_ptr, col_idx, vals, x) -> np.ndarray:
+    """Rows summed strictly left to right on the host, numpy: the product
+    ``vals[p] * x[col[p]]`` and each ``acc + prod`` rounded separately, as
+    the reference's sequential oracle (kernels.py:97-114) does one Python
+    float at a time.  Rows are visited longest first so that step j adds
+    entry j of a prefix of the rows (one vectorised add per column
+    position, total work nnz)."""
+    rp = np.asarray(row_ptr, dtype=np.int64)
+    n = rp.shape[0] - 1
+    y = np.zeros(n, dtype=VALUE_DTYPE)
+    if n == 0 or rp[-1] == 0:
+        return y
+    prods = np.asarray(vals, dtype=VALUE_DTYPE) * x[np.asarray(col_idx, dtype=np.int64)]
+    lens = np.diff(rp)
+    order = np.argsort(-lens, kind="stable")
+    starts = rp[:-1][order]
+    sl = lens[order]
+    acc = np.zeros(n, dtype=VALUE_DTYPE)
+    active = n
+    for j in range(int(sl[0])):
+        while active > 0 and sl[active - 1] <= j:
+            active -= 1
+        acc[:active] += prods[starts[:active] + j]
+    y[order] = acc
+    return y
+
+
 def spmv_csr_ref(a: CsrMatrix, x, *, out=None) -> np.ndarray:
-    """Plain CSR y = A x, rows summed left to right (kernels.py:97-114)."""
+    """Plain CSR y = A x, rows summed left to right (kernels.py:97-114).
+
+    The reference keeps this as its sequential host oracle, and so does this
+    package: it runs on the host (numpy, bitwise the
+    reference's per-row chain) and is what run_benchmark / the CLI verify
+    the device kernels against.  It is not a fallback of any device path --
+    spmv_csr2 / spmv_csr3 / spmv_gpu35 / spmv_device only run the CUDA
+    library.  The device k = 1 kernel is ``spmv_device(a, x)``."""
     x = _check_x(a, x)
-    if a.n_rows == 0:
-        return np.zeros(0, dtype=VALUE_DTYPE)
-    return a.device().spmv_host(x, out=out)
+    y = host_row_sums(a.row_ptr, a.col_idx, a.vals, x)
+    if out is not None:
+        out[:] = y
+        return out
+    return y
 
 
 def spmv_csr2(m: CsrKMatrix, x, workers: int = 1, executor=None, *,
@@ -191,6 +229,24 @@ def emulate_gpu_spmv35(m: CsrKMatrix, x, dims: BlockDims) -> tuple:
     return _listing(m, x, dims, 4)
 
 
+def check_device_vector(t, dev, length: int, name: str, dtype=None) -> None:
+    """Raise ValueError unless ``t`` is a contiguous 1-D CUDA tensor on the
+    matrix's device with ``length`` elements (and ``dtype`` when given):
+    the kernels take raw device pointers, so a host tensor, another GPU's
+    tensor, a short or a mistyped vector would be read or written out of
+    bounds."""
+    if not getattr(t, "is_cuda", False):
+        raise ValueError(f"{name} must be a CUDA tensor")
+    if t.device.index != dev.device:
+        raise ValueError(f"{name} is on cuda:{t.device.index}, the matrix on cuda:{dev.device}")
+    if dtype is not None and t.dtype != dtype:
+        raise ValueError(f"{name} must be {dtype}, got {t.dtype}")
+    if t.dim() != 1 or t.shape[0] != length:
+        raise ValueError(f"{name} must have length {length}, got {tuple(t.shape)}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+
+
 def spmv_device(m, x, y=None, *, dims: BlockDims | None = None, variant: str = "serial",
                 stream=None):
     """Device-resident SpMV on torch CUDA tensors (float64 or float32).
@@ -205,13 +261,14 @@ def spmv_device(m, x, y=None, *, dims: BlockDims | None = None, variant: str = "
 
     base = m.base if isinstance(m, CsrKMatrix) else m
     dev = m if isinstance(m, nat.DeviceMatrix) else m.device()
-    f32 = x.dtype == torch.float32
     if x.dtype not in (torch.float32, torch.float64):
         raise ValueError("x must be float32 or float64")
-    if x.dim() != 1 or x.shape[0] != base.n_cols or not x.is_contiguous():
-        raise ValueError(f"x must have length {base.n_cols}, got {tuple(x.shape)}")
+    f32 = x.dtype == torch.float32
+    check_device_vector(x, dev, base.n_cols, "x")
     if y is None:
         y = torch.empty(base.n_rows, dtype=x.dtype, device=x.device)
+    else:
+        check_device_vector(y, dev, base.n_rows, "y", dtype=x.dtype)
     if f32:
         dev.ensure_f32()
     nx = 1

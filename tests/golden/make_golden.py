@@ -7,6 +7,8 @@ the committed files this script writes):
     python tests/golden/make_golden.py small      # ~1 min  -> small_cases.npz
     python tests/golden/make_golden.py medium     # ~2 min  -> configs.json
     python tests/golden/make_golden.py large      # ~20 min -> configs.json
+    python tests/golden/make_golden.py b200 [C2 C3 C5 C1]   # adds runs at the
+                                                  # B200 profile's targets
 
 ``small`` stores full arrays for many small matrices (the shapes of the
 reference's own sweep, pkg/tests/test_acceptance.py:86-154, plus the kernel
@@ -242,7 +244,8 @@ def run_config(name, spec, targets_list, emu=False, csr_ref=True):
         y_ref = ref.spmv_csr_ref(a, x)
         rec["y_ref"] = digest(y_ref, "<f8")
     rec["runs"] = []
-    for targets in targets_list:
+    for entry in targets_list:
+        targets, emu_dims = (entry if isinstance(entry, tuple) else (entry, None))
         t1 = time.time()
         res = ref.band_k(a, 3, targets)
         t_band = time.time() - t1
@@ -270,10 +273,14 @@ def run_config(name, spec, targets_list, emu=False, csr_ref=True):
         run["y_csr3_unpermuted"] = digest(yu, "<f8")
         if csr_ref:
             run["max_rel_error_vs_ref"] = ref.max_rel_error(yu, y_ref)
-        if emu:
-            dims = ref.BlockDims(4, 8, 12)
+        if emu or emu_dims:
+            d = emu_dims or (4, 8, 12)
+            dims = ref.BlockDims(*d)
+            t2 = time.time()
             y35, _ = ref.emulate_gpu_spmv35(m, xp, dims)
-            run["y_emu35_4x8x12"] = digest(y35, "<f8")
+            run["y_emu35_%dx%dx%d" % tuple(d)] = digest(y35, "<f8")
+            run["emu35_seconds"] = round(time.time() - t2, 1)
+            del y35
         rec["runs"].append(run)
         print(f"  {name} targets {targets}: band_k {t_band:.1f}s", flush=True)
     rec["seconds"] = round(time.time() - t0, 1)
@@ -294,6 +301,43 @@ LARGE = {
     "C3": ({"kind": "stencil", "shape": [192, 192, 192], "points": 27}, [[10, 20]], False),
     "C5": ({"kind": "irregular", "rows": 5_000_000}, [[14, 9]], False),
 }
+
+
+# The B200 profile's picks (paper_2203_05096_b200/data/b200.json through
+# tune_gpu) for the benchmarked configs: band_k targets [srs, ssrs] and, for
+# the strided order, the block dims whose x lanes the streaming kernel uses.
+# C1 [9, 13] dims 2x12x1 (cuda3); C2 [8, 12] 2x12x1 (cuda3); C3 [5, 10]
+# 4x8x8 (cuda35); C5 [7, 11] 4x8x12 (cuda3; its strided order pinned too).
+B200 = {
+    "C1": ({"kind": "stencil", "shape": [1000, 1000], "points": 5}, [([9, 13], (4, 8, 12))]),
+    "C2": ({"kind": "stencil", "shape": [256, 256, 256], "points": 7}, [([8, 12], (8, 8, 8))]),
+    "C3": ({"kind": "stencil", "shape": [192, 192, 192], "points": 27}, [([5, 10], (4, 8, 8))]),
+    "C5": ({"kind": "irregular", "rows": 5_000_000}, [([7, 11], (4, 8, 12))]),
+}
+
+
+def add_b200_runs():
+    """Append runs at the B200 profile's targets to the existing entries of
+    configs.json (the input / stats digests are already there)."""
+    path = os.path.join(HERE, "configs.json")
+    with open(path) as fh:
+        data = json.load(fh)
+    only = sys.argv[2:]
+    for name, (spec, runs) in B200.items():
+        if only and name not in only:
+            continue
+        print(f"{name} (b200 targets) ...", flush=True)
+        rec = run_config(name, spec, runs, emu=False, csr_ref=False)
+        old = data.setdefault(name, rec)
+        if old is not rec:
+            if old["input"] != rec["input"]:
+                raise SystemExit(f"{name}: input digests changed")
+            have = {tuple(r["targets"]) for r in old["runs"]}
+            old["runs"] += [r for r in rec["runs"] if tuple(r["targets"]) not in have]
+        with open(path, "w") as fh:
+            json.dump(data, fh, indent=1, sort_keys=True)
+            fh.write("\n")
+    print(f"wrote {path}")
 
 
 def configs(which):
@@ -322,5 +366,7 @@ if __name__ == "__main__":
         small()
     elif mode in ("medium", "large"):
         configs(mode)
+    elif mode == "b200":
+        add_b200_runs()
     else:
         raise SystemExit(f"unknown mode {mode}")

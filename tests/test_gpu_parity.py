@@ -475,15 +475,15 @@ def test_auto_plan_follows_the_order():
     assert dev.plan()["tile_cost"] == 1000
 
 
-@pytest.mark.parametrize("layout", [0, 1])
+@pytest.mark.parametrize("cut_mode", [0, 1, 2])
 @pytest.mark.parametrize("kind", ["mixed", "stencil", "irregular", "empty_rows"])
-def test_sliced_layout_bitwise(layout, kind):
-    """Serial f64 launches through the sliced tiles (SELL-32 per tile, rows
-    sorted by length) equal the reference's row order bit for bit, under
-    several plans (staged and direct tiles), for whole launches, tile ranges
-    and the pinned host pipeline."""
+def test_cut_modes_bitwise(cut_mode, kind):
+    """Tile cuts on rows, on super-super-row boundaries (the paper's SSR ->
+    block mapping) or auto give the reference's row order bit for bit, under
+    several plans (staged and direct tiles), for whole launches and tile
+    ranges; group cuts fall only on SSR starts."""
     torch = pytest.importorskip("torch")
-    rng = np.random.default_rng(len(kind) + layout)
+    rng = np.random.default_rng(len(kind) + cut_mode)
     if kind == "mixed":
         a = _mixed_rows_matrix(rng, 20000)
     elif kind == "stencil":
@@ -505,13 +505,17 @@ def test_sliced_layout_bitwise(layout, kind):
     x = rng.uniform(-1.0, 1.0, b.n_rows)
     want = O.spmv_serial(b.row_ptr, b.col_idx, b.vals, x)
     dev = m.device()
-    dev.set_layout(layout)
+    dev.set_cut_mode(cut_mode)
     xd = torch.from_numpy(x).cuda()
+    ssr_rows = set((m.sr_ptr.astype(np.int64)[m.ssr_ptr.astype(np.int64)]).tolist())
     for tile_cost, stages in ((0, 0), (256, 3), (4096, 2), (48, 1)):
         dev.set_plan(tile_cost, 0, stages)
         np.testing.assert_array_equal(ck.spmv_csr3(m, x), want)
         plan = dev.plan()
-        assert plan["sliced"] == int(layout == 1)
+        assert plan["cut_mode"] == cut_mode
+        if cut_mode == 2 and plan["n_long"] == 0:
+            assert plan["group_aligned"] == 1
+            assert set(dev.tile_rows().tolist()) <= ssr_rows
         yd = torch.full_like(xd, float("nan"))
         nt = plan["n_tiles"]
         cut = nt // 3
@@ -522,8 +526,8 @@ def test_sliced_layout_bitwise(layout, kind):
         np.testing.assert_array_equal(yd.cpu().numpy(), want)
 
 
-def test_tile_range_and_layout_argument_checks():
-    """The C-ABI rejects bad tile ranges and layouts with ValueError."""
+def test_tile_range_and_cut_mode_argument_checks():
+    """The C-ABI rejects bad tile ranges and cut modes with ValueError."""
     torch = pytest.importorskip("torch")
     rng = np.random.default_rng(12)
     a = random_csr(rng, 2000, 2000, 0.004)
@@ -538,7 +542,7 @@ def test_tile_range_and_layout_argument_checks():
     with pytest.raises(ValueError, match="tile range"):
         dev.spmv_tiles_ptr(x.data_ptr(), y.data_ptr(), 3, 2, s)
     dev.spmv_tiles_ptr(x.data_ptr(), y.data_ptr(), 2, 2, s)  # empty range: no-op
-    with pytest.raises(ValueError, match="layout"):
-        dev.set_layout(2)
+    with pytest.raises(ValueError, match="cut mode"):
+        dev.set_cut_mode(3)
     tr = dev.tile_rows()
     assert tr[0] == 0 and tr[-1] == 2000 and len(tr) == nt + 1 and np.all(np.diff(tr) >= 0)

@@ -19,7 +19,7 @@ reps = int(sys.argv[6]) if len(sys.argv) > 6 else 5
 dev = m.device()
 dev.set_plan(tc, 0, st)
 dev.set_schedule(g, CTAS)
-dev.set_layout(int(os.environ.get("LAYOUT", "0")))
+dev.set_cut_mode(int(os.environ.get("CUT", "0")))
 xd = torch.from_numpy(xp).cuda()
 yd = torch.empty_like(xd)
 for _ in range(reps):

@@ -80,12 +80,12 @@ def main():
                     dims = ck.BlockDims(int(k), 1, 1)
                 dev.set_plan(0, 0, 0)
                 dev.set_schedule(0, 0)
-                dev.set_layout(0)
+                dev.set_cut_mode(0)
                 want = ck.spmv_device(m, xd, yd, dims=dims, variant=variant_i).clone()
                 for g, CTAS, LAY in [(g, c, la) for g in (GATHER if vb == 8 else (0,))
                                      for c in CTAS_LIST for la in LAYOUTS]:
                   dev.set_schedule(g, CTAS)
-                  dev.set_layout(LAY)
+                  dev.set_cut_mode(LAY)
                   for t in TILES:
                     for s in STAGES:
                         try:
@@ -98,13 +98,13 @@ def main():
                         gbs = spmv_bytes(n, n, nnz, vb) / (ms * 1e-3) / 1e9
                         rec = {"config": cfg, "dtype": str(dtype)[6:], "variant": variant_i,
                                "nx": dims.x if variant_i == "strided" else 0,
-                               "gather": g, "ctas": CTAS, "layout": LAY, "tile_cost": t, "stages": s, "ms": round(ms, 4),
+                               "gather": g, "ctas": CTAS, "cut_mode": LAY, "tile_cost": t, "stages": s, "ms": round(ms, 4),
                                "gbs": round(gbs, 1), "bitwise_equal": same}
                         print(json.dumps(rec), flush=True)
                         out.append(rec)
             dev.set_plan(0, 0, 0)
             dev.set_schedule(2, 0)
-            dev.set_layout(0)
+            dev.set_cut_mode(0)
         del m, dev
         torch.cuda.empty_cache()
     os.makedirs("gpurun_out", exist_ok=True)

@@ -19,8 +19,8 @@ xd = torch.from_numpy(xp).cuda()
 yd = torch.empty_like(xd)
 byts = spmv_bytes(a.n_rows, a.n_rows, a.nnz, 8)
 for rep in range(2):
-    for layout in (0, 1):
-        dev.set_layout(layout)
+    for layout in (0, 1):  # cut mode: auto, rows
+        dev.set_cut_mode(layout)
         ck.spmv_device(m, xd, yd)
         torch.cuda.synchronize()
         with bench.ClockSampler(0) as clk:
