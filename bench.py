@@ -19,14 +19,23 @@ no flush is needed between steps.
              HBM copy bandwidth (MEASURED_PEAKS.json)
   cpu_baseline  the reference's CSR-3 algorithm restated in C + OpenMP
              (oracle/, kind "port"), all host cores, bounded sample
+  parity     the timed launch's y against the oracle: bitwise in fp64,
+             1e-5 of |A||x| in fp32 (the run fails otherwise)
 
-N > 1 (torchrun, one process per GPU): the matrix's super-super-rows are
-split across ranks by nonzeros (paper_2203_05096_b200.dist) and each step
-exchanges the x halo over NCCL before the local SpMV (strong scaling).
+N > 1 (one process per GPU; `--gpus N` without torchrun re-launches itself
+under torch.distributed.run): the SAME matrix as the N = 1 line, its
+super-super-rows split across ranks by nonzeros (paper_2203_05096_b200.dist
+DistSpMV), each rank holding its rows and a footprint-sized x; every step
+posts the x halo over NCCL, computes the interior tiles while it is in
+flight, then the boundary tiles (strong scaling; rank 0 also times the whole
+matrix on one GPU and prints T1 / (N T_N)).  --config C4: the CG loop on
+z-slabs.
 
-``--impl reference`` times the reference's CPU CSR-3 algorithm (the oracle
-port; the Python reference cannot be shipped to the GPU box) on the host
-cores for the same config and prints the same JSON line.
+``--impl reference`` times the UNMODIFIED reference package (baseline/_ref,
+pip-installed from /root/reference/pkg): its own spmv_csr3 with
+workers=os.cpu_count() on the CSR-k matrix its own band_k / pack_csrk built
+(same config, same B200-model group sizes), on the host cores; no module of
+this repo's package and none of its .so files are loaded on that arm.
 """
 
 from __future__ import annotations
@@ -182,6 +191,38 @@ def cpu_baseline(m, xp, budget_s=10.0, threads=None):
                       f"over super-super-rows), mean {mean * 1e3:.1f} ms"}, y
 
 
+def oracle_y(m, xp, variant, nx, threads=None):
+    """The oracle's y for the timed order (test infrastructure: the checker
+    of the bench's own output, never the thing measured)."""
+    from oracle import oracle as O
+
+    b = m.base
+    if variant == "strided":
+        return O.spmv_strided(b.row_ptr, b.col_idx, b.vals, xp, nx)
+    rows = O.csr3_group_rows(m.sr_ptr, m.ssr_ptr)
+    return O.spmv_grouped(rows, b.row_ptr, b.col_idx, b.vals, xp, threads or os.cpu_count())
+
+
+def parity_of(y_dev, want, m, xp, f32):
+    """Bitwise for fp64; for fp32 |y - y64| <= 1e-5 (|A||x|)_i per row
+    (north_star's tolerance)."""
+    from oracle import oracle as O
+
+    y_dev = np.asarray(y_dev, dtype=np.float64)
+    diff = np.abs(y_dev - want)
+    if not f32:
+        ok = bool(np.array_equal(y_dev, want))
+        return {"kind": "bitwise", "ok": ok, "max_abs_diff": float(diff.max()) if diff.size else 0.0,
+                "against": "oracle/csrk_oracle.c (pinned to the reference's goldens) on the "
+                           "same CSR-k matrix and x"}
+    b = m.base
+    scale = O.abs_row_dot(b.row_ptr, b.col_idx, b.vals, xp)
+    worst = float(np.max(diff / np.maximum(scale, 1e-300))) if diff.size else 0.0
+    return {"kind": "scaled", "tolerance": 1e-5, "ok": bool(worst <= 1e-5),
+            "max_scaled_error": worst,
+            "against": "oracle/csrk_oracle.c fp64 y on the same CSR-k matrix and x"}
+
+
 def run_ours(args, log):
     import torch
 
@@ -191,7 +232,8 @@ def run_ours(args, log):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if world > 1 or (os.environ.get("CSRK_DIST") == "1" and "RANK" in os.environ):
         from paper_2203_05096_b200 import dist
-        return dist.bench_main(args, log, sampler=ClockSampler, peak=measured_peak())
+        return dist.bench_main(args, log, sampler=ClockSampler, peak=measured_peak(),
+                               oracle_check=oracle_y)
     torch.cuda.set_device(0)
     a, m, xp, params, build_t = build_matrix(args.config, log)
     n, nnz = a.n_rows, a.nnz
@@ -268,7 +310,14 @@ def run_ours(args, log):
     if not f32:
         assert np.array_equal(y_dev, y_pin), "device-resident and host-path y differ"
 
-    base, _ = cpu_baseline(m, xp, budget_s=args.cpu_budget)
+    base, y_base = cpu_baseline(m, xp, budget_s=args.cpu_budget)
+    # parity of the TIMED output: the device-resident y of the last timed
+    # launch against the oracle (the cpu_baseline's own y for the serial
+    # order, the strided restatement otherwise)
+    want = y_base if variant == "serial" else oracle_y(m, xp, variant, dims.x)
+    parity = parity_of(y_dev, want, m, xp, f32)
+    if not parity["ok"]:
+        raise SystemExit(f"parity check failed: {parity}")
     key = f"{args.config}_{'f32' if f32 else 'f64'}"
     line = {
         "metric": METRIC,
@@ -309,7 +358,8 @@ def run_ours(args, log):
                 "ms_per_step": round(e2e_s * 1e3, 3),
                 "call": call_text},
         "cpu_baseline": base,
-        "gpu_launches": args.steps,
+        "parity": parity,
+        "gpu_launches": args.steps * (2 if m.device().plan()["n_long"] > 0 else 1),
         "clocks": clk.summary(),
         "build_seconds": {k: round(v, 2) for k, v in build_t.items()},
     }
@@ -583,6 +633,21 @@ def run_reference(args, log):
     }
 
 
+def _relaunch_torchrun(n: int, argv) -> None:
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={n}", "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.abspath(__file__), *argv]
+    print(f"[bench] --gpus {n}: " + " ".join(cmd), file=sys.stderr, flush=True)
+    rc = subprocess.run(cmd).returncode
+    if rc:
+        raise SystemExit(rc)
+
+
 def main(argv=None):
     ap = argparse.ArgumentParser(description=__doc__.split("\n")[1])
     ap.add_argument("--gpus", type=int, default=1)
@@ -596,7 +661,20 @@ def main(argv=None):
     ap.add_argument("--side", type=int, default=512, help="C4: grid side")
     ap.add_argument("--fp32", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=10.0)
+    ap.add_argument("--exchange", choices=("halo", "allgather"), default=None,
+                    help="N > 1: x exchange (default halo; allgather = the literal "
+                         "north-star collective)")
+    ap.add_argument("--partition", choices=("blocks", "slab"), default="blocks",
+                    help="N > 1, C2: SSR row blocks of the CSR-k matrix (strong scaling, "
+                         "default) or round 1's weak-scaling z-slabs")
+    ap.add_argument("--probe-launch", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args(argv)
+    world_env = os.environ.get("WORLD_SIZE")
+    if args.gpus > 1 and world_env is None and args.impl == "ours":
+        # one process per GPU: re-launch this command under torchrun
+        return _relaunch_torchrun(args.gpus, sys.argv[1:] if argv is None else argv)
+    if world_env is not None and args.impl == "ours" and int(world_env) != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world_env}")
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
     rank = int(os.environ.get("RANK", "0"))
@@ -620,6 +698,9 @@ def main(argv=None):
 
 
 def _run(args, log):
+    if args.probe_launch:  # tests: the process layout only, no GPU work
+        return {"probe": True, "world_size": int(os.environ.get("WORLD_SIZE", "1")),
+                "n_gpus": args.gpus, "torchrun": "LOCAL_RANK" in os.environ}
     if args.impl == "reference":
         line = run_reference(args, log)
     elif args.config == "C4" and int(os.environ.get("WORLD_SIZE", "1")) == 1 and \

@@ -48,6 +48,8 @@ __all__ = [
     "halo_plan",
     "RankBlock",
     "local_block",
+    "interior_rows",
+    "XExchange",
     "Exchange",
     "DistSpMV",
     "bench_main",
@@ -251,10 +253,13 @@ class SlabSpMV:
         xp, yp = x_local.data_ptr(), y_own.data_ptr()
         d2h.wait_stream(cur)
         for c in range(k):
-            for j in (c - 1, c, c + 1):  # interior rows read one plane beyond
-                if 0 <= j < k:
-                    cur.wait_event(ev_x[j])
             if tcut[c + 1] > tcut[c]:
+                # the x chunks the chunk's rows read: its real row span (a
+                # tile may run past rcut[c + 1]) widened by one plane each way
+                ra, rb = int(tr[tcut[c]]) - p, int(tr[tcut[c + 1]]) + p
+                for j in range(k):
+                    if rcut[j] < rb and rcut[j + 1] > ra:
+                        cur.wait_event(ev_x[j])
                 self.dev.spmv_tiles_ptr(xp, yp, tcut[c], tcut[c + 1], s, f32=self.f32)
                 ev = torch.cuda.Event()
                 ev.record(cur)
@@ -395,8 +400,9 @@ class RankBlock:
     ssr_ptr: np.ndarray
 
 
-def local_block(m, r0: int, r1: int) -> RankBlock:
-    """Slice a CsrKMatrix (k = 3) at SSR-aligned rows [r0, r1)."""
+def local_block(m, r0: int, r1: int, col0: int = 0) -> RankBlock:
+    """Slice a CsrKMatrix (k = 3) at SSR-aligned rows [r0, r1); columns are
+    shifted by ``-col0`` (the first global column of the rank's local x)."""
     b = m.base
     rp = b.row_ptr.astype(np.int64)
     p0, p1 = int(rp[r0]), int(rp[r1])
@@ -406,67 +412,135 @@ def local_block(m, r0: int, r1: int) -> RankBlock:
     q0, q1 = int(np.searchsorted(ssr, s0)), int(np.searchsorted(ssr, s1))
     if sr[s0] != r0 or sr[s1] != r1 or ssr[q0] != s0 or ssr[q1] != s1:
         raise ValueError("rank block must start and end on super-super-row boundaries")
+    ci = b.col_idx[p0:p1]
+    if col0:
+        ci = (ci.astype(np.int64) - col0).astype(np.uint32)
     return RankBlock(
-        r0=r0, r1=r1, n_cols=b.n_cols,
+        r0=r0, r1=r1, n_cols=b.n_cols - col0,
         row_ptr=(rp[r0:r1 + 1] - p0).astype(np.uint32),
-        col_idx=b.col_idx[p0:p1], vals=b.vals[p0:p1],
+        col_idx=ci, vals=b.vals[p0:p1],
         sr_ptr=(sr[s0:s1 + 1] - r0).astype(np.uint32),
         ssr_ptr=(ssr[q0:q1 + 1] - s0).astype(np.uint32))
 
 
-class Exchange:
-    """x exchange of one rank on a full-length x buffer (any device)."""
+def interior_rows(row_ptr, col_idx, own0: int, own1: int) -> tuple:
+    """[a, b): a row range of a block whose every row reads only columns in
+    [own0, own1) -- rows are sorted by column, so a row's first / last entry
+    are its extremes.  Rows before ``a`` or from ``b`` on may read halo
+    columns (the block's first and last rows under a banded order)."""
+    rp = np.asarray(row_ptr, dtype=np.int64)
+    ci = np.asarray(col_idx, dtype=np.int64)
+    n = rp.shape[0] - 1
+    nz = rp[1:] > rp[:-1]
+    first = np.where(nz, ci[np.minimum(rp[:-1], max(len(ci) - 1, 0))], own0)
+    last = np.where(nz, ci[np.maximum(rp[1:] - 1, 0)], own0)
+    lo_bad = np.flatnonzero(nz & (first < own0))
+    hi_bad = np.flatnonzero(nz & (last >= own1))
+    a = int(lo_bad[-1]) + 1 if lo_bad.size else 0
+    b = int(hi_bad[0]) if hi_bad.size else n
+    return a, max(a, b)
 
-    def __init__(self, rank: int, world: int, cuts, fps, mode: str = "halo", group=None):
+
+class XExchange:
+    """Fills the halo of one rank's local x (global columns [x0, x1), owned
+    slice [r0, r1) inside it) from the peers that own those columns.
+
+      "halo"       (default) one ``batch_isend_irecv`` of exactly the
+                   contiguous windows each rank's rows read from each peer
+                   (halo_plan); with Band-k ordering these are narrow bands
+                   next to the owned slice;
+      "allgather"  the literal north-star collective: every rank's owned
+                   slice, padded to the largest, all-gathered into one
+                   buffer, then the footprint windows copied into place.
+
+    Both post asynchronously (``start``) and return works the caller waits
+    on (``finish``) -- the interior rows are computed in between.  Works on
+    CPU tensors over gloo (tests) and CUDA tensors over NCCL."""
+
+    def __init__(self, rank: int, world: int, cuts, fps, x0: int, mode: str = "halo",
+                 group=None):
         if mode not in ("halo", "allgather"):
             raise ValueError(f"unknown exchange mode {mode!r}")
         self.rank, self.world, self.mode, self.group = rank, world, mode, group
         self.cuts = [int(c) for c in cuts]
+        self.x0 = int(x0)
         plan = halo_plan(self.cuts, fps)
         self.sends = [(d, a, b) for s, d, a, b in plan if s == rank]
         self.recvs = [(s, a, b) for s, d, a, b in plan if d == rank]
         self.maxlen = max(self.cuts[g + 1] - self.cuts[g] for g in range(world))
-        self._gather = None
+        self._bufs = None
+        self._pending = []
 
     def bytes_received(self, itemsize: int = 8) -> int:
         if self.mode == "allgather":
             return (self.world - 1) * self.maxlen * itemsize
         return sum(b - a for _, a, b in self.recvs) * itemsize
 
-    def __call__(self, x_full):
+    def bytes_sent(self, itemsize: int = 8) -> int:
+        if self.mode == "allgather":
+            return self.maxlen * itemsize
+        return sum(b - a for _, a, b in self.sends) * itemsize
+
+    def start(self, x_local) -> list:
         import torch
         import torch.distributed as dist
 
         if self.world == 1:
-            return x_full
+            return []
+        x0 = self.x0
         if self.mode == "halo":
-            ops = [dist.P2POp(dist.isend, x_full[a:b], d, group=self.group)
+            ops = [dist.P2POp(dist.isend, x_local[a - x0:b - x0], d, group=self.group)
                    for d, a, b in self.sends]
-            ops += [dist.P2POp(dist.irecv, x_full[a:b], s, group=self.group)
+            ops += [dist.P2POp(dist.irecv, x_local[a - x0:b - x0], s, group=self.group)
                     for s, a, b in self.recvs]
-            if ops:
-                for req in dist.batch_isend_irecv(ops):
-                    req.wait()
-            return x_full
+            # a rank without peers posts nothing; the communicator already
+            # exists (the constructor's collective), so the other ranks'
+            # batches do not wait on it
+            self._pending = []
+            return dist.batch_isend_irecv(ops) if ops else []
+        if self._bufs is None or self._bufs[0].device != x_local.device or \
+                self._bufs[0].dtype != x_local.dtype:
+            self._bufs = (torch.zeros(self.maxlen, dtype=x_local.dtype, device=x_local.device),
+                          torch.zeros(self.world * self.maxlen, dtype=x_local.dtype,
+                                      device=x_local.device))
+        mine, every = self._bufs
         lo, hi = self.cuts[self.rank], self.cuts[self.rank + 1]
-        if self._gather is None or self._gather[0].device != x_full.device:
-            self._gather = [torch.zeros(self.maxlen, dtype=x_full.dtype, device=x_full.device)
-                            for _ in range(self.world)]
-        mine = self._gather[self.rank]
-        mine[: hi - lo].copy_(x_full[lo:hi])
-        dist.all_gather(self._gather, mine.clone(), group=self.group)
-        for g in range(self.world):
-            a, b = self.cuts[g], self.cuts[g + 1]
-            if g != self.rank and b > a:
-                x_full[a:b].copy_(self._gather[g][: b - a])
-        return x_full
+        mine[:hi - lo].copy_(x_local[lo - x0:hi - x0])
+        work = dist.all_gather_into_tensor(every, mine, group=self.group, async_op=True)
+        self._pending = [(s, a, b) for s, a, b in self.recvs]
+        return [work]
+
+    def finish(self, x_local, works) -> None:
+        for w in works:
+            w.wait()
+        if self.mode == "allgather":
+            _, every = self._bufs
+            for s, a, b in self._pending:
+                off = s * self.maxlen + (a - self.cuts[s])
+                x_local[a - self.x0:b - self.x0].copy_(every[off:off + (b - a)])
+
+    def __call__(self, x_local):
+        self.finish(x_local, self.start(x_local))
+        return x_local
 
 
 class DistSpMV:
-    """y_local = A[r0:r1, :] x on this rank's GPU after the x exchange."""
+    """y_own = A[r0:r1, :] x on this rank's GPU.
+
+    The packed matrix's super-super-rows are split by nonzeros
+    (partition_by_nnz, the reference's static chunks kernels.py:150-155 with
+    nonzero weights).  The rank keeps only its rows, with columns local to
+    its footprint: x_local holds global columns [x0, x1) -- the owned slice
+    [r0, r1) plus the halo its rows read -- never a global-length x.
+
+    One step posts the exchange of the halo, runs the interior tiles (rows
+    that read owned columns only; interior_rows) while it is in flight,
+    waits, then runs the boundary tiles before / after them: the NVLink
+    transfer overlaps the bulk of the SpMV.  y is bitwise the single-GPU
+    result (rows are summed whole, in the reference's order)."""
 
     def __init__(self, m, rank: int, world: int, mode: str = "halo", group=None,
-                 device=None, f32: bool = False):
+                 device=None, f32: bool = False, variant: str = "serial", nx: int = 1):
         from . import _native as nat
 
         b = m.base
@@ -474,60 +548,97 @@ class DistSpMV:
         self.fps = footprints(b.row_ptr, b.col_idx, self.cuts)
         self.rank, self.world = rank, world
         self.r0, self.r1 = int(self.cuts[rank]), int(self.cuts[rank + 1])
-        blk = local_block(m, self.r0, self.r1)
+        lo, hi = (int(v) for v in self.fps[rank])
+        self.x0 = min(lo, self.r0) if hi > lo else self.r0
+        self.x1 = max(hi, self.r1) if hi > lo else self.r1
+        blk = local_block(m, self.r0, self.r1, col0=self.x0)
+        self.n_own = self.r1 - self.r0
+        self.n_local_cols = self.x1 - self.x0
         self.nnz_local = int(blk.row_ptr[-1])
         self.nnz_total = b.nnz
         self.n = b.n_rows
-        self.dev = nat.DeviceMatrix.upload(
-            blk.row_ptr, blk.col_idx, blk.vals, self.r1 - self.r0, b.n_cols, k=3,
-            sr_ptr=blk.sr_ptr, ssr_ptr=blk.ssr_ptr, device=device, f32=f32)
-        self.exchange = Exchange(rank, world, self.cuts, self.fps, mode, group)
         self.f32 = f32
+        self.var = nat.CSRK_STRIDED if variant == "strided" else nat.CSRK_SERIAL
+        self.nx = int(nx) if variant == "strided" else 1
+        self.dev = None
+        self.t_lo = self.t_hi = self.n_tiles = 0
+        if self.n_own > 0:
+            self.dev = nat.DeviceMatrix.upload(
+                blk.row_ptr, blk.col_idx, blk.vals, self.n_own, self.n_local_cols, k=3,
+                sr_ptr=blk.sr_ptr, ssr_ptr=blk.ssr_ptr, device=device, f32=f32)
+            self.dev.prepare(self.var, self.nx, f32)
+            self.n_tiles = self.dev.plan()["n_tiles"]
+            a, bb = interior_rows(blk.row_ptr, blk.col_idx, self.r0 - self.x0,
+                                  self.r1 - self.x0)
+            self.t_lo, self.t_hi = interior_tiles(self.dev.tile_rows(), a, bb)
+        self.exchange = XExchange(rank, world, self.cuts, self.fps, self.x0, mode, group)
+        _collective_warmup(group)
 
-    def step(self, x_full, y_local, stream=None, dims=None, strided=False):
-        """Exchange x then run the local SpMV (stream-ordered)."""
+    @property
+    def own(self) -> slice:
+        """The owned x entries inside x_local."""
+        return slice(self.r0 - self.x0, self.r1 - self.x0)
+
+    def new_x_local(self, dtype=None, device=None):
         import torch
 
-        from . import _native as nat
+        dtype = dtype or (torch.float32 if self.f32 else torch.float64)
+        return torch.zeros(max(1, self.n_local_cols), dtype=dtype, device=device or "cuda")
 
-        self.exchange(x_full)
-        if self.r1 > self.r0:
-            s = stream or torch.cuda.current_stream(x_full.device)
-            self.dev.spmv_ptr(x_full.data_ptr(), y_local.data_ptr(), s.cuda_stream,
-                              variant=nat.CSRK_STRIDED if strided else nat.CSRK_SERIAL,
-                              nx=dims.x if (strided and dims) else 1, f32=self.f32)
-        return y_local
+    def _tiles(self, x_local, y_own, t0, t1, s):
+        if t1 > t0:
+            self.dev.spmv_tiles_ptr(x_local.data_ptr(), y_own.data_ptr(), t0, t1, s,
+                                    variant=self.var, nx=self.nx, f32=self.f32)
+
+    def step(self, x_local, y_own):
+        """Post the x exchange, interior tiles, wait, boundary tiles -- all
+        ordered on the current stream (NCCL's works wait on it and it waits
+        on them)."""
+        import torch
+
+        works = self.exchange.start(x_local)
+        if self.dev is not None:
+            s = torch.cuda.current_stream(x_local.device).cuda_stream
+            self._tiles(x_local, y_own, self.t_lo, self.t_hi, s)
+            self.exchange.finish(x_local, works)
+            self._tiles(x_local, y_own, 0, self.t_lo, s)
+            self._tiles(x_local, y_own, self.t_hi, self.n_tiles, s)
+        else:
+            self.exchange.finish(x_local, works)
+        return y_own
+
+    @property
+    def launches_per_step(self) -> int:
+        if self.dev is None:
+            return 0
+        n_long = 1 if self.dev.plan()["n_long"] > 0 else 0
+        parts = [self.t_hi > self.t_lo, self.t_lo > 0, self.t_hi < self.n_tiles]
+        return sum(parts) * (1 + n_long)
+
+    def local_bytes(self, itemsize: int) -> int:
+        """Algorithmic HBM bytes of this rank's SpMV (SURVEY.md §8(d) on the
+        rank's block: its nonzeros, row pointers, local x and y)."""
+        return (self.nnz_local * (itemsize + 4) + 4 * (self.n_own + 1)
+                + (self.n_local_cols + self.n_own) * itemsize)
 
 
-def _cached_build(cfg: str, rank: int, log):
-    """Rank 0 builds the packed matrix and writes it to a cache file; the
-    other ranks load it (one Band-k per job instead of one per rank)."""
+def _collective_warmup(group=None) -> None:
+    """One collective over the group before any point-to-point batch: with
+    NCCL the first batch_isend_irecv must otherwise involve every rank, and
+    a rank with no halo posts none (torch's batch_isend_irecv contract)."""
+    import torch
     import torch.distributed as dist
 
-    import paper_2203_05096_b200 as ck
+    if not dist.is_available() or not dist.is_initialized():
+        return
+    dev = "cuda" if dist.get_backend(group) == "nccl" else "cpu"
+    t = torch.zeros(1, device=dev)
+    dist.all_reduce(t, group=group)
 
-    path = os.path.join(os.environ.get("TMPDIR", "/tmp"), f"csrk_bench_{cfg}_{os.getpid()}")
-    obj = [path]
-    dist.broadcast_object_list(obj, src=0)
-    path = obj[0] + ".npz"
-    if rank == 0:
-        import bench as _bench  # the driver script's builder
 
-        a, m, xp, params, bt = _bench.build_matrix(cfg, log)
-        np.savez(path, row_ptr=m.base.row_ptr, col_idx=m.base.col_idx, vals=m.base.vals,
-                 sr_ptr=m.sr_ptr, ssr_ptr=m.ssr_ptr, fwd=m.perm.fwd, xp=xp,
-                 params=np.array([params.ssrs, params.srs]))
-    dist.barrier()
-    z = np.load(path)
-    n = len(z["row_ptr"]) - 1
-    base = ck.CsrMatrix(n, n, z["row_ptr"], z["col_idx"], z["vals"], _trusted=True)
-    perm = ck.Permutation.from_forward(z["fwd"])
-    m = ck.CsrKMatrix(base, 3, (z["sr_ptr"], z["ssr_ptr"]), perm, _trusted=True)
-    xp = z["xp"]
-    dist.barrier()
-    if rank == 0:
-        os.remove(path)
-    return m, xp, [int(v) for v in z["params"]]
+# kept for callers of the round-1 name: the exchange on a full-length x
+def Exchange(rank, world, cuts, fps, mode="halo", group=None):  # noqa: N802
+    return XExchange(rank, world, cuts, fps, 0, mode, group)
 
 
 METRIC = "SpMV GFLOP/s and achieved HBM GB/s (% of peak) at 1/2/4/8 B200 vs host CPU"
@@ -540,6 +651,15 @@ def _max_over_ranks(v: float) -> float:
     t = torch.tensor([float(v)], dtype=torch.float64, device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+def _min_over_ranks(v: int) -> int:
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([int(v)], dtype=torch.int64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MIN)
+    return int(t.item())
 
 
 def _sum_over_ranks(v: int) -> int:
@@ -771,15 +891,192 @@ def bench_cg_slabs(args, log, rank: int, world: int, local: int, sampler=None, p
     }
 
 
-def bench_main(args, log, sampler=None, peak=None):
-    """bench.py --gpus N under torchrun.  C2 (the default): weak scaling over
-    C2-sized slabs (bench_slabs).  Other configs: the config's CSR-k matrix
-    partitioned by nonzeros over the ranks (strong scaling), halo exchange +
-    local SpMV per step.  Device time max-reduced over ranks."""
+def bench_blocks(args, log, rank: int, world: int, local: int, sampler=None, peak=None,
+                 oracle_check=None):
+    """Strong scaling of one config's CSR-k matrix (the N = 1 bench line's
+    matrix: synthetic input, native Band-k with the B200 model's sizes, device
+    pack) over ``world`` GPUs: super-super-rows split by nonzeros
+    (DistSpMV), x halo over NCCL overlapped with the interior tiles.  Every
+    rank builds the matrix on its own GPU (device Band-k is deterministic and
+    bit-exact, ~2 s at C2), keeps its row block, and rank 0 also times the
+    whole matrix on one GPU (T1) for the efficiency T1 / (N T_N).  Device
+    time with CUDA events on the launching stream, max over ranks."""
+    import time
+
     import torch
     import torch.distributed as dist
 
+    import bench as _bench  # the driver script's builder (repo root)
+
     from .bench import spmv_bytes
+
+    a, m, xp, params, build_t = _bench.build_matrix(args.config, log)
+    n, nnz = a.n_rows, a.nnz
+    variant = "strided" if params.kernel_variant.value == "cuda35" else "serial"
+    nx = params.block_dims.x if variant == "strided" else 1
+    f32 = args.fp32
+    dtype = torch.float32 if f32 else torch.float64
+    vb = 4 if f32 else 8
+    mode = getattr(args, "exchange", None) or os.environ.get("CSRK_EXCHANGE", "halo")
+    op = DistSpMV(m, rank, world, mode=mode, device=local, f32=f32, variant=variant, nx=nx)
+    x_local = op.new_x_local(dtype)
+    x_local[op.own] = torch.from_numpy(xp[op.r0:op.r1]).to("cuda", dtype)
+    # columns outside the owned slice are the exchange's job: poison them
+    # so a missing halo shows up in the parity check
+    if op.own.start > 0:
+        x_local[:op.own.start] = float("nan")
+    if op.own.stop < x_local.numel():
+        x_local[op.own.stop:] = float("nan")
+    y = torch.empty(max(1, op.n_own), dtype=dtype, device="cuda")
+
+    def step():
+        op.step(x_local, y)
+
+    # T1: the whole matrix on rank 0's GPU alone (the others wait)
+    t1_ms = None
+    if rank == 0:
+        from . import kernels
+
+        xf = torch.from_numpy(xp).to("cuda", dtype)
+        yf = torch.empty(n, dtype=dtype, device="cuda")
+        dims = params.block_dims
+
+        def full():
+            kernels.spmv_device(m, xf, yf, dims=dims, variant=variant)
+
+        for _ in range(3):
+            full()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = max(10, args.steps)
+        e0.record()
+        for _ in range(reps):
+            full()
+        e1.record()
+        torch.cuda.synchronize()
+        t1_ms = e0.elapsed_time(e1) / reps
+        del xf, yf
+    dist.barrier()
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    clk_ctx = sampler(torch.cuda.current_device()) if (sampler and rank == 0) else None
+    if clk_ctx is not None:
+        clk_ctx.__enter__()
+    burn = max(5, args.warmup)
+    for _ in range(burn):  # untimed load while the sampler collects
+        step()
+    torch.cuda.synchronize()
+    if clk_ctx is not None:
+        time.sleep(0.3)
+    dist.barrier()
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    for _ in range(args.steps):
+        step()
+    ev1.record()
+    torch.cuda.synchronize()
+    dist.barrier()
+    if clk_ctx is not None:
+        clk_ctx.__exit__(None, None, None)
+    ms_rank = ev0.elapsed_time(ev1) / args.steps
+    ms = _max_over_ranks(ms_rank)
+    # parity of this rank's rows against the oracle (the timed output)
+    ok = True
+    max_diff = 0.0
+    if oracle_check is not None and op.n_own > 0:
+        want = oracle_check(m, xp, variant, nx)[op.r0:op.r1]
+        got = y[:op.n_own].double().cpu().numpy()
+        if f32:
+            from .kernels import host_row_sums
+
+            b = m.base
+            scale = host_row_sums(b.row_ptr, b.col_idx, np.abs(b.vals), np.abs(xp))[op.r0:op.r1]
+            ok = bool(np.all(np.abs(got - want) <= 1e-5 * scale))
+        else:
+            ok = bool(np.array_equal(got, want))
+        max_diff = float(np.max(np.abs(got - want))) if got.size else 0.0
+    ok_all = _min_over_ranks(int(ok))
+    # e2e: each rank's owned x slice up from pinned host memory, the step,
+    # its y slice down; max over ranks
+    x_pin = torch.empty(max(1, op.n_own), dtype=dtype, pin_memory=True)
+    x_pin[:op.n_own] = x_local[op.own].cpu()
+    y_pin = torch.empty(max(1, op.n_own), dtype=dtype, pin_memory=True)
+    e2e_steps = max(3, min(args.steps, 20))
+    torch.cuda.synchronize()
+    dist.barrier()
+    te = 0.0
+    for it in range(e2e_steps + 1):
+        if it == 1:
+            torch.cuda.synchronize()
+            dist.barrier()
+            te = time.perf_counter()
+        x_local[op.own].copy_(x_pin[:op.n_own], non_blocking=True)
+        op.step(x_local, y)
+        y_pin[:op.n_own].copy_(y[:op.n_own], non_blocking=True)
+        torch.cuda.synchronize()
+    e2e_s = _max_over_ranks((time.perf_counter() - te) / e2e_steps)
+    ex_max = _max_over_ranks(op.exchange.bytes_received(vb))
+    local_gbs = op.local_bytes(vb) / (ms_rank * 1e-3) / 1e9
+    gbs_min = -_max_over_ranks(-local_gbs)
+    launches = _sum_over_ranks(op.launches_per_step)
+    if rank != 0:
+        return None
+    algo = spmv_bytes(n, n, nnz, vb)
+    peak_v, peak_src = peak if peak else (None, None)
+    gflops = 2.0 * nnz / (ms * 1e-3) / 1e9
+    return {
+        "metric": METRIC,
+        "value": round(gflops, 2), "unit": "GFLOP/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32" if f32 else "f64",
+        "data": "synthetic (deterministic grid Laplacian / irregular rows, x ~ U[-1,1) seed 0)",
+        "config": {"workload": _bench.CONFIG_TEXT.get(args.config, args.config),
+                   "config_id": args.config, "n_rows": n, "nnz": nnz,
+                   "ssrs_target": params.ssrs, "srs_target": params.srs,
+                   "kernel": f"csrk_stream_kernel ({variant}"
+                             + (f", nx={nx})" if variant == "strided" else ")"),
+                   "parallelism": f"row blocks of whole super-super-rows x{world}, "
+                                  f"balanced by nonzeros; {mode} x exchange over NCCL "
+                                  "overlapped with the interior tiles",
+                   "exchange_bytes_per_rank_max": ex_max,
+                   "l2": "inputs larger than L2; no flush" if algo >= 4 * 126e6 / world
+                         else "per-rank inputs may fit L2 at this N"},
+        "hbm_gbs": round(algo / (ms * 1e-3) / 1e9, 1),
+        "roofline": {"bound": "hbm", "achieved": round(gbs_min, 1), "peak": peak_v,
+                     "unit": "GB/s", "frac": round(gbs_min / peak_v, 4) if peak_v else None,
+                     "peak_source": peak_src,
+                     "per": "slowest rank: its block's algorithmic bytes / its own step time",
+                     "traffic": None,
+                     "algorithmic_bytes_per_launch": op.local_bytes(vb)},
+        "t1_ms": round(t1_ms, 4) if t1_ms else None,
+        "efficiency_t1_over_n_tn": round(t1_ms / (world * ms), 4) if t1_ms else None,
+        "parity": {"kind": "scaled 1e-5" if f32 else "bitwise", "ok": bool(ok_all),
+                   "against": "oracle/csrk_oracle.c on the same CSR-k matrix and x",
+                   "max_abs_diff_rank0": max_diff},
+        "e2e": {"value": round(2.0 * nnz / e2e_s / 1e9, 2), "unit": "GFLOP/s",
+                "h2d_bytes_per_step": n * vb, "d2h_bytes_per_step": n * vb,
+                "ms_per_step": round(e2e_s * 1e3, 3),
+                "call": "dist.DistSpMV.step per rank with its pinned host x / y slices"},
+        "cpu_baseline": None,
+        "gpu_launches": args.steps * launches,
+        "clocks": clk_ctx.summary() if clk_ctx is not None else None,
+        "build_seconds": {k: round(v, 2) for k, v in build_t.items()},
+    }
+
+
+def bench_main(args, log, sampler=None, peak=None, oracle_check=None):
+    """bench.py --gpus N (one process per GPU, torchrun).  C1/C2/C3/C5: the
+    config's CSR-k matrix split over the ranks (strong scaling, the same
+    matrix and kernel as the N = 1 line; bench_blocks).  C4: the CG loop of
+    the 512^3 Laplacian on z-slabs (strong scaling, bench_cg_slabs).
+    ``--partition slab`` keeps round 1's weak-scaling slab run of C2."""
+    import torch
+    import torch.distributed as dist
 
     rank = int(os.environ["RANK"])
     world = int(os.environ["WORLD_SIZE"])
@@ -788,52 +1085,11 @@ def bench_main(args, log, sampler=None, peak=None):
     from . import _native as nat
     nat.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    if args.config in ("C2", "C4"):
-        fn = bench_slabs if args.config == "C2" else bench_cg_slabs
-        try:
-            return fn(args, log, rank, world, local, sampler, peak)
-        finally:
-            dist.destroy_process_group()
-    m, xp, (ssrs, srs) = _cached_build(args.config, rank, log)
-    mode = os.environ.get("CSRK_EXCHANGE", "halo")
-    op = DistSpMV(m, rank, world, mode=mode, device=local, f32=args.fp32)
-    dtype = torch.float32 if args.fp32 else torch.float64
-    x_full = torch.zeros(op.n, dtype=dtype, device="cuda")
-    x_full[op.r0:op.r1] = torch.from_numpy(xp[op.r0:op.r1]).to("cuda", dtype)
-    y = torch.empty(max(1, op.r1 - op.r0), dtype=dtype, device="cuda")
-    for _ in range(args.warmup):
-        op.step(x_full, y)
-    torch.cuda.synchronize()
-    dist.barrier()
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
-    ev0.record()
-    for _ in range(args.steps):
-        op.step(x_full, y)
-    ev1.record()
-    torch.cuda.synchronize()
-    ms = torch.tensor([ev0.elapsed_time(ev1) / args.steps], device="cuda")
-    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    dist.barrier()
-    ms = float(ms.item())
-    vbytes = 4 if args.fp32 else 8
-    gflops = 2.0 * op.nnz_total / (ms * 1e-3) / 1e9
-    line = None
-    if rank == 0:
-        algo = spmv_bytes(op.n, op.n, op.nnz_total, vbytes)
-        line = {
-            "metric": "SpMV GFLOP/s and achieved HBM GB/s (% of peak) at 1/2/4/8 B200 vs host CPU",
-            "value": round(gflops, 2), "unit": "GFLOP/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": "f32" if args.fp32 else "f64",
-            "data": "synthetic (deterministic grid Laplacian, x ~ U[-1,1) seed 0)",
-            "config": {"workload": args.config, "n_rows": op.n, "nnz": op.nnz_total,
-                       "parallelism": f"row-block SSR partition x{world}, {mode} x exchange",
-                       "exchange_bytes_rank0": op.exchange.bytes_received(vbytes),
-                       "ssrs_target": ssrs, "srs_target": srs},
-            "aggregate_hbm_gbs": round(algo / (ms * 1e-3) / 1e9, 1),
-            "gpu_launches": args.steps,
-        }
-    dist.destroy_process_group()
-    return line
+    try:
+        if args.config == "C4":
+            return bench_cg_slabs(args, log, rank, world, local, sampler, peak)
+        if getattr(args, "partition", "blocks") == "slab":
+            return bench_slabs(args, log, rank, world, local, sampler, peak)
+        return bench_blocks(args, log, rank, world, local, sampler, peak, oracle_check)
+    finally:
+        dist.destroy_process_group()

@@ -73,3 +73,28 @@ def test_missing_library_fails_loudly(monkeypatch, tmp_path):
     monkeypatch.setattr(_native, "LIB_PATH", str(tmp_path / "absent.so"))
     with pytest.raises(RuntimeError, match="no CPU fallback"):
         _native.lib()
+
+
+@pytest.mark.gpu
+def test_spmv_kernels_launch_first():
+    """The hot kernels run through the library before anything else of the
+    GPU suite (csrk_stream_kernel in both orders, long_rows_kernel beside
+    it), checked against the oracle -- no Band-k on this path."""
+    import numpy as np
+
+    import paper_2203_05096_b200 as ck
+    from oracle import oracle as O
+
+    rng = np.random.default_rng(11)
+    n = 20000
+    lens = rng.integers(0, 16, n)
+    lens[[5, 9000]] = (700, 3000)
+    rows = np.repeat(np.arange(n), lens)
+    a = ck.csr_from_arrays(n, n, rows, rng.integers(0, n, len(rows)),
+                           rng.uniform(-1, 1, len(rows)))
+    m = ck.pack_csrk(a, ck.Permutation.identity(n), [[1] * n, [n]])
+    x = rng.uniform(-1, 1, n)
+    assert np.array_equal(ck.spmv_csr3(m, x), O.spmv_serial(a.row_ptr, a.col_idx, a.vals, x))
+    assert np.array_equal(ck.spmv_gpu35(m, x, ck.BlockDims(8, 1, 1)),
+                          O.spmv_strided(a.row_ptr, a.col_idx, a.vals, x, 8))
+    assert m.device().plan()["n_long"] == 2

@@ -122,6 +122,72 @@ def test_exchange_over_gloo(world, mode):
         assert nbytes > 0
 
 
+def _local_worker(rank, world, port, mode, result_q):
+    """DistSpMV's host-side pieces on CPU tensors over gloo: the rank's block
+    with footprint-local columns, the interior rows computed BEFORE the
+    exchange (halo poisoned with NaN), the exchange, then the boundary rows."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        m = _packed()
+        b = m.base
+        cuts = D.partition_by_nnz(b.row_ptr, m.sr_ptr, m.ssr_ptr, world)
+        fps = D.footprints(b.row_ptr, b.col_idx, cuts)
+        r0, r1 = int(cuts[rank]), int(cuts[rank + 1])
+        lo, hi = (int(v) for v in fps[rank])
+        x0, x1 = min(lo, r0), max(hi, r1)
+        blk = D.local_block(m, r0, r1, col0=x0)
+        x = np.random.default_rng(1).uniform(-1, 1, b.n_rows)
+        x_local = torch.full((x1 - x0,), float("nan"), dtype=torch.float64)
+        x_local[r0 - x0:r1 - x0] = torch.from_numpy(x[r0:r1])
+        a, bb = D.interior_rows(blk.row_ptr, blk.col_idx, r0 - x0, r1 - x0)
+        want = O.spmv_serial(b.row_ptr, b.col_idx, b.vals, x)[r0:r1]
+        early = O.spmv_serial(blk.row_ptr, blk.col_idx, blk.vals, x_local.numpy())
+        ok_interior = bool(np.array_equal(early[a:bb], want[a:bb]))
+        ex = D.XExchange(rank, world, cuts, fps, x0, mode)
+        ex.finish(x_local, ex.start(x_local))
+        ok_window = bool(torch.equal(x_local, torch.from_numpy(x[x0:x1])))
+        y = O.spmv_serial(blk.row_ptr, blk.col_idx, blk.vals, x_local.numpy())
+        result_q.put((rank, ok_interior, ok_window, bool(np.array_equal(y, want)),
+                      bb - a, r1 - r0, x1 - x0, ex.bytes_received()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,mode", [(2, "halo"), (2, "allgather"), (3, "halo"),
+                                        (4, "halo"), (3, "allgather")])
+def test_footprint_local_exchange_over_gloo(world, mode):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_local_worker, args=(r, world, port, mode, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    results = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    n = _packed().base.n_rows
+    for rank, ok_int, ok_win, ok_y, n_int, n_own, n_loc, nbytes in results:
+        assert ok_int, f"rank {rank}: interior rows read the halo"
+        assert ok_win, f"rank {rank}: footprint x not filled by {mode}"
+        assert ok_y, f"rank {rank}: local SpMV differs"
+        assert n_loc < n, "local x must be footprint-sized, not global"
+        assert 0 <= n_int <= n_own
+    assert sum(r[4] for r in results) > 0  # (a narrow middle block may be all halo)
+
+
+def test_interior_rows_edge_cases():
+    # rows: [own only], [reads below], [empty], [reads above]
+    rp = np.array([0, 2, 4, 4, 6], dtype=np.uint32)
+    ci = np.array([5, 6, 3, 7, 6, 12], dtype=np.uint32)
+    assert D.interior_rows(rp, ci, 5, 10) == (2, 3)
+    assert D.interior_rows(rp, ci, 0, 20) == (0, 4)
+    assert D.interior_rows(np.zeros(1, np.uint32), np.zeros(0, np.uint32), 0, 1) == (0, 0)
+
+
 @pytest.mark.gpu
 def test_partitioned_device_spmv_reassembles_bitwise():
     from paper_2203_05096_b200 import _native as nat
@@ -141,6 +207,47 @@ def test_partitioned_device_spmv_reassembles_bitwise():
                                           ssr_ptr=blk.ssr_ptr)
             ys.append(dev.spmv_host(x) if blk.r1 > blk.r0 else np.zeros(0))
         np.testing.assert_array_equal(np.concatenate(ys), want)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("variant,nx", [("serial", 1), ("strided", 4)])
+def test_dist_blocks_interior_then_boundary_bitwise(variant, nx):
+    """DistSpMV's device part on one GPU, rank by rank: footprint-local x
+    with a NaN halo, the interior tiles (they must not read the halo), then
+    the halo filled (what the exchange delivers) and the boundary tiles --
+    the slices reassemble the single-GPU y bit for bit."""
+    n, rp, ci, va = synthetic.stencil_arrays((40, 40, 40), 7, values="uniform")
+    a = ck.CsrMatrix(n, n, rp, ci, va)
+    res = ck.band_k(a, 3, [8, 8])
+    m = ck.pack_csrk(a, res.perm, res.level_group_sizes)
+    b = m.base
+    x = np.random.default_rng(5).uniform(-1, 1, n)
+    want = (O.spmv_serial(b.row_ptr, b.col_idx, b.vals, x) if variant == "serial"
+            else O.spmv_strided(b.row_ptr, b.col_idx, b.vals, x, nx))
+    for parts in (1, 2, 3, 8):
+        got = []
+        interior_seen = 0
+        for g in range(parts):
+            op = D.DistSpMV(m, g, parts, variant=variant, nx=nx)
+            xl = torch.full((op.n_local_cols,), float("nan"), dtype=torch.float64,
+                            device="cuda")
+            xl[op.own] = torch.from_numpy(x[op.r0:op.r1]).cuda()
+            y = torch.full((op.n_own,), float("nan"), dtype=torch.float64, device="cuda")
+            s = torch.cuda.current_stream().cuda_stream
+            op._tiles(xl, y, op.t_lo, op.t_hi, s)
+            torch.cuda.synchronize()
+            tr = op.dev.tile_rows()
+            ra, rb = int(tr[op.t_lo]), int(tr[op.t_hi])
+            np.testing.assert_array_equal(y[ra:rb].cpu().numpy(), want[op.r0 + ra:op.r0 + rb])
+            interior_seen += rb - ra
+            xl.copy_(torch.from_numpy(x[op.x0:op.x1]).cuda())
+            op._tiles(xl, y, 0, op.t_lo, s)
+            op._tiles(xl, y, op.t_hi, op.n_tiles, s)
+            torch.cuda.synchronize()
+            got.append(y.cpu().numpy())
+            assert op.n_local_cols < n or parts == 1
+        np.testing.assert_array_equal(np.concatenate(got), want)
+        assert interior_seen > 0
 
 
 def _host_slab(shape, points, lay, values="uniform"):
@@ -328,11 +435,12 @@ def test_dist_cg_over_gloo(world):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("config", ["C2", "C4"])
+@pytest.mark.parametrize("config", ["C2", "C2-slab", "C4"])
 def test_bench_multi_gpu_path_one_rank(config):
-    """bench.py's torchrun path (NCCL process group, slab partition, halo
-    exchange code, distributed CG) end to end with one rank (CSRK_DIST=1):
-    the JSON line has the contract's keys and the weak / strong labels."""
+    """bench.py's torchrun path (NCCL process group, SSR row blocks with the
+    halo exchange and the oracle parity check, the slab partition, the
+    distributed CG) end to end with one rank (CSRK_DIST=1): the JSON line
+    has the contract's keys and the weak / strong labels."""
     import json
     import subprocess
     import sys
@@ -341,7 +449,9 @@ def test_bench_multi_gpu_path_one_rank(config):
     port = _free_port()
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=1",
            "--master-addr", "127.0.0.1", "--master-port", str(port), "bench.py", "--gpus", "1",
-           "--steps", "3", "--warmup", "3", "--config", config]
+           "--steps", "3", "--warmup", "3", "--config", config.split("-")[0]]
+    if config == "C2-slab":
+        cmd += ["--partition", "slab"]
     if config == "C4":
         cmd += ["--side", "96", "--iters", "10"]
     env = dict(os.environ, CSRK_DIST="1")
@@ -352,16 +462,19 @@ def test_bench_multi_gpu_path_one_rank(config):
                 "roofline", "gpu_launches", "clocks"):
         assert key in line, key
     assert line["n_gpus"] == 1 and line["value"] > 0
-    assert line["scaling"] == ("weak" if config == "C2" else "strong")
+    assert line["scaling"] == ("weak" if config == "C2-slab" else "strong")
+    if config == "C2":
+        assert line["parity"]["ok"] and line["efficiency_t1_over_n_tn"] > 0
     assert line["e2e"]["h2d_bytes_per_step"] > 0
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("chunks", [1, 3, 8])
-def test_slab_host_pipeline_bitwise(chunks):
+@pytest.mark.parametrize("chunks,nz", [(1, 40), (3, 40), (8, 40), (8, 6), (5, 5)])
+def test_slab_host_pipeline_bitwise(chunks, nz):
     """SlabSpMV.step_host (chunked H2D / interior tiles / D2H on three
-    streams) gives the bits of the device-resident step (one rank)."""
-    shape = (40, 48, 56)
+    streams) gives the bits of the device-resident step (one rank),
+    including one-plane chunks whose tiles read two chunks ahead."""
+    shape = (nz, 48, 56)
     op = D.SlabSpMV(shape, 7, 0, 1)
     lay = op.lay
     x = torch.from_numpy(np.random.default_rng(chunks).uniform(-1, 1, lay.n_own))
@@ -378,3 +491,22 @@ def test_slab_host_pipeline_bitwise(chunks):
         op.step_host(x_pin, y_pin, x_local, y, chunks=chunks)
         torch.cuda.synchronize()
         np.testing.assert_array_equal(y_pin.numpy(), want)
+
+
+def test_bench_gpus_flag_relaunches_under_torchrun():
+    """`python bench.py --gpus N` without torchrun re-launches itself as N
+    ranks (torch.distributed.run); rank 0 prints the one JSON line."""
+    import json
+    import subprocess
+    import sys
+
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items()
+           if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT")}
+    out = subprocess.run([sys.executable, "bench.py", "--gpus", "3", "--probe-launch"],
+                         cwd=repo, env=env, capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    line = json.loads(lines[0])
+    assert line["world_size"] == 3 and line["n_gpus"] == 3 and line["torchrun"]

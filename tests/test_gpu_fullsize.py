@@ -1,7 +1,9 @@
 """Full-size configurations (BASELINE.json configs C2, C3, C5) against the
 digests the unmodified reference produced (tests/golden/configs.json, ~5 min
 of reference Band-k each): device and host Band-k permutations and group
-sizes, the device-packed CSR-k arrays, and y of the CSR-3 kernel."""
+sizes, the device-packed CSR-k arrays, y of the CSR-3 kernel and y of the
+strided (GPUSpMV-3.5) order -- at the Volta model's targets and at the
+B200 model's targets, i.e. exactly the matrix and order bench.py times."""
 
 from __future__ import annotations
 
@@ -34,6 +36,9 @@ def test_full_size_pipeline_matches_reference(name, configs_golden, capsys):
     assert digest(a.row_ptr, "<u4") == rec["input"]["row_ptr"]
     assert digest(a.col_idx, "<u4") == rec["input"]["col_idx"]
     x = np.random.default_rng(0).uniform(-1.0, 1.0, a.n_rows)
+    # the bench's matrix: the B200 model's targets must be one of the runs
+    params = ck.tune_gpu(ck.compute_stats(a), ck.b200_profile())
+    assert [params.srs, params.ssrs] in [r["targets"] for r in rec["runs"]]
     for run in rec["runs"]:
         t0 = time.perf_counter()
         res = ck.band_k(a, 3, run["targets"], backend="device")
@@ -52,6 +57,9 @@ def test_full_size_pipeline_matches_reference(name, configs_golden, capsys):
         y3 = ck.spmv_csr3(m, xp)
         assert digest(y3, "<f8") == run["y_csr3"]
         assert digest(ck.unpermute_vector(res.perm, y3), "<f8") == run["y_csr3_unpermuted"]
+        for key in [k for k in run if k.startswith("y_emu35_")]:
+            dims = ck.BlockDims(*(int(v) for v in key[len("y_emu35_"):].split("x")))
+            assert digest(ck.spmv_gpu35(m, xp, dims), "<f8") == run[key], key
         with capsys.disabled():
             print(f"\n[{name}] device band_k {t_dev:.2f}s (reference {run['band_k_seconds']}s)")
     if name == "C2":  # the host implementation too, once
