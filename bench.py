@@ -245,6 +245,8 @@ def run_ours(args, log):
     xd = torch.from_numpy(xp).to("cuda", dtype)
     yd = torch.empty(n, dtype=dtype, device="cuda")
     stream = torch.cuda.current_stream()
+    if os.environ.get("CSRK_LAYOUT"):  # sweeps: force the whole-matrix layout
+        m.device().set_layout(int(os.environ["CSRK_LAYOUT"]))
 
     def step():
         ck.spmv_device(m, xd, yd, dims=dims, variant=variant, stream=stream)
@@ -336,10 +338,11 @@ def run_ours(args, log):
                    "config_id": args.config, "n_rows": n, "nnz": nnz,
                    "ssrs_target": params.ssrs, "srs_target": params.srs,
                    "n_sr": m.num_super_rows, "n_ssr": m.num_ssr,
-                   "kernel": f"csrk_stream_kernel ({variant})",
+                   "kernel": ("csrk_panel_kernel" if m.device().plan()["panels"]
+                              else "csrk_stream_kernel") + f" ({variant})",
                    "plan": {k: v for k, v in m.device().plan().items()
                             if k in ("tile_cost", "stages", "n_tiles", "group_aligned",
-                                     "gather_first", "ctas_per_sm")},
+                                     "gather_first", "ctas_per_sm", "panels", "n_panels")},
                    "parallelism": "1 GPU",
                    "l2": ("inputs larger than L2 (algorithmic %.2f GB per step vs 126 MB "
                           "L2); no flush" % (algo_bytes / 1e9)) if not flush else
@@ -537,15 +540,16 @@ def reference_matrix(ref, cfg: str, log):
     cached = os.path.exists(path)
     if cached:
         z = np.load(path)
-        perm = ref.Permutation.from_forward(z["fwd"])
+        perm = ref.Permutation.from_forward(z["fwd"].astype(np.int64))
         groups = [z["sizes0"].tolist(), z["sizes1"].tolist()]
     else:
         res = ref.band_k(a, 3, targets)
         perm, groups = res.perm, [list(g) for g in res.level_group_sizes]
         try:
             os.makedirs(REF_CACHE, exist_ok=True)
-            np.savez(path, fwd=perm.fwd, sizes0=np.asarray(groups[0], dtype=np.int64),
-                     sizes1=np.asarray(groups[1], dtype=np.int64))
+            np.savez_compressed(path, fwd=np.asarray(perm.fwd, dtype=np.uint32),
+                                sizes0=np.asarray(groups[0], dtype=np.int64),
+                                sizes1=np.asarray(groups[1], dtype=np.int64))
         except OSError:
             pass
     t_band = time.perf_counter() - t0

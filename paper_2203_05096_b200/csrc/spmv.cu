@@ -739,6 +739,121 @@ int launch_long_rows(const csrk_matrix *m, const V *vals, const V *x, V *y, cuda
   return CSRK_OK;
 }
 
+// ---- column-sorted panels (irregular rows) ---------------------------------
+//
+// On a matrix whose rows read x at scattered columns (C5: ~10 random columns
+// within +-65536 of the row) the streaming kernel is bound by the L1TEX
+// unit: each of a warp's 32 gathers hits its own 128-byte line, one line per
+// cycle per SM (profiles/r01_gather_probe.txt: 0.93 gathers / SM-cycle).
+// The same gathers issued in column order within a panel of ~1-2 k rows land
+// a warp's lanes on few lines: 2.1x the gather rate at 2000-row panels,
+// 2.9x at 4000 (profiles/r02_sorted_gather_probe.txt).  The order of the
+// gathers is free -- only each row's SUM order is fixed -- so a panel's
+// entries are stored a second time sorted by column with their position in
+// the panel; phase A gathers x in that order, multiplies (__dmul_rn) and
+// drops each product into shared memory at its CSR position; phase B sums
+// every row from shared memory left to right (or in the strided order) --
+// bit for bit the reference's chain.  +2 bytes per nonzero of HBM traffic
+// (the positions) buy the gather rate.
+
+template <int NX, typename V, typename RowPtr>
+__device__ __forceinline__ void sum_panel_rows(uint32_t r0, uint32_t r1, const double *prod,
+                                               RowPtr srp, V *__restrict__ y, int ct) {
+  if constexpr (NX == 0) {
+    for (uint32_t r = r0 + ct; r < r1; r += kConsumers)
+      y[r] = Elem<V>::out(row_products<double>(prod, srp(r), srp(r + 1)));
+  } else {
+    constexpr int P = pow2_ceil(NX);
+    constexpr int kSubPerWarp = 32 / P;
+    constexpr int kSubs = kConsumers / P;
+    const int lane = ct % P;
+    const int sub = ct / P;
+    const int warp_first = (ct / 32) * kSubPerWarp;
+    for (uint32_t base = r0 + warp_first; base < r1; base += kSubs) {
+      const uint32_t r = base + (sub - warp_first);
+      double acc = 0.0;
+      if (r < r1) acc = lane_products<NX, double>(prod, srp(r), srp(r + 1), lane);
+      acc = subwarp_tree<P>(acc);
+      if (r < r1 && lane == 0) y[r] = Elem<V>::out(acc);
+    }
+  }
+}
+
+template <typename V, int NX>
+__global__ void __launch_bounds__(kConsumers)
+    csrk_panel_kernel(const uint32_t *__restrict__ row_ptr, const uint32_t *__restrict__ pcol,
+                      const V *__restrict__ pval, const uint16_t *__restrict__ ppos,
+                      const V *__restrict__ x, V *__restrict__ y,
+                      const uint32_t *__restrict__ prow, const uint32_t *__restrict__ pptr,
+                      uint32_t n_panels) {
+  extern __shared__ __align__(16) double prod[];
+  const int ct = threadIdx.x;
+  constexpr int U = 8;
+  for (uint32_t t = blockIdx.x; t < n_panels; t += gridDim.x) {
+    const uint32_t r0 = prow[t], r1 = prow[t + 1], q0 = pptr[t], q1 = pptr[t + 1];
+    // phase A: gathers in column order, products to their CSR positions
+    for (uint32_t j = q0 + ct; j < q1; j += kConsumers * U) {
+      uint32_t c[U], ps[U];
+      double v[U], xv[U];
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const uint32_t q = j + k * kConsumers;
+        const uint32_t qq = q < q1 ? q : q0;  // spare lanes re-read entry q0 (one line)
+        c[k] = __ldcs(pcol + qq);
+        v[k] = static_cast<double>(__ldcs(pval + qq));
+        ps[k] = __ldcs(reinterpret_cast<const unsigned short *>(ppos) + qq);
+      }
+#pragma unroll
+      for (int k = 0; k < U; ++k) xv[k] = Elem<V>::load_x(x, c[k]);
+#pragma unroll
+      for (int k = 0; k < U; ++k)
+        if (j + k * kConsumers < q1) prod[ps[k]] = __dmul_rn(v[k], xv[k]);
+    }
+    __syncthreads();
+    // phase B: rows summed from shared memory in the reference's order
+    sum_panel_rows<NX, V>(r0, r1, prod, [&](uint32_t r) { return row_ptr[r] - q0; }, y, ct);
+    __syncthreads();  // the next panel's products overwrite these
+  }
+}
+
+__global__ void panel_keys_kernel(const uint32_t *__restrict__ col_idx, int64_t nnz,
+                                  const uint32_t *__restrict__ pptr, int64_t n_panels,
+                                  int col_bits, uint64_t *__restrict__ keys,
+                                  uint32_t *__restrict__ vals) {
+  for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < nnz;
+       p += int64_t(gridDim.x) * blockDim.x) {
+    int64_t lo = 0, hi = n_panels - 1;  // last panel whose first nonzero <= p
+    while (lo < hi) {
+      const int64_t mid = (lo + hi + 1) / 2;
+      if (pptr[mid] <= static_cast<uint64_t>(p))
+        lo = mid;
+      else
+        hi = mid - 1;
+    }
+    keys[p] = (static_cast<uint64_t>(lo) << col_bits) | col_idx[p];
+    vals[p] = static_cast<uint32_t>(p);
+  }
+}
+
+template <typename V>
+__global__ void panel_fill_kernel(const uint64_t *__restrict__ keys,
+                                  const uint32_t *__restrict__ src, int64_t nnz, int col_bits,
+                                  const uint32_t *__restrict__ pptr, const double *__restrict__ v64,
+                                  const float *__restrict__ v32, uint32_t *__restrict__ pcol,
+                                  uint16_t *__restrict__ ppos, double *__restrict__ o64,
+                                  float *__restrict__ o32) {
+  const uint64_t cmask = (uint64_t(1) << col_bits) - 1;
+  for (int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; j < nnz;
+       j += int64_t(gridDim.x) * blockDim.x) {
+    const uint64_t k = keys[j];
+    const uint32_t p = src[j];
+    pcol[j] = static_cast<uint32_t>(k & cmask);
+    ppos[j] = static_cast<uint16_t>(p - pptr[k >> col_bits]);
+    if (o64) o64[j] = v64[p];
+    if (o32) o32[j] = v32[p];
+  }
+}
+
 // ---- tile plan -------------------------------------------------------------
 
 __device__ __forceinline__ uint32_t group_start(const uint32_t *sr_ptr,
@@ -1366,6 +1481,7 @@ int prepare_plan(const csrk_matrix *cm, int value_type, int variant, int nx) {
   csrk_matrix *m = const_cast<csrk_matrix *>(cm);  // the plan is a cache
   if (m->n_rows == 0) return CSRK_OK;
   if (!m->plan.row_stats) CSRK_TRY(ensure_plan(m, 0, 0, 0, m->stream));
+  if (panels_wanted(m)) CSRK_TRY(ensure_panels(m, value_type, m->stream));
   if (!m->plan.auto_tile) return CSRK_OK;
   const int64_t tc = auto_tile_cost(m->plan.mean_short, variant, nx);
   if (tc != m->plan.tile_cost) {
@@ -1385,6 +1501,184 @@ int chunk_max_cols(const csrk_matrix *m, const uint32_t *row_cut_dev, int chunks
   return CSRK_OK;
 }
 
+// ---- panels: plan, build, launch ------------------------------------------
+
+// panel capacity (nonzeros; shared memory = 8 B each) and CTAs per SM;
+// CSRK_PANEL_CAP / CSRK_PANEL_CTAS override (sweeps)
+static int64_t panel_cap_default() {
+  static const int64_t v = [] {
+    const char *e = std::getenv("CSRK_PANEL_CAP");
+    return e ? std::max<int64_t>(512, std::min<int64_t>(std::atoll(e), 27000)) : int64_t(12288);
+  }();
+  return v;
+}
+static int panel_ctas_default() {
+  static const int v = [] {
+    const char *e = std::getenv("CSRK_PANEL_CTAS");
+    return e ? std::max(1, std::min(std::atoi(e), 8)) : 2;
+  }();
+  return v;
+}
+
+// Auto: irregular rows (variance > 10, the paper's class boundary, where
+// the gathers scatter) without rows the long-row kernel owns.  Stencils keep
+// the streaming kernel: their gathers already fall on shared lines and the
+// positions would add 2 bytes per nonzero to an HBM-bound kernel.
+bool panels_wanted(const csrk_matrix *m) {
+  if (m->n_rows == 0 || !m->plan.row_stats || m->plan.n_long > 0) return false;
+  if (m->layout == kLayoutPanels) return true;
+  if (m->layout == kLayoutStream) return false;
+  return m->plan.row_var > 10.0;
+}
+
+void free_panels(csrk_matrix *m) {
+  PanelPlan &pn = m->panel;
+  cudaFree(pn.row);
+  cudaFree(pn.col);
+  cudaFree(pn.pos);
+  cudaFree(pn.val64);
+  cudaFree(pn.val32);
+  pn = PanelPlan();
+}
+
+int ensure_panels(csrk_matrix *m, int value_type, cudaStream_t s) {
+  PanelPlan &pn = m->panel;
+  const bool need32 = value_type == CSRK_F32;
+  if (pn.built && (!need32 || pn.val32)) return CSRK_OK;
+  if (pn.built && need32 && !pn.val32 && m->vals32) {
+    // add the f32 copy in the existing order: re-run the build below
+    free_panels(m);
+  }
+  const int64_t cap = panel_cap_default();
+  // rows <= kLongRow nonzeros here (n_long == 0): a panel's cost (nonzeros +
+  // rows) stays below pitch + kLongRow + 1, so its nonzeros fit `cap`
+  const int64_t pitch = cap - (kLongRow + 1);
+  const int64_t total = m->nnz + m->n_rows;
+  const int64_t n_panels = std::max<int64_t>(1, (total + pitch - 1) / pitch);
+  CSRK_CUDA_TRY(cudaMalloc(&pn.row, 2 * (n_panels + 1) * sizeof(uint32_t)));
+  pn.ptr = pn.row + (n_panels + 1);
+  const unsigned b = static_cast<unsigned>((n_panels + 1 + 255) / 256);
+  tile_bounds_kernel<<<b, 256, 0, s>>>(m->row_ptr, m->sr_ptr, m->ssr_ptr, 1, m->n_rows,
+                                       m->n_rows, pitch, n_panels, pn.row);
+  tile_ptr_kernel<<<b, 256, 0, s>>>(m->row_ptr, pn.row, n_panels, pn.ptr);
+  CSRK_CUDA_TRY(cudaGetLastError());
+  const int64_t nnz = m->nnz;
+  int col_bits = 1;
+  while ((int64_t(1) << col_bits) < m->n_cols) ++col_bits;
+  int panel_bits = 1;
+  while ((int64_t(1) << panel_bits) < n_panels) ++panel_bits;
+  if (col_bits + panel_bits > 64) {
+    set_error("panel keys do not fit 64 bits");
+    return CSRK_EINVAL;
+  }
+  CSRK_CUDA_TRY(cudaMalloc(&pn.col, padded_nnz(nnz) * sizeof(uint32_t)));
+  CSRK_CUDA_TRY(cudaMalloc(&pn.pos, padded_nnz(nnz) * sizeof(uint16_t)));
+  if (m->vals64) CSRK_CUDA_TRY(cudaMalloc(&pn.val64, padded_nnz(nnz) * sizeof(double)));
+  if (m->vals32) CSRK_CUDA_TRY(cudaMalloc(&pn.val32, padded_nnz(nnz) * sizeof(float)));
+  if (nnz > 0) {
+    uint64_t *keys = nullptr;
+    uint32_t *vals = nullptr;
+    keep_async_pool();
+    CSRK_CUDA_TRY(cudaMallocAsync(&keys, 2 * nnz * sizeof(uint64_t), s));
+    CSRK_CUDA_TRY(cudaMallocAsync(&vals, 2 * nnz * sizeof(uint32_t), s));
+    const unsigned g = static_cast<unsigned>(std::min<int64_t>((nnz + 255) / 256, 148 * 32));
+    panel_keys_kernel<<<g, 256, 0, s>>>(m->col_idx, nnz, pn.ptr, n_panels, col_bits, keys, vals);
+    CSRK_CUDA_TRY(cudaGetLastError());
+    const int end_bit = ((col_bits + panel_bits + 7) / 8) * 8;
+    int rc = radix_sort_pairs(keys, vals, keys + nnz, vals + nnz, nnz, 0, end_bit, s);
+    if (rc == CSRK_OK) {
+      panel_fill_kernel<double><<<g, 256, 0, s>>>(keys, vals, nnz, col_bits, pn.ptr, m->vals64,
+                                                  m->vals32, pn.col, pn.pos, pn.val64, pn.val32);
+      rc = cudaGetLastError() == cudaSuccess ? CSRK_OK : CSRK_ECUDA;
+    }
+    cudaFreeAsync(keys, s);
+    cudaFreeAsync(vals, s);
+    CSRK_TRY(rc);
+  }
+  CSRK_CUDA_TRY(cudaStreamSynchronize(s));
+  pn.cap = cap;
+  pn.n_panels = n_panels;
+  pn.built = true;
+  return CSRK_OK;
+}
+
+namespace {
+
+template <typename V, int NX>
+int launch_panels_nx(const csrk_matrix *m, const V *pval, const V *x, V *y, cudaStream_t s) {
+  const PanelPlan &pn = m->panel;
+  const size_t smem = static_cast<size_t>(pn.cap) * sizeof(double);
+  auto kern = csrk_panel_kernel<V, NX>;
+  static thread_local size_t cached_smem = 0;
+  static thread_local int cached_per_sm = 0, cached_device = -1;
+  int dev = 0;
+  CSRK_CUDA_TRY(cudaGetDevice(&dev));
+  if (cached_smem != smem || cached_device != dev) {
+    CSRK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem)));
+    int smem_sm = 0;
+    CSRK_CUDA_TRY(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor,
+                                         dev));
+    const int ctas = panel_ctas_default();
+    int pct = static_cast<int>(ctas * (smem + 1024) * 100.0 / smem_sm + 0.999);
+    pct = pct < 1 ? 1 : (pct > 100 ? 100 : pct);
+    CSRK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+    int per_sm = 0;
+    CSRK_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kConsumers, smem));
+    cached_per_sm = std::min(per_sm, ctas);
+    cached_smem = smem;
+    cached_device = dev;
+  }
+  if (cached_per_sm < 1) {
+    set_error("panel kernel does not fit on an SM (%zu bytes of shared memory)", smem);
+    return CSRK_EINVAL;
+  }
+  const int64_t grid = std::min<int64_t>(int64_t(cached_per_sm) * m->sm_count, pn.n_panels);
+  kern<<<static_cast<unsigned>(grid), kConsumers, smem, s>>>(
+      m->row_ptr, pn.col, pval, pn.pos, x, y, pn.row, pn.ptr, static_cast<uint32_t>(pn.n_panels));
+  CSRK_CUDA_TRY(cudaGetLastError());
+  return CSRK_OK;
+}
+
+template <typename V>
+int launch_panels(const csrk_matrix *m, int variant, int nx, const V *pval, const V *x, V *y,
+                  cudaStream_t s) {
+  if (variant == CSRK_SERIAL) return launch_panels_nx<V, 0>(m, pval, x, y, s);
+  switch (nx) {
+#define CSRK_PANEL_CASE(N) \
+  case N:                  \
+    return launch_panels_nx<V, N>(m, pval, x, y, s);
+    CSRK_PANEL_CASE(1)
+    CSRK_PANEL_CASE(2)
+    CSRK_PANEL_CASE(3)
+    CSRK_PANEL_CASE(4)
+    CSRK_PANEL_CASE(5)
+    CSRK_PANEL_CASE(6)
+    CSRK_PANEL_CASE(7)
+    CSRK_PANEL_CASE(8)
+    CSRK_PANEL_CASE(9)
+    CSRK_PANEL_CASE(10)
+    CSRK_PANEL_CASE(11)
+    CSRK_PANEL_CASE(12)
+    CSRK_PANEL_CASE(13)
+    CSRK_PANEL_CASE(14)
+    CSRK_PANEL_CASE(15)
+    CSRK_PANEL_CASE(16)
+    CSRK_PANEL_CASE(20)
+    CSRK_PANEL_CASE(24)
+    CSRK_PANEL_CASE(28)
+    CSRK_PANEL_CASE(32)
+#undef CSRK_PANEL_CASE
+    default:
+      set_error("strided SpMV supports nx in 1..16, 20, 24, 28, 32; got %d "
+                "(use the listing-4 kernel for other block dimensions)",
+                nx);
+      return CSRK_EINVAL;
+  }
+}
+
+}  // namespace
+
 int launch_spmv(const csrk_matrix *m, int value_type, int variant, int nx,
                 const void *x, void *y, cudaStream_t stream, int64_t t0,
                 int64_t t1) {
@@ -1396,6 +1690,16 @@ int launch_spmv(const csrk_matrix *m, int value_type, int variant, int nx,
   if (!m->plan.tile_row) {
     set_error("matrix has no tile plan");
     return CSRK_EINVAL;
+  }
+  // whole-matrix launches on the column-sorted panels (built by prepare_plan)
+  const bool whole = t0 <= 0 && (t1 < 0 || t1 >= m->plan.n_tiles);
+  if (whole && m->panel.built && panels_wanted(m)) {
+    if (value_type == CSRK_F64 && m->panel.val64)
+      return launch_panels<double>(m, variant, nx, m->panel.val64, static_cast<const double *>(x),
+                                   static_cast<double *>(y), stream);
+    if (value_type == CSRK_F32 && m->panel.val32)
+      return launch_panels<float>(m, variant, nx, m->panel.val32, static_cast<const float *>(x),
+                                  static_cast<float *>(y), stream);
   }
   if (value_type == CSRK_F64) {
     if (!m->vals64) {
