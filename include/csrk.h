@@ -302,6 +302,25 @@ int csrk_cg(const csrk_matrix *m, int value_type, int variant, int nx,
 int csrk_power(const csrk_matrix *m, int value_type, int variant, int nx,
                void *x, void *y, int iters, void *stream);
 
+/* Step kernels of the distributed CG (paper_2203_05096_b200.dist.DistCG;
+ * no reference counterpart -- the C4 caller of spmv_csr3 at N GPUs).  Each
+ * finishes its reduction on the device (the last block folds the per-block
+ * partials in a fixed order: deterministic, one launch) into a caller-owned
+ * device array `scalars` = {rr, pAp, rr_new, alpha, beta}, which the
+ * caller's all-reduce updates in place between the calls:
+ *   csrk_vec_dot(p, Ap -> &scalars[1])          then all-reduce scalars[1]
+ *   csrk_cg_update(x += a p; r -= a Ap; rr_new)  then all-reduce scalars[2]
+ *   csrk_cg_direction(p = r + b p; rr = rr_new)
+ * `partials` holds >= 592 doubles, `counter` one zeroed unsigned (re-armed
+ * by every call).  Stream-ordered, no host synchronisation. */
+int csrk_vec_dot(int value_type, int64_t n, const void *a, const void *b, double *partials,
+                 unsigned *counter, double *out, void *stream);
+int csrk_cg_update(int value_type, int64_t n, void *x, void *r, const void *p,
+                   const void *ap, double *scalars, double *partials, unsigned *counter,
+                   void *stream);
+int csrk_cg_direction(int value_type, int64_t n, void *p, const void *r, double *scalars,
+                      unsigned *counter, void *stream);
+
 /* ---- Band-k reordering (native) -------------------------------------------
  * Bit-exact native restatement of reorder.py (band_k 415-469 and its
  * helpers).  Results are held in an opaque object and read back with

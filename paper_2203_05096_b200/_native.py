@@ -66,6 +66,9 @@ _SIGNATURES = {
     "csrk_matrix_group_uniform": ([P, I64, I64], C.c_int),
     "csrk_cg": ([P, C.c_int, C.c_int, C.c_int, P, P, P, P, P, C.c_int, F64P, P], C.c_int),
     "csrk_power": ([P, C.c_int, C.c_int, C.c_int, P, P, C.c_int, P], C.c_int),
+    "csrk_vec_dot": ([C.c_int, I64, P, P, P, P, P, P], C.c_int),
+    "csrk_cg_update": ([C.c_int, I64, P, P, P, P, P, P, P, P], C.c_int),
+    "csrk_cg_direction": ([C.c_int, I64, P, P, P, P, P], C.c_int),
     "csrk_dgraph_build": ([P, C.POINTER(P)], C.c_int),
     "csrk_dgraph_relabel": ([P, I64P, C.POINTER(P)], C.c_int),
     "csrk_dgraph_contract": ([P, I64P, I64, C.POINTER(P)], C.c_int),

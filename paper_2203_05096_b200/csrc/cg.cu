@@ -192,6 +192,102 @@ __global__ void scale_by_max_kernel(const T *__restrict__ y, T *__restrict__ x, 
     x[i] = static_cast<T>(static_cast<double>(y[i]) * inv);
 }
 
+// ---- step kernels of the distributed CG (dist.DistCG) -------------------
+//
+// Across GPUs every dot product is a rank-local partial followed by an
+// all-reduce, so the iteration is split where the all-reduces go: each
+// kernel below ends its own reduction on the device (the last block to
+// finish folds the per-block partials in a fixed order -- deterministic, one
+// launch), and the scalars live in a caller-owned device array that the
+// caller's NCCL all-reduce updates in place between the kernels:
+//   dot(p, Ap) -> sc[PAP]          | all-reduce sc[PAP]
+//   update     -> x, r, sc[RRNEW]  | all-reduce sc[RRNEW]
+//   direction  -> p, sc[RR] = sc[RRNEW]
+// Three launches + two all-reduces per iteration beside the SpMV, all on one
+// stream without host synchronisation (graph-capturable).
+enum { kScRR = 0, kScPAP = 1, kScRRNew = 2, kScAlpha = 3, kScBeta = 4 };
+
+// the last block of the grid to arrive folds `partials` into *out and
+// re-arms the counter
+__device__ __forceinline__ void last_block_fold(const double *partials, unsigned *counter,
+                                                double *out) {
+  __shared__ bool s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  if (threadIdx.x < 32) {
+    double v = 0.0;
+    for (unsigned i = threadIdx.x; i < gridDim.x; i += 32)
+      v += reinterpret_cast<const volatile double *>(partials)[i];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if (threadIdx.x == 0) {
+      *out = v;
+      *counter = 0u;
+    }
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kRedThreads)
+    dist_dot_kernel(const T *__restrict__ a, const T *__restrict__ b, int64_t n,
+                    double *__restrict__ partials, unsigned *counter, double *out) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    s += static_cast<double>(a[i]) * static_cast<double>(b[i]);
+  const double t = block_sum<T>(s, red);
+  if (threadIdx.x == 0) partials[blockIdx.x] = t;
+  last_block_fold(partials, counter, out);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kRedThreads)
+    dist_update_kernel(T *__restrict__ x, T *__restrict__ r, const T *__restrict__ p,
+                       const T *__restrict__ ap, int64_t n, double *__restrict__ sc,
+                       double *__restrict__ partials, unsigned *counter) {
+  __shared__ double red[32];
+  const double pap = sc[kScPAP];
+  const double alpha = pap != 0.0 ? sc[kScRR] / pap : 0.0;
+  double s = 0.0;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    x[i] = static_cast<T>(static_cast<double>(x[i]) + alpha * static_cast<double>(p[i]));
+    const double ri = static_cast<double>(r[i]) - alpha * static_cast<double>(ap[i]);
+    r[i] = static_cast<T>(ri);
+    const double rv = static_cast<double>(static_cast<T>(ri));
+    s += rv * rv;
+  }
+  const double t = block_sum<T>(s, red);
+  if (threadIdx.x == 0) partials[blockIdx.x] = t;
+  if (blockIdx.x == 0 && threadIdx.x == 0) sc[kScAlpha] = alpha;
+  last_block_fold(partials, counter, sc + kScRRNew);
+}
+
+// p = r + beta p with beta = rr' / rr; the last block publishes rr = rr'
+template <typename T>
+__global__ void __launch_bounds__(kRedThreads)
+    dist_direction_kernel(T *__restrict__ p, const T *__restrict__ r, int64_t n,
+                          double *__restrict__ sc, unsigned *counter) {
+  const double rr = sc[kScRR], rr_new = sc[kScRRNew];
+  const double beta = rr != 0.0 ? rr_new / rr : 0.0;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    p[i] = static_cast<T>(static_cast<double>(r[i]) + beta * static_cast<double>(p[i]));
+  __shared__ bool s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (s_last && threadIdx.x == 0) {  // every block has read sc[RR]
+    sc[kScBeta] = beta;
+    sc[kScRR] = rr_new;
+    *counter = 0u;
+  }
+}
+
 struct Scratch {
   double *pap_part = nullptr, *rr_part = nullptr;
   CgScalars *sc = nullptr;
@@ -324,6 +420,75 @@ int csrk_power(const csrk_matrix *m, int value_type, int variant, int nx, void *
                             static_cast<float *>(y), iters, s);
   return power_run<double>(m, value_type, variant, nx, static_cast<double *>(x),
                            static_cast<double *>(y), iters, s);
+}
+
+}  // extern "C"
+
+namespace {
+inline unsigned red_grid(int64_t n) {
+  int64_t b = (n + kRedThreads - 1) / kRedThreads;
+  return static_cast<unsigned>(b < 1 ? 1 : (b > kRedBlocks ? kRedBlocks : b));
+}
+}  // namespace
+
+extern "C" {
+
+int csrk_vec_dot(int value_type, int64_t n, const void *a, const void *b, double *partials,
+                 unsigned *counter, double *out, void *stream) {
+  if (n < 0 || (n > 0 && (!a || !b)) || !partials || !counter || !out) {
+    set_error("invalid argument to csrk_vec_dot");
+    return CSRK_EINVAL;
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const unsigned g = red_grid(n);
+  if (value_type == CSRK_F32)
+    dist_dot_kernel<float><<<g, kRedThreads, 0, s>>>(static_cast<const float *>(a),
+                                                     static_cast<const float *>(b), n,
+                                                     partials, counter, out);
+  else
+    dist_dot_kernel<double><<<g, kRedThreads, 0, s>>>(static_cast<const double *>(a),
+                                                      static_cast<const double *>(b), n,
+                                                      partials, counter, out);
+  CSRK_CUDA_TRY(cudaGetLastError());
+  return CSRK_OK;
+}
+
+int csrk_cg_update(int value_type, int64_t n, void *x, void *r, const void *p, const void *ap,
+                   double *scalars, double *partials, unsigned *counter, void *stream) {
+  if (n < 0 || (n > 0 && (!x || !r || !p || !ap)) || !scalars || !partials || !counter) {
+    set_error("invalid argument to csrk_cg_update");
+    return CSRK_EINVAL;
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const unsigned g = red_grid(n);
+  if (value_type == CSRK_F32)
+    dist_update_kernel<float><<<g, kRedThreads, 0, s>>>(
+        static_cast<float *>(x), static_cast<float *>(r), static_cast<const float *>(p),
+        static_cast<const float *>(ap), n, scalars, partials, counter);
+  else
+    dist_update_kernel<double><<<g, kRedThreads, 0, s>>>(
+        static_cast<double *>(x), static_cast<double *>(r), static_cast<const double *>(p),
+        static_cast<const double *>(ap), n, scalars, partials, counter);
+  CSRK_CUDA_TRY(cudaGetLastError());
+  return CSRK_OK;
+}
+
+int csrk_cg_direction(int value_type, int64_t n, void *p, const void *r, double *scalars,
+                      unsigned *counter, void *stream) {
+  if (n < 0 || (n > 0 && (!p || !r)) || !scalars || !counter) {
+    set_error("invalid argument to csrk_cg_direction");
+    return CSRK_EINVAL;
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const unsigned g = red_grid(n);
+  if (value_type == CSRK_F32)
+    dist_direction_kernel<float><<<g, kRedThreads, 0, s>>>(
+        static_cast<float *>(p), static_cast<const float *>(r), n, scalars, counter);
+  else
+    dist_direction_kernel<double><<<g, kRedThreads, 0, s>>>(
+        static_cast<double *>(p), static_cast<const double *>(r), n, scalars, counter);
+  CSRK_CUDA_TRY(cudaGetLastError());
+  return CSRK_OK;
 }
 
 }  // extern "C"

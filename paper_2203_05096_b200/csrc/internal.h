@@ -113,6 +113,7 @@ struct TilePlan {
 // are summed from there in the reference's order.
 struct PanelPlan {
   int64_t cap = 0;            // nonzeros per panel (shared-memory products)
+  int64_t rcap = 0;           // rows per panel
   int64_t n_panels = 0;
   uint32_t *row = nullptr;    // n_panels + 1 panel row bounds, then n_panels + 1 first nonzeros
   uint32_t *ptr = nullptr;

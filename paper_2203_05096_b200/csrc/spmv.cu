@@ -756,16 +756,16 @@ int launch_long_rows(const csrk_matrix *m, const V *vals, const V *x, V *y, cuda
 // bit for bit the reference's chain.  +2 bytes per nonzero of HBM traffic
 // (the positions) buy the gather rate.
 
-template <int NX, typename V, typename RowPtr>
+template <int NX, int NCT, typename V, typename RowPtr>
 __device__ __forceinline__ void sum_panel_rows(uint32_t r0, uint32_t r1, const double *prod,
                                                RowPtr srp, V *__restrict__ y, int ct) {
   if constexpr (NX == 0) {
-    for (uint32_t r = r0 + ct; r < r1; r += kConsumers)
+    for (uint32_t r = r0 + ct; r < r1; r += NCT)
       y[r] = Elem<V>::out(row_products<double>(prod, srp(r), srp(r + 1)));
   } else {
     constexpr int P = pow2_ceil(NX);
     constexpr int kSubPerWarp = 32 / P;
-    constexpr int kSubs = kConsumers / P;
+    constexpr int kSubs = NCT / P;
     const int lane = ct % P;
     const int sub = ct / P;
     const int warp_first = (ct / 32) * kSubPerWarp;
@@ -779,41 +779,190 @@ __device__ __forceinline__ void sum_panel_rows(uint32_t r0, uint32_t r1, const d
   }
 }
 
-template <typename V, int NX>
-__global__ void __launch_bounds__(kConsumers)
+// Panel kernel geometry: a ring of kPanelStages chunks of kPanelChunk sorted
+// entries (column, value, position), two row-pointer buffers (the current
+// panel's and the next one's) and the panel's products.
+constexpr int kPanelChunk = 2048;
+constexpr int kPanelStages = 2;
+
+template <typename V>
+struct PanelGeo {
+  uint32_t pcap, rcap;
+  uint32_t col_off, val_off, pos_off, stage_bytes, rows_off, rows_bytes, prod_off, total;
+  __host__ __device__ PanelGeo(uint32_t pcap_, uint32_t rcap_) : pcap(pcap_), rcap(rcap_) {
+    col_off = 0;
+    val_off = round_up(kPanelChunk * 4, 128);
+    pos_off = val_off + round_up(kPanelChunk * sizeof(V), 128);
+    stage_bytes = pos_off + round_up(kPanelChunk * 2, 128);
+    rows_off = 1024 + kPanelStages * stage_bytes;  // (1 KB of barriers / meta first)
+    rows_bytes = round_up((rcap + 1 + 8) * 4, 128);
+    prod_off = rows_off + 2 * rows_bytes;
+    total = prod_off + round_up(pcap * 8, 128);
+  }
+};
+
+struct PanelMeta {
+  uint32_t r0, r1, q0, q1, ra0;
+};
+
+// Warp-specialised like the streaming kernel: warp 0 streams each panel's
+// row pointers (double-buffered) and its sorted entries (a ring of 2-k
+// chunks) into shared memory with TMA bulk copies; the consumer warps read a
+// chunk into registers, free the stage, gather x and drop the products at
+// their positions -- the gathers of the next chunk are issued before the
+// products of the current one are stored, so two chunks of gathers are in
+// flight per thread -- then sum the panel's rows from shared memory.
+template <typename V, int NX, int NCW>
+__global__ void __launch_bounds__(32 * (NCW + 1), 1)
     csrk_panel_kernel(const uint32_t *__restrict__ row_ptr, const uint32_t *__restrict__ pcol,
                       const V *__restrict__ pval, const uint16_t *__restrict__ ppos,
                       const V *__restrict__ x, V *__restrict__ y,
                       const uint32_t *__restrict__ prow, const uint32_t *__restrict__ pptr,
-                      uint32_t n_panels) {
-  extern __shared__ __align__(16) double prod[];
-  const int ct = threadIdx.x;
-  constexpr int U = 8;
-  for (uint32_t t = blockIdx.x; t < n_panels; t += gridDim.x) {
-    const uint32_t r0 = prow[t], r1 = prow[t + 1], q0 = pptr[t], q1 = pptr[t + 1];
-    // phase A: gathers in column order, products to their CSR positions
-    for (uint32_t j = q0 + ct; j < q1; j += kConsumers * U) {
-      uint32_t c[U], ps[U];
-      double v[U], xv[U];
-#pragma unroll
-      for (int k = 0; k < U; ++k) {
-        const uint32_t q = j + k * kConsumers;
-        const uint32_t qq = q < q1 ? q : q0;  // spare lanes re-read entry q0 (one line)
-        c[k] = __ldcs(pcol + qq);
-        v[k] = static_cast<double>(__ldcs(pval + qq));
-        ps[k] = __ldcs(reinterpret_cast<const unsigned short *>(ppos) + qq);
-      }
-#pragma unroll
-      for (int k = 0; k < U; ++k) xv[k] = Elem<V>::load_x(x, c[k]);
-#pragma unroll
-      for (int k = 0; k < U; ++k)
-        if (j + k * kConsumers < q1) prod[ps[k]] = __dmul_rn(v[k], xv[k]);
+                      uint32_t n_panels, uint32_t pcap, uint32_t rcap) {
+  constexpr int NCT = NCW * 32;
+  constexpr int PER = kPanelChunk / NCT;  // entries per consumer thread per chunk
+  extern __shared__ __align__(128) unsigned char smem[];
+  const PanelGeo<V> geo(pcap, rcap);
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem);
+  uint64_t *empty = full + kPanelStages;
+  uint64_t *rfull = empty + kPanelStages;
+  uint64_t *rempty = rfull + 2;
+  PanelMeta *pmeta = reinterpret_cast<PanelMeta *>(rempty + 2);  // [2]
+  double *prod = reinterpret_cast<double *>(smem + geo.prod_off);
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    for (int i = 0; i < kPanelStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], NCW);
     }
-    __syncthreads();
-    // phase B: rows summed from shared memory in the reference's order
-    sum_panel_rows<NX, V>(r0, r1, prod, [&](uint32_t r) { return row_ptr[r] - q0; }, y, ct);
-    __syncthreads();  // the next panel's products overwrite these
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&rfull[i], 1);
+      mbar_init(&rempty[i], NCW);
+    }
+    fence_barrier_init();
   }
+  __syncthreads();
+  const uint32_t grid = gridDim.x;
+  if (tid < 32) {
+    // ---------------- producer ----------------
+    if (tid != 0) return;
+    const uint64_t policy = evict_first_policy();
+    uint32_t ci = 0, pi = 0;
+    for (uint32_t t = blockIdx.x; t < n_panels; t += grid, ++pi) {
+      const uint32_t r0 = prow[t], r1 = prow[t + 1], q0 = pptr[t], q1 = pptr[t + 1];
+      const uint32_t slot = pi & 1;
+      if (pi >= 2) mbar_wait(&rempty[slot], ((pi / 2) + 1) & 1);
+      const uint32_t ra0 = r0 & ~3u, ra1 = round_up(r1 + 1, 4);
+      pmeta[slot] = PanelMeta{r0, r1, q0, q1, ra0};
+      mbar_arrive_expect_tx(&rfull[slot], (ra1 - ra0) * 4u);
+      tma_bulk_load(smem + geo.rows_off + slot * geo.rows_bytes, row_ptr + ra0, (ra1 - ra0) * 4u,
+                    &rfull[slot], policy);
+      const uint32_t qend = round_up(q1, 8);
+      for (uint32_t a = q0 & ~7u; a < q1; a += kPanelChunk, ++ci) {
+        const uint32_t s = ci % kPanelStages;
+        if (ci >= kPanelStages) mbar_wait(&empty[s], ((ci / kPanelStages) + 1) & 1);
+        const uint32_t n8 = min(a + kPanelChunk, qend) - a;
+        unsigned char *st = smem + 1024 + s * geo.stage_bytes;
+        mbar_arrive_expect_tx(&full[s], n8 * (4u + static_cast<uint32_t>(sizeof(V)) + 2u));
+        tma_bulk_load(st + geo.col_off, pcol + a, n8 * 4u, &full[s], policy);
+        tma_bulk_load(st + geo.val_off, pval + a, n8 * static_cast<uint32_t>(sizeof(V)), &full[s],
+                      policy);
+        tma_bulk_load(st + geo.pos_off, ppos + a, n8 * 2u, &full[s], policy);
+      }
+    }
+    return;
+  }
+  // ---------------- consumers ----------------
+  const int ct = tid - 32;
+  uint32_t ci = 0, pi = 0;
+  for (uint32_t t = blockIdx.x; t < n_panels; t += grid, ++pi) {
+    const uint32_t slot = pi & 1;
+    mbar_wait(&rfull[slot], (pi / 2) & 1);
+    const PanelMeta pm = pmeta[slot];
+    const uint32_t *sr = reinterpret_cast<const uint32_t *>(smem + geo.rows_off +
+                                                            slot * geo.rows_bytes) - pm.ra0;
+    // phase A: chunks of sorted entries; gathers of chunk c + 1 are issued
+    // before the products of chunk c are stored
+    uint32_t ca[PER], cb[PER], pa[PER], pb[PER];
+    double va[PER], vb[PER], xa[PER], xb[PER];
+    bool oka[PER], okb[PER];
+    auto take = [&](uint32_t a, uint32_t (&c)[PER], uint32_t (&ps)[PER], double (&v)[PER],
+                    bool (&ok)[PER]) {
+      const uint32_t s = ci % kPanelStages;
+      mbar_wait(&full[s], (ci / kPanelStages) & 1);
+      const unsigned char *st = smem + 1024 + s * geo.stage_bytes;
+      const uint32_t *scol = reinterpret_cast<const uint32_t *>(st + geo.col_off);
+      const V *sval = reinterpret_cast<const V *>(st + geo.val_off);
+      const uint16_t *spos = reinterpret_cast<const uint16_t *>(st + geo.pos_off);
+#pragma unroll
+      for (int k = 0; k < PER; ++k) {
+        const uint32_t i = ct + k * NCT;
+        const uint32_t q = a + i;
+        ok[k] = q >= pm.q0 && q < pm.q1;
+        c[k] = ok[k] ? scol[i] : 0u;  // spare lanes gather x[0] (one line)
+        v[k] = static_cast<double>(sval[i]);
+        ps[k] = spos[i];
+      }
+      __syncwarp();
+      if ((ct & 31) == 0) mbar_arrive(&empty[s]);
+      ++ci;
+    };
+    uint32_t a = pm.q0 & ~7u;
+    if (a < pm.q1) {
+      take(a, ca, pa, va, oka);
+#pragma unroll
+      for (int k = 0; k < PER; ++k) xa[k] = Elem<V>::load_x(x, ca[k]);
+      for (a += kPanelChunk;; a += kPanelChunk) {
+        const bool more = a < pm.q1;
+        if (more) {
+          take(a, cb, pb, vb, okb);
+#pragma unroll
+          for (int k = 0; k < PER; ++k) xb[k] = Elem<V>::load_x(x, cb[k]);
+        }
+#pragma unroll
+        for (int k = 0; k < PER; ++k)
+          if (oka[k]) prod[pa[k]] = __dmul_rn(va[k], xa[k]);
+        if (!more) break;
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+          ca[k] = cb[k];
+          pa[k] = pb[k];
+          va[k] = vb[k];
+          xa[k] = xb[k];
+          oka[k] = okb[k];
+        }
+      }
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(NCT) : "memory");
+    // phase B: the panel's rows summed from shared memory in the reference's order
+    sum_panel_rows<NX, NCT, V>(pm.r0, pm.r1, prod, [&](uint32_t r) { return sr[r] - pm.q0; },
+                               y, ct);
+    __syncwarp();
+    if ((ct & 31) == 0) mbar_arrive(&rempty[slot]);
+    asm volatile("bar.sync 1, %0;" ::"n"(NCT) : "memory");  // products are reused
+  }
+}
+
+// prow[t] = first row whose cost row_ptr[r] + w * r reaches t * pitch
+__global__ void panel_bounds_kernel(const uint32_t *__restrict__ row_ptr, int64_t n_rows,
+                                    int64_t w, int64_t pitch, int64_t n_panels,
+                                    uint32_t *__restrict__ prow) {
+  const int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (t > n_panels) return;
+  if (t == n_panels) {
+    prow[t] = static_cast<uint32_t>(n_rows);
+    return;
+  }
+  const int64_t target = t * pitch;
+  int64_t lo = 0, hi = n_rows;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) / 2;
+    if (static_cast<int64_t>(row_ptr[mid]) + w * mid >= target)
+      hi = mid;
+    else
+      lo = mid + 1;
+  }
+  prow[t] = static_cast<uint32_t>(lo);
 }
 
 __global__ void panel_keys_kernel(const uint32_t *__restrict__ col_idx, int64_t nnz,
@@ -1503,19 +1652,29 @@ int chunk_max_cols(const csrk_matrix *m, const uint32_t *row_cut_dev, int chunks
 
 // ---- panels: plan, build, launch ------------------------------------------
 
-// panel capacity (nonzeros; shared memory = 8 B each) and CTAs per SM;
-// CSRK_PANEL_CAP / CSRK_PANEL_CTAS override (sweeps)
+// panel capacity (nonzeros: shared-memory products of 8 B each), consumer
+// warps per CTA and CTAs per SM; CSRK_PANEL_CAP / _WARPS / _CTAS override
+// (sweeps).  A panel also holds at most cap / kPanelRowWeight rows (its row
+// pointers are staged next to the products).
+constexpr int64_t kPanelRowWeight = 2;
 static int64_t panel_cap_default() {
   static const int64_t v = [] {
     const char *e = std::getenv("CSRK_PANEL_CAP");
-    return e ? std::max<int64_t>(512, std::min<int64_t>(std::atoll(e), 27000)) : int64_t(12288);
+    return e ? std::max<int64_t>(1024, std::min<int64_t>(std::atoll(e), 14336)) : int64_t(12288);
+  }();
+  return v;
+}
+static int panel_warps_default() {
+  static const int v = [] {
+    const char *e = std::getenv("CSRK_PANEL_WARPS");
+    return e && std::atoi(e) == 8 ? 8 : 16;
   }();
   return v;
 }
 static int panel_ctas_default() {
   static const int v = [] {
     const char *e = std::getenv("CSRK_PANEL_CTAS");
-    return e ? std::max(1, std::min(std::atoi(e), 8)) : 2;
+    return e ? std::max(1, std::min(std::atoi(e), 4)) : 1;
   }();
   return v;
 }
@@ -1545,21 +1704,19 @@ int ensure_panels(csrk_matrix *m, int value_type, cudaStream_t s) {
   PanelPlan &pn = m->panel;
   const bool need32 = value_type == CSRK_F32;
   if (pn.built && (!need32 || pn.val32)) return CSRK_OK;
-  if (pn.built && need32 && !pn.val32 && m->vals32) {
-    // add the f32 copy in the existing order: re-run the build below
-    free_panels(m);
-  }
+  if (pn.built) free_panels(m);  // rebuilt with the f32 copy as well
   const int64_t cap = panel_cap_default();
-  // rows <= kLongRow nonzeros here (n_long == 0): a panel's cost (nonzeros +
-  // rows) stays below pitch + kLongRow + 1, so its nonzeros fit `cap`
-  const int64_t pitch = cap - (kLongRow + 1);
-  const int64_t total = m->nnz + m->n_rows;
+  const int64_t w = kPanelRowWeight;
+  // rows <= kLongRow nonzeros here (n_long == 0): a panel's cost (nonzeros
+  // + w rows) stays below pitch + kLongRow + w, so its nonzeros fit `cap`
+  // and its rows cap / w
+  const int64_t pitch = cap - (kLongRow + w);
+  const int64_t total = m->nnz + w * m->n_rows;
   const int64_t n_panels = std::max<int64_t>(1, (total + pitch - 1) / pitch);
   CSRK_CUDA_TRY(cudaMalloc(&pn.row, 2 * (n_panels + 1) * sizeof(uint32_t)));
   pn.ptr = pn.row + (n_panels + 1);
   const unsigned b = static_cast<unsigned>((n_panels + 1 + 255) / 256);
-  tile_bounds_kernel<<<b, 256, 0, s>>>(m->row_ptr, m->sr_ptr, m->ssr_ptr, 1, m->n_rows,
-                                       m->n_rows, pitch, n_panels, pn.row);
+  panel_bounds_kernel<<<b, 256, 0, s>>>(m->row_ptr, m->n_rows, w, pitch, n_panels, pn.row);
   tile_ptr_kernel<<<b, 256, 0, s>>>(m->row_ptr, pn.row, n_panels, pn.ptr);
   CSRK_CUDA_TRY(cudaGetLastError());
   const int64_t nnz = m->nnz;
@@ -1571,10 +1728,20 @@ int ensure_panels(csrk_matrix *m, int value_type, cudaStream_t s) {
     set_error("panel keys do not fit 64 bits");
     return CSRK_EINVAL;
   }
-  CSRK_CUDA_TRY(cudaMalloc(&pn.col, padded_nnz(nnz) * sizeof(uint32_t)));
-  CSRK_CUDA_TRY(cudaMalloc(&pn.pos, padded_nnz(nnz) * sizeof(uint16_t)));
-  if (m->vals64) CSRK_CUDA_TRY(cudaMalloc(&pn.val64, padded_nnz(nnz) * sizeof(double)));
-  if (m->vals32) CSRK_CUDA_TRY(cudaMalloc(&pn.val32, padded_nnz(nnz) * sizeof(float)));
+  // (+kPanelChunk: a panel's last chunk is read whole by the consumers)
+  const int64_t padded = padded_nnz(nnz) + kPanelChunk;
+  CSRK_CUDA_TRY(cudaMalloc(&pn.col, padded * sizeof(uint32_t)));
+  CSRK_CUDA_TRY(cudaMalloc(&pn.pos, padded * sizeof(uint16_t)));
+  CSRK_CUDA_TRY(cudaMemsetAsync(pn.col, 0, padded * sizeof(uint32_t), s));
+  CSRK_CUDA_TRY(cudaMemsetAsync(pn.pos, 0, padded * sizeof(uint16_t), s));
+  if (m->vals64) {
+    CSRK_CUDA_TRY(cudaMalloc(&pn.val64, padded * sizeof(double)));
+    CSRK_CUDA_TRY(cudaMemsetAsync(pn.val64, 0, padded * sizeof(double), s));
+  }
+  if (m->vals32) {
+    CSRK_CUDA_TRY(cudaMalloc(&pn.val32, padded * sizeof(float)));
+    CSRK_CUDA_TRY(cudaMemsetAsync(pn.val32, 0, padded * sizeof(float), s));
+  }
   if (nnz > 0) {
     uint64_t *keys = nullptr;
     uint32_t *vals = nullptr;
@@ -1597,6 +1764,7 @@ int ensure_panels(csrk_matrix *m, int value_type, cudaStream_t s) {
   }
   CSRK_CUDA_TRY(cudaStreamSynchronize(s));
   pn.cap = cap;
+  pn.rcap = cap / w;
   pn.n_panels = n_panels;
   pn.built = true;
   return CSRK_OK;
@@ -1604,11 +1772,12 @@ int ensure_panels(csrk_matrix *m, int value_type, cudaStream_t s) {
 
 namespace {
 
-template <typename V, int NX>
+template <typename V, int NX, int NCW>
 int launch_panels_nx(const csrk_matrix *m, const V *pval, const V *x, V *y, cudaStream_t s) {
   const PanelPlan &pn = m->panel;
-  const size_t smem = static_cast<size_t>(pn.cap) * sizeof(double);
-  auto kern = csrk_panel_kernel<V, NX>;
+  const PanelGeo<V> geo(static_cast<uint32_t>(pn.cap), static_cast<uint32_t>(pn.rcap));
+  const size_t smem = geo.total;
+  auto kern = csrk_panel_kernel<V, NX, NCW>;
   static thread_local size_t cached_smem = 0;
   static thread_local int cached_per_sm = 0, cached_device = -1;
   int dev = 0;
@@ -1624,7 +1793,8 @@ int launch_panels_nx(const csrk_matrix *m, const V *pval, const V *x, V *y, cuda
     pct = pct < 1 ? 1 : (pct > 100 ? 100 : pct);
     CSRK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
     int per_sm = 0;
-    CSRK_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kConsumers, smem));
+    CSRK_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * (NCW + 1),
+                                                                smem));
     cached_per_sm = std::min(per_sm, ctas);
     cached_smem = smem;
     cached_device = dev;
@@ -1634,20 +1804,27 @@ int launch_panels_nx(const csrk_matrix *m, const V *pval, const V *x, V *y, cuda
     return CSRK_EINVAL;
   }
   const int64_t grid = std::min<int64_t>(int64_t(cached_per_sm) * m->sm_count, pn.n_panels);
-  kern<<<static_cast<unsigned>(grid), kConsumers, smem, s>>>(
-      m->row_ptr, pn.col, pval, pn.pos, x, y, pn.row, pn.ptr, static_cast<uint32_t>(pn.n_panels));
+  kern<<<static_cast<unsigned>(grid), 32 * (NCW + 1), smem, s>>>(
+      m->row_ptr, pn.col, pval, pn.pos, x, y, pn.row, pn.ptr, static_cast<uint32_t>(pn.n_panels),
+      static_cast<uint32_t>(pn.cap), static_cast<uint32_t>(pn.rcap));
   CSRK_CUDA_TRY(cudaGetLastError());
   return CSRK_OK;
+}
+
+template <typename V, int NX>
+int launch_panels_w(const csrk_matrix *m, const V *pval, const V *x, V *y, cudaStream_t s) {
+  return panel_warps_default() == 8 ? launch_panels_nx<V, NX, 8>(m, pval, x, y, s)
+                                    : launch_panels_nx<V, NX, 16>(m, pval, x, y, s);
 }
 
 template <typename V>
 int launch_panels(const csrk_matrix *m, int variant, int nx, const V *pval, const V *x, V *y,
                   cudaStream_t s) {
-  if (variant == CSRK_SERIAL) return launch_panels_nx<V, 0>(m, pval, x, y, s);
+  if (variant == CSRK_SERIAL) return launch_panels_w<V, 0>(m, pval, x, y, s);
   switch (nx) {
 #define CSRK_PANEL_CASE(N) \
   case N:                  \
-    return launch_panels_nx<V, N>(m, pval, x, y, s);
+    return launch_panels_w<V, N>(m, pval, x, y, s);
     CSRK_PANEL_CASE(1)
     CSRK_PANEL_CASE(2)
     CSRK_PANEL_CASE(3)

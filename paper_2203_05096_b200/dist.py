@@ -31,6 +31,7 @@ weak-scaling bench (a C2-sized slab per GPU) and of the multi-GPU CG (C4).
 
 from __future__ import annotations
 
+import ctypes as C
 import os
 from dataclasses import dataclass
 
@@ -43,6 +44,7 @@ __all__ = [
     "SlabExchange",
     "SlabSpMV",
     "DistCG",
+    "DeviceCgSteps",
     "partition_by_nnz",
     "footprints",
     "halo_plan",
@@ -184,6 +186,9 @@ class SlabSpMV:
         self.t_lo, self.t_hi = interior_tiles(self.dev.tile_rows(), *lay.interior_rows())
         self.exchange = SlabExchange(lay, group)
         self._pipe = None
+        self.own = slice(lay.own_off, lay.own_off + lay.n_own)
+        self.n_own = lay.n_own
+        self.n_local_cols = lay.n_cols
 
     def step(self, x_local, y_own):
         """Exchange the halo planes while the interior tiles run, then the
@@ -284,56 +289,140 @@ class SlabSpMV:
         return y_host
 
 
-class DistCG:
-    """Conjugate gradients on a slab-partitioned operator (BASELINE config
-    C4: repeated SpMVs as a CG inner loop, at N GPUs).
+class DeviceCgSteps:
+    """The device step kernels of csrc/cg.cu behind DistCG (raw pointers,
+    the caller's current stream)."""
 
-    ``op`` has ``.lay`` (a SlabLayout) and ``.step(x_local, y_own)`` (halo
-    exchange + local SpMV).  Vectors are this rank's slices; the search
-    direction lives in a local-x buffer so its halo planes can be exchanged.
-    The two dot products per iteration are all-reduced over the ranks; all
-    scalars stay on the device (no host synchronisation per iteration).
-    Classic CG, the same recurrence as csrk_cg (csrc/cg.cu)."""
+    RED_BLOCKS = 592  # csrc/cg.cu kRedBlocks
 
-    def __init__(self, op, group=None):
-        self.op, self.group = op, group
-
-    def _dot(self, a, b):
+    def __init__(self, device):
         import torch
+
+        self.sc = torch.zeros(8, dtype=torch.float64, device=device)
+        self.part = torch.zeros(self.RED_BLOCKS, dtype=torch.float64, device=device)
+        self.cnt = torch.zeros(4, dtype=torch.int32, device=device)
+
+    @staticmethod
+    def _args(t):
+        import torch
+
+        from . import _native as nat
+
+        vt = nat.CSRK_F32 if t.dtype == torch.float32 else nat.CSRK_F64
+        s = C.c_void_p(torch.cuda.current_stream(t.device).cuda_stream)
+        return vt, s
+
+    def dot(self, a, b, slot: int):
+        from . import _native as nat
+
+        vt, s = self._args(a)
+        nat.call("csrk_vec_dot", vt, a.numel(), C.c_void_p(a.data_ptr()),
+                 C.c_void_p(b.data_ptr()), C.c_void_p(self.part.data_ptr()),
+                 C.c_void_p(self.cnt.data_ptr()), C.c_void_p(self.sc.data_ptr() + 8 * slot), s)
+
+    def update(self, x, r, p, ap):
+        from . import _native as nat
+
+        vt, s = self._args(x)
+        nat.call("csrk_cg_update", vt, x.numel(), C.c_void_p(x.data_ptr()),
+                 C.c_void_p(r.data_ptr()), C.c_void_p(p.data_ptr()), C.c_void_p(ap.data_ptr()),
+                 C.c_void_p(self.sc.data_ptr()), C.c_void_p(self.part.data_ptr()),
+                 C.c_void_p(self.cnt.data_ptr()), s)
+
+    def direction(self, p, r):
+        from . import _native as nat
+
+        vt, s = self._args(p)
+        nat.call("csrk_cg_direction", vt, p.numel(), C.c_void_p(p.data_ptr()),
+                 C.c_void_p(r.data_ptr()), C.c_void_p(self.sc.data_ptr()),
+                 C.c_void_p(self.cnt.data_ptr()), s)
+
+
+class DistCG:
+    """Conjugate gradients on a partitioned operator (BASELINE config C4:
+    repeated SpMVs as a CG inner loop, at N GPUs).
+
+    ``op`` is a SlabSpMV or a DistSpMV: ``.own`` (the owned slice of its
+    local x), ``.n_local_cols``, ``.n_own`` and ``.step(x_local, y_own)``
+    (halo exchange overlapped with the interior tiles, then the boundary
+    tiles).  The search direction lives in a local-x buffer so its halo can
+    be exchanged; the other vectors are this rank's slices.  Per iteration:
+    the SpMV, then the device step kernels of csrc/cg.cu (csrk_vec_dot,
+    csrk_cg_update, csrk_cg_direction -- each finishes its reduction on the
+    device) with one NCCL all-reduce of a device scalar after the first two:
+    no host synchronisation, so :meth:`graphed` captures the whole run into
+    one CUDA graph.  The recurrence is csrk_cg's (classic CG).  ``steps``
+    replaces the step kernels (the CPU tests pass a host stand-in)."""
+
+    def __init__(self, op, group=None, steps=None):
         import torch.distributed as dist
 
-        d = torch.dot(a.double(), b.double()).reshape(1)
-        if dist.is_initialized():
-            dist.all_reduce(d, group=self.group)
-        return d
+        self.op, self.group = op, group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self._steps = steps
+
+    def _allreduce(self, t):
+        import torch.distributed as dist
+
+        if self.world > 1:
+            dist.all_reduce(t, group=self.group)
+
+    def scratch(self, b_own):
+        import torch
+
+        return (torch.zeros(self.op.n_local_cols, dtype=b_own.dtype, device=b_own.device),
+                torch.empty_like(b_own), torch.empty_like(b_own))
 
     def run(self, b_own, x_own, iters: int, scratch=None):
         """``iters`` CG iterations from x_own (updated in place); returns
-        (x_own, rr) with rr the device tensor of the last r.r."""
+        (x_own, rr) with rr the device scalar of the last r.r."""
         import torch
 
-        lay = self.op.lay
-        own = slice(lay.own_off, lay.own_off + lay.n_own)
-        if scratch is None:
-            scratch = (torch.zeros(lay.n_cols, dtype=b_own.dtype, device=b_own.device),
-                       torch.empty_like(b_own), torch.empty_like(b_own))
-        p_local, r, ap = scratch
-        p = p_local[own]
+        op = self.op
+        if self._steps is None:
+            self._steps = DeviceCgSteps(b_own.device)
+        st = self._steps
+        sc = st.sc
+        p_local, r, ap = scratch if scratch is not None else self.scratch(b_own)
+        p = p_local[op.own]
         p.copy_(x_own)
-        self.op.step(p_local, ap)  # ap = A x0
+        op.step(p_local, ap)  # ap = A x0
         torch.sub(b_own, ap, out=r)
         p.copy_(r)
-        rr = self._dot(r, r)
+        st.dot(r, r, 0)
+        self._allreduce(sc[0:1])
         for _ in range(iters):
-            self.op.step(p_local, ap)
-            alpha = (rr / self._dot(p, ap)).to(p.dtype)
-            x_own.addcmul_(p, alpha)  # x += alpha p (no temporaries)
-            r.addcmul_(ap, alpha, value=-1.0)
-            rr_new = self._dot(r, r)
-            beta = (rr_new / rr).to(p.dtype)
-            torch.addcmul(r, p, beta, out=p)  # p = r + beta p
-            rr = rr_new
-        return x_own, rr
+            op.step(p_local, ap)
+            st.dot(p, ap, 1)
+            self._allreduce(sc[1:2])
+            st.update(x_own, r, p, ap)
+            self._allreduce(sc[2:3])
+            st.direction(p, r)
+        return x_own, sc[0:1]
+
+    def graphed(self, b_own, x_own, iters: int, scratch=None):
+        """The whole run (x_own reset to 0, the initial residual, ``iters``
+        iterations) captured once into a CUDA graph -- SpMV launches, halo
+        point-to-point, all-reduces and step kernels; returns the graph
+        (``.replay()``)."""
+        import torch
+
+        scratch = scratch if scratch is not None else self.scratch(b_own)
+        s = torch.cuda.Stream(device=b_own.device)
+        s.wait_stream(torch.cuda.current_stream(b_own.device))
+        with torch.cuda.stream(s):  # warm-up outside the capture (plans, comms)
+            x_own.zero_()
+            self.run(b_own, x_own, iters, scratch)
+        torch.cuda.current_stream(b_own.device).wait_stream(s)
+        torch.cuda.synchronize(b_own.device)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            x_own.zero_()
+            self.run(b_own, x_own, iters, scratch)
+        return g
+
+    def launches_per_iteration(self) -> int:
+        return self.op.launches_per_step + 3
 
 
 def partition_by_nnz(row_ptr, sr_ptr, ssr_ptr, n_parts: int) -> np.ndarray:

@@ -367,6 +367,10 @@ class _HostSlabOp:
         self.lay = D.SlabLayout.of(shape, rank, world)
         self.rp, self.ci, self.va, _ = _host_slab(shape, points, self.lay)
         self.ex = D.SlabExchange(self.lay)
+        self.own = slice(self.lay.own_off, self.lay.own_off + self.lay.n_own)
+        self.n_own = self.lay.n_own
+        self.n_local_cols = self.lay.n_cols
+        self.launches_per_step = 1
 
     def step(self, x_local, y_own):
         if self.lay.world > 1:
@@ -374,6 +378,30 @@ class _HostSlabOp:
         y_own.copy_(torch.from_numpy(O.spmv_serial(self.rp, self.ci, self.va,
                                                    x_local.numpy())))
         return y_own
+
+
+class _HostCgSteps:
+    """CPU stand-in for dist.DeviceCgSteps: the same step semantics (the
+    reduction folded into sc, rr published by the direction step)."""
+
+    def __init__(self):
+        self.sc = torch.zeros(8, dtype=torch.float64)
+
+    def dot(self, a, b, slot):
+        self.sc[slot] = torch.dot(a.double(), b.double())
+
+    def update(self, x, r, p, ap):
+        pap = float(self.sc[1])
+        alpha = float(self.sc[0]) / pap if pap != 0.0 else 0.0
+        x.add_(p, alpha=alpha)
+        r.add_(ap, alpha=-alpha)
+        self.sc[2] = torch.dot(r.double(), r.double())
+
+    def direction(self, p, r):
+        rr, rr_new = float(self.sc[0]), float(self.sc[2])
+        beta = rr_new / rr if rr != 0.0 else 0.0
+        p.mul_(beta).add_(r)
+        self.sc[0] = rr_new
 
 
 def _cg_worker(rank, world, port, shape, iters, result_q):
@@ -387,7 +415,7 @@ def _cg_worker(rank, world, port, shape, iters, result_q):
         g0 = op.lay.global_row0
         b_own = torch.from_numpy(b[g0:g0 + op.lay.n_own].copy())
         x_own = torch.zeros_like(b_own)
-        x_own, rr = D.DistCG(op).run(b_own, x_own, iters)
+        x_own, rr = D.DistCG(op, steps=_HostCgSteps()).run(b_own, x_own, iters)
         result_q.put((rank, g0, x_own.numpy(), float(rr.item())))
     finally:
         dist.destroy_process_group()

@@ -579,7 +579,7 @@ def test_panel_layout_bitwise(layout, kind):
     np.testing.assert_array_equal(ck.spmv_csr3(m, x), O.spmv_serial(b.row_ptr, b.col_idx,
                                                                     b.vals, x))
     plan = dev.plan()
-    irregular = kind != "stencil"
+    irregular = ck.compute_stats(b).variance > 10.0  # the auto rule's class boundary
     assert plan["panels"] == int(layout == 1 or (layout == 2 and irregular))
     if plan["panels"]:
         assert plan["n_panels"] >= 1
