@@ -783,7 +783,7 @@ __device__ __forceinline__ void sum_panel_rows(uint32_t r0, uint32_t r1, const d
 // entries (column, value, position), two row-pointer buffers (the current
 // panel's and the next one's) and the panel's products.
 constexpr int kPanelChunk = 2048;
-constexpr int kPanelStages = 2;
+constexpr int kPanelStages = 3;  // two chunks held by the consumers, one filling
 
 template <typename V>
 struct PanelGeo {
@@ -886,8 +886,12 @@ __global__ void __launch_bounds__(32 * (NCW + 1), 1)
     uint32_t ca[PER], cb[PER], pa[PER], pb[PER];
     double va[PER], vb[PER], xa[PER], xb[PER];
     bool oka[PER], okb[PER];
+    // a chunk's stage is released only after its products are stored: the
+    // values read from the stage are then consumed (a release right after
+    // the shared loads raced with the next TMA fill -- compute-sanitizer
+    // racecheck, wrong rows)
     auto take = [&](uint32_t a, uint32_t (&c)[PER], uint32_t (&ps)[PER], double (&v)[PER],
-                    bool (&ok)[PER]) {
+                    bool (&ok)[PER]) -> uint32_t {
       const uint32_t s = ci % kPanelStages;
       mbar_wait(&full[s], (ci / kPanelStages) & 1);
       const unsigned char *st = smem + 1024 + s * geo.stage_bytes;
@@ -903,26 +907,31 @@ __global__ void __launch_bounds__(32 * (NCW + 1), 1)
         v[k] = static_cast<double>(sval[i]);
         ps[k] = spos[i];
       }
+      ++ci;
+      return s;
+    };
+    auto release = [&](uint32_t s) {
       __syncwarp();
       if ((ct & 31) == 0) mbar_arrive(&empty[s]);
-      ++ci;
     };
     uint32_t a = pm.q0 & ~7u;
     if (a < pm.q1) {
-      take(a, ca, pa, va, oka);
+      uint32_t sa = take(a, ca, pa, va, oka), sb = 0;
 #pragma unroll
       for (int k = 0; k < PER; ++k) xa[k] = Elem<V>::load_x(x, ca[k]);
       for (a += kPanelChunk;; a += kPanelChunk) {
         const bool more = a < pm.q1;
         if (more) {
-          take(a, cb, pb, vb, okb);
+          sb = take(a, cb, pb, vb, okb);
 #pragma unroll
           for (int k = 0; k < PER; ++k) xb[k] = Elem<V>::load_x(x, cb[k]);
         }
 #pragma unroll
         for (int k = 0; k < PER; ++k)
           if (oka[k]) prod[pa[k]] = __dmul_rn(va[k], xa[k]);
+        release(sa);
         if (!more) break;
+        sa = sb;
 #pragma unroll
         for (int k = 0; k < PER; ++k) {
           ca[k] = cb[k];
@@ -1660,7 +1669,7 @@ constexpr int64_t kPanelRowWeight = 2;
 static int64_t panel_cap_default() {
   static const int64_t v = [] {
     const char *e = std::getenv("CSRK_PANEL_CAP");
-    return e ? std::max<int64_t>(1024, std::min<int64_t>(std::atoll(e), 14336)) : int64_t(12288);
+    return e ? std::max<int64_t>(1024, std::min<int64_t>(std::atoll(e), 10240)) : int64_t(10240);
   }();
   return v;
 }
