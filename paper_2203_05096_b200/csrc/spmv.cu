@@ -780,10 +780,12 @@ __device__ __forceinline__ void sum_panel_rows(uint32_t r0, uint32_t r1, const d
 }
 
 // Panel kernel geometry: a ring of kPanelStages chunks of kPanelChunk sorted
-// entries (column, value, position), two row-pointer buffers (the current
-// panel's and the next one's) and the panel's products.
-constexpr int kPanelChunk = 2048;
-constexpr int kPanelStages = 3;  // two chunks held by the consumers, one filling
+// entries (column, value, position, plus the chunk's panel meta), two
+// row-pointer buffers (the current panel's and the next one's) and the
+// panel's products.
+constexpr int kPanelChunk = 1024;
+constexpr int kPanelStages = 4;
+constexpr int kPanelDepth = kPanelStages - 1;  // chunks whose gathers are in flight
 
 template <typename V>
 struct PanelGeo {
@@ -805,13 +807,21 @@ struct PanelMeta {
   uint32_t r0, r1, q0, q1, ra0;
 };
 
-// Warp-specialised like the streaming kernel: warp 0 streams each panel's
-// row pointers (double-buffered) and its sorted entries (a ring of 2-k
-// chunks) into shared memory with TMA bulk copies; the consumer warps read a
-// chunk into registers, free the stage, gather x and drop the products at
-// their positions -- the gathers of the next chunk are issued before the
-// products of the current one are stored, so two chunks of gathers are in
-// flight per thread -- then sum the panel's rows from shared memory.
+struct ChunkMeta {
+  uint32_t a, q0, q1, n8;  // first entry (8-aligned), the panel's entries, entries loaded
+};
+
+// Warp-specialised like the streaming kernel.  Warp 0 streams, per panel,
+// its row pointers (double-buffered) and its sorted entries (a ring of
+// 1-k-entry chunks, at least one chunk per panel) into shared memory with
+// TMA bulk copies.  The consumer warps walk the CTA's chunk sequence with
+// kPanelDepth chunks of gathers in flight: a chunk is "issued" (columns read
+// from its stage, x gathered into registers) and retired kPanelDepth steps
+// later (values and positions re-read from the stage -- it is still held --,
+// products dropped into shared memory at their CSR positions, stage
+// released).  When the chunk being retired starts a new panel, the previous
+// panel's rows are summed from shared memory first -- while the newer
+// chunks' gathers are still in flight.
 template <typename V, int NX, int NCW>
 __global__ void __launch_bounds__(32 * (NCW + 1), 1)
     csrk_panel_kernel(const uint32_t *__restrict__ row_ptr, const uint32_t *__restrict__ pcol,
@@ -821,6 +831,7 @@ __global__ void __launch_bounds__(32 * (NCW + 1), 1)
                       uint32_t n_panels, uint32_t pcap, uint32_t rcap) {
   constexpr int NCT = NCW * 32;
   constexpr int PER = kPanelChunk / NCT;  // entries per consumer thread per chunk
+  constexpr int D = kPanelDepth;
   extern __shared__ __align__(128) unsigned char smem[];
   const PanelGeo<V> geo(pcap, rcap);
   uint64_t *full = reinterpret_cast<uint64_t *>(smem);
@@ -828,6 +839,7 @@ __global__ void __launch_bounds__(32 * (NCW + 1), 1)
   uint64_t *rfull = empty + kPanelStages;
   uint64_t *rempty = rfull + 2;
   PanelMeta *pmeta = reinterpret_cast<PanelMeta *>(rempty + 2);  // [2]
+  ChunkMeta *cmeta = reinterpret_cast<ChunkMeta *>(pmeta + 2);  // [kPanelStages]
   double *prod = reinterpret_cast<double *>(smem + geo.prod_off);
   const int tid = threadIdx.x;
   if (tid == 0) {
@@ -858,98 +870,118 @@ __global__ void __launch_bounds__(32 * (NCW + 1), 1)
       tma_bulk_load(smem + geo.rows_off + slot * geo.rows_bytes, row_ptr + ra0, (ra1 - ra0) * 4u,
                     &rfull[slot], policy);
       const uint32_t qend = round_up(q1, 8);
-      for (uint32_t a = q0 & ~7u; a < q1; a += kPanelChunk, ++ci) {
+      uint32_t a = q0 & ~7u;
+      do {  // at least one chunk per panel (an empty one carries the panel)
         const uint32_t s = ci % kPanelStages;
         if (ci >= kPanelStages) mbar_wait(&empty[s], ((ci / kPanelStages) + 1) & 1);
-        const uint32_t n8 = min(a + kPanelChunk, qend) - a;
+        const uint32_t n8 = a < q1 ? min(a + kPanelChunk, qend) - a : 0u;
+        cmeta[s] = ChunkMeta{a, q0, q1, n8};
         unsigned char *st = smem + 1024 + s * geo.stage_bytes;
-        mbar_arrive_expect_tx(&full[s], n8 * (4u + static_cast<uint32_t>(sizeof(V)) + 2u));
-        tma_bulk_load(st + geo.col_off, pcol + a, n8 * 4u, &full[s], policy);
-        tma_bulk_load(st + geo.val_off, pval + a, n8 * static_cast<uint32_t>(sizeof(V)), &full[s],
-                      policy);
-        tma_bulk_load(st + geo.pos_off, ppos + a, n8 * 2u, &full[s], policy);
-      }
+        if (n8) {
+          mbar_arrive_expect_tx(&full[s], n8 * (4u + static_cast<uint32_t>(sizeof(V)) + 2u));
+          tma_bulk_load(st + geo.col_off, pcol + a, n8 * 4u, &full[s], policy);
+          tma_bulk_load(st + geo.val_off, pval + a, n8 * static_cast<uint32_t>(sizeof(V)),
+                        &full[s], policy);
+          tma_bulk_load(st + geo.pos_off, ppos + a, n8 * 2u, &full[s], policy);
+        } else {
+          mbar_arrive(&full[s]);
+        }
+        a += kPanelChunk;
+        ++ci;
+      } while (a < q1);
     }
     return;
   }
   // ---------------- consumers ----------------
   const int ct = tid - 32;
-  uint32_t ci = 0, pi = 0;
-  for (uint32_t t = blockIdx.x; t < n_panels; t += grid, ++pi) {
+  // the CTA's chunk sequence (the producer's): panels blockIdx.x, + grid,
+  // ...; a panel's chunks run until the next start passes its last entry
+  uint32_t nt = blockIdx.x, npi = 0;
+  uint32_t issue_ci = 0;  // ring index of the next chunk to issue
+  struct Ref {
+    uint32_t s, pi;
+    bool valid;
+  };
+  Ref ref[D];
+  double xr[D][PER];
+#pragma unroll
+  for (int d = 0; d < D; ++d) ref[d].valid = false;
+  int64_t cur_pi = -1;  // panel whose products are being accumulated
+
+  auto finish_panel = [&](uint32_t pi) {
+    asm volatile("bar.sync 1, %0;" ::"n"(NCT) : "memory");  // all products stored
     const uint32_t slot = pi & 1;
     mbar_wait(&rfull[slot], (pi / 2) & 1);
     const PanelMeta pm = pmeta[slot];
     const uint32_t *sr = reinterpret_cast<const uint32_t *>(smem + geo.rows_off +
                                                             slot * geo.rows_bytes) - pm.ra0;
-    // phase A: chunks of sorted entries; gathers of chunk c + 1 are issued
-    // before the products of chunk c are stored
-    uint32_t ca[PER], cb[PER], pa[PER], pb[PER];
-    double va[PER], vb[PER], xa[PER], xb[PER];
-    bool oka[PER], okb[PER];
-    // a chunk's stage is released only after its products are stored: the
-    // values read from the stage are then consumed (a release right after
-    // the shared loads raced with the next TMA fill -- compute-sanitizer
-    // racecheck, wrong rows)
-    auto take = [&](uint32_t a, uint32_t (&c)[PER], uint32_t (&ps)[PER], double (&v)[PER],
-                    bool (&ok)[PER]) -> uint32_t {
-      const uint32_t s = ci % kPanelStages;
-      mbar_wait(&full[s], (ci / kPanelStages) & 1);
-      const unsigned char *st = smem + 1024 + s * geo.stage_bytes;
-      const uint32_t *scol = reinterpret_cast<const uint32_t *>(st + geo.col_off);
-      const V *sval = reinterpret_cast<const V *>(st + geo.val_off);
-      const uint16_t *spos = reinterpret_cast<const uint16_t *>(st + geo.pos_off);
-#pragma unroll
-      for (int k = 0; k < PER; ++k) {
-        const uint32_t i = ct + k * NCT;
-        const uint32_t q = a + i;
-        ok[k] = q >= pm.q0 && q < pm.q1;
-        c[k] = ok[k] ? scol[i] : 0u;  // spare lanes gather x[0] (one line)
-        v[k] = static_cast<double>(sval[i]);
-        ps[k] = spos[i];
-      }
-      ++ci;
-      return s;
-    };
-    auto release = [&](uint32_t s) {
-      __syncwarp();
-      if ((ct & 31) == 0) mbar_arrive(&empty[s]);
-    };
-    uint32_t a = pm.q0 & ~7u;
-    if (a < pm.q1) {
-      uint32_t sa = take(a, ca, pa, va, oka), sb = 0;
-#pragma unroll
-      for (int k = 0; k < PER; ++k) xa[k] = Elem<V>::load_x(x, ca[k]);
-      for (a += kPanelChunk;; a += kPanelChunk) {
-        const bool more = a < pm.q1;
-        if (more) {
-          sb = take(a, cb, pb, vb, okb);
-#pragma unroll
-          for (int k = 0; k < PER; ++k) xb[k] = Elem<V>::load_x(x, cb[k]);
-        }
-#pragma unroll
-        for (int k = 0; k < PER; ++k)
-          if (oka[k]) prod[pa[k]] = __dmul_rn(va[k], xa[k]);
-        release(sa);
-        if (!more) break;
-        sa = sb;
-#pragma unroll
-        for (int k = 0; k < PER; ++k) {
-          ca[k] = cb[k];
-          pa[k] = pb[k];
-          va[k] = vb[k];
-          xa[k] = xb[k];
-          oka[k] = okb[k];
-        }
-      }
-    }
-    asm volatile("bar.sync 1, %0;" ::"n"(NCT) : "memory");
-    // phase B: the panel's rows summed from shared memory in the reference's order
     sum_panel_rows<NX, NCT, V>(pm.r0, pm.r1, prod, [&](uint32_t r) { return sr[r] - pm.q0; },
                                y, ct);
     __syncwarp();
     if ((ct & 31) == 0) mbar_arrive(&rempty[slot]);
     asm volatile("bar.sync 1, %0;" ::"n"(NCT) : "memory");  // products are reused
+  };
+
+  auto issue = [&](Ref &rf, double (&xv)[PER]) {
+    rf.valid = nt < n_panels;
+    if (!rf.valid) return;
+    rf.pi = npi;
+    rf.s = issue_ci % kPanelStages;
+    mbar_wait(&full[rf.s], (issue_ci / kPanelStages) & 1);
+    ++issue_ci;
+    const ChunkMeta cm = cmeta[rf.s];
+    const uint32_t *scol =
+        reinterpret_cast<const uint32_t *>(smem + 1024 + rf.s * geo.stage_bytes + geo.col_off);
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const uint32_t i = ct + k * NCT;
+      const uint32_t q = cm.a + i;
+      const uint32_t c = (i < cm.n8 && q >= cm.q0 && q < cm.q1) ? scol[i] : 0u;
+      xv[k] = Elem<V>::load_x(x, c);  // spare lanes gather x[0] (one line)
+    }
+    if (cm.a + kPanelChunk >= cm.q1) {  // the panel's last chunk
+      nt += grid;
+      ++npi;
+    }
+  };
+
+  auto retire = [&](const Ref &rf, const double (&xv)[PER]) {
+    if (static_cast<int64_t>(rf.pi) != cur_pi) {
+      if (cur_pi >= 0) finish_panel(static_cast<uint32_t>(cur_pi));
+      cur_pi = rf.pi;
+    }
+    const ChunkMeta cm = cmeta[rf.s];
+    const unsigned char *st = smem + 1024 + rf.s * geo.stage_bytes;
+    const V *sval = reinterpret_cast<const V *>(st + geo.val_off);
+    const uint16_t *spos = reinterpret_cast<const uint16_t *>(st + geo.pos_off);
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const uint32_t i = ct + k * NCT;
+      const uint32_t q = cm.a + i;
+      if (i < cm.n8 && q >= cm.q0 && q < cm.q1)
+        prod[spos[i]] = __dmul_rn(static_cast<double>(sval[i]), xv[k]);
+    }
+    __syncwarp();
+    if ((ct & 31) == 0) mbar_arrive(&empty[rf.s]);
+  };
+
+  // prologue: D chunks in flight
+#pragma unroll
+  for (int d = 0; d < D; ++d) issue(ref[d], xr[d]);
+  while (ref[0].valid) {
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      if (ref[d].valid) {
+        retire(ref[d], xr[d]);
+        issue(ref[d], xr[d]);
+      }
+    }
   }
+  // (ref[0] invalid: the remaining valid slots, if any, are newer)
+#pragma unroll
+  for (int d = 1; d < D; ++d)
+    if (ref[d].valid) retire(ref[d], xr[d]);
+  if (cur_pi >= 0) finish_panel(static_cast<uint32_t>(cur_pi));
 }
 
 // prow[t] = first row whose cost row_ptr[r] + w * r reaches t * pitch
@@ -1669,7 +1701,7 @@ constexpr int64_t kPanelRowWeight = 2;
 static int64_t panel_cap_default() {
   static const int64_t v = [] {
     const char *e = std::getenv("CSRK_PANEL_CAP");
-    return e ? std::max<int64_t>(1024, std::min<int64_t>(std::atoll(e), 10240)) : int64_t(10240);
+    return e ? std::max<int64_t>(1024, std::min<int64_t>(std::atoll(e), 13312)) : int64_t(10240);
   }();
   return v;
 }
