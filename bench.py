@@ -245,8 +245,6 @@ def run_ours(args, log):
     xd = torch.from_numpy(xp).to("cuda", dtype)
     yd = torch.empty(n, dtype=dtype, device="cuda")
     stream = torch.cuda.current_stream()
-    if os.environ.get("CSRK_LAYOUT"):  # sweeps: force the whole-matrix layout
-        m.device().set_layout(int(os.environ["CSRK_LAYOUT"]))
 
     def step():
         ck.spmv_device(m, xd, yd, dims=dims, variant=variant, stream=stream)
@@ -338,11 +336,10 @@ def run_ours(args, log):
                    "config_id": args.config, "n_rows": n, "nnz": nnz,
                    "ssrs_target": params.ssrs, "srs_target": params.srs,
                    "n_sr": m.num_super_rows, "n_ssr": m.num_ssr,
-                   "kernel": ("csrk_panel_kernel" if m.device().plan()["panels"]
-                              else "csrk_stream_kernel") + f" ({variant})",
+                   "kernel": f"csrk_stream_kernel ({variant})",
                    "plan": {k: v for k, v in m.device().plan().items()
                             if k in ("tile_cost", "stages", "n_tiles", "group_aligned",
-                                     "gather_first", "ctas_per_sm", "panels", "n_panels")},
+                                     "gather_first", "ctas_per_sm", "n_long")},
                    "parallelism": "1 GPU",
                    "l2": ("inputs larger than L2 (algorithmic %.2f GB per step vs 126 MB "
                           "L2); no flush" % (algo_bytes / 1e9)) if not flush else

@@ -111,9 +111,8 @@ int csrk_matrix_set_plan(csrk_matrix *m, int64_t tile_cost, int64_t cap,
                          int64_t stages);
 /* out = tile_cost, cap, rcap, stages, n_tiles, group_aligned, gather mode,
  *       ctas_per_sm (the f64 value when auto), cut mode, n_long (rows
- *       longer than 128 nonzeros, summed by the long-row kernel), whether
- *       whole-matrix launches use the column-sorted panels, n_panels built */
-int csrk_matrix_plan(const csrk_matrix *m, int64_t out[12]);
+ *       longer than 128 nonzeros, summed by the long-row kernel) */
+int csrk_matrix_plan(const csrk_matrix *m, int64_t out[10]);
 /* Schedule of the streaming kernel (B200 tuning knobs with no reference
  * counterpart; results are bitwise identical under every setting).
  * gather: 0 = inline (each row gathers its x while summing), 1 = gather-first
@@ -132,14 +131,6 @@ int csrk_matrix_set_schedule(csrk_matrix *m, int gather, int ctas_per_sm);
  * largest group so a tile still fits its stage).  Results are bitwise the
  * same; this is the A/B knob of DESIGN.md §7. */
 int csrk_matrix_set_cut_mode(csrk_matrix *m, int mode);
-/* Layout of whole-matrix launches: 0 = the streaming tiles (TMA-staged CSR),
- * 1 = column-sorted panels (a second copy of the entries, sorted by column
- * within panels of ~12 k nonzeros, with their in-panel positions: the x
- * gathers of a warp then share 128-byte lines; products are summed in the
- * reference's order from shared memory -- bitwise the same y), 2 = auto
- * (default: panels for irregular rows -- variance > 10 -- without rows
- * longer than 128 nonzeros).  Tile-range launches always stream. */
-int csrk_matrix_set_layout(csrk_matrix *m, int layout);
 /* Build (or rebuild) the tile plan a launch with this value type / order /
  * nx would use, without launching: csrk_spmv_tiles and
  * csrk_matrix_tile_rows then index exactly that plan. */

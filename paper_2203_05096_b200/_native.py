@@ -49,7 +49,6 @@ _SIGNATURES = {
     "csrk_matrix_plan": ([P, I64P], C.c_int),
     "csrk_matrix_set_schedule": ([P, C.c_int, C.c_int], C.c_int),
     "csrk_matrix_set_cut_mode": ([P, C.c_int], C.c_int),
-    "csrk_matrix_set_layout": ([P, C.c_int], C.c_int),
     "csrk_matrix_prepare": ([P, C.c_int, C.c_int, C.c_int], C.c_int),
     "csrk_spmv": ([P, C.c_int, C.c_int, C.c_int, P, P, P], C.c_int),
     "csrk_spmv_tiles": ([P, C.c_int, C.c_int, C.c_int, P, P, I64, I64, P], C.c_int),
@@ -291,20 +290,15 @@ class DeviceMatrix:
         """Tile cuts: 0 auto, 1 rows, 2 group (SSR) boundaries (include/csrk.h)."""
         call("csrk_matrix_set_cut_mode", self.ptr, int(mode))
 
-    def set_layout(self, layout: int):
-        """Whole-matrix launches: 0 streaming tiles, 1 column-sorted panels,
-        2 auto (include/csrk.h)."""
-        call("csrk_matrix_set_layout", self.ptr, int(layout))
-
     def prepare(self, variant=CSRK_SERIAL, nx=1, f32=False):
         """Build the tile plan a launch of this order would use (no launch)."""
         call("csrk_matrix_prepare", self.ptr, CSRK_F32 if f32 else CSRK_F64, variant, nx)
 
     def plan(self) -> dict:
-        out = np.zeros(12, dtype=np.int64)
+        out = np.zeros(10, dtype=np.int64)
         call("csrk_matrix_plan", self.ptr, i64p(out))
         keys = ("tile_cost", "cap", "rcap", "stages", "n_tiles", "group_aligned",
-                "gather_first", "ctas_per_sm", "cut_mode", "n_long", "panels", "n_panels")
+                "gather_first", "ctas_per_sm", "cut_mode", "n_long")
         return {k: int(v) for k, v in zip(keys, out)}
 
     def stats(self):

@@ -58,7 +58,6 @@ static void release(csrk_matrix *m) {
   cudaFree(m->ssr_ptr);
   cudaFree(m->plan.tile_row);
   cudaFree(m->plan.long_rows);
-  csrk::free_panels(m);
   cudaFree(m->x_stage);
   cudaFree(m->y_stage);
   for (auto e : m->pipe.ev_x) cudaEventDestroy(e);
@@ -650,7 +649,7 @@ int csrk_spmv_host(csrk_matrix *m, int value_type, int variant, int nx,
   return CSRK_OK;
 }
 
-int csrk_matrix_plan(const csrk_matrix *m, int64_t out[12]) {
+int csrk_matrix_plan(const csrk_matrix *m, int64_t out[10]) {
   if (!m || !out) {
     set_error("null argument");
     return CSRK_EINVAL;
@@ -665,8 +664,6 @@ int csrk_matrix_plan(const csrk_matrix *m, int64_t out[12]) {
   out[7] = m->plan.ctas_per_sm ? m->plan.ctas_per_sm : auto_ctas(m->plan.row_var, 8);
   out[8] = m->plan.cut_mode;
   out[9] = m->plan.n_long;
-  out[10] = csrk::panels_wanted(m) ? 1 : 0;
-  out[11] = m->panel.built ? m->panel.n_panels : 0;
   return CSRK_OK;
 }
 
@@ -689,21 +686,6 @@ int csrk_matrix_set_cut_mode(csrk_matrix *m, int mode) {
   CSRK_TRY(ensure_plan(m, m->plan.tile_cost, m->plan.cap, m->plan.stages, m->stream, true));
   m->plan.auto_tile = keep;
   CSRK_CUDA_TRY(cudaStreamSynchronize(m->stream));
-  return CSRK_OK;
-}
-
-int csrk_matrix_set_layout(csrk_matrix *m, int layout) {
-  if (!m) {
-    set_error("null argument");
-    return CSRK_EINVAL;
-  }
-  if (layout < 0 || layout > 2) {
-    set_error("layout must be 0 (streaming tiles), 1 (column-sorted panels) or 2 (auto), "
-              "got %d", layout);
-    return CSRK_EINVAL;
-  }
-  CSRK_LOCK(m);
-  m->layout = layout;
   return CSRK_OK;
 }
 

@@ -105,28 +105,6 @@ struct TilePlan {
   int64_t n_long = 0;
 };
 
-// Column-sorted panels (the gather layout for irregular rows, csrc/spmv.cu
-// "panels"): contiguous row ranges of at most `cap` nonzeros whose entries
-// are stored a second time sorted by column (stable), with each entry's
-// position inside the panel, so a warp's 32 x gathers fall on few 128-byte
-// lines.  Products land in shared memory at their CSR positions and rows
-// are summed from there in the reference's order.
-struct PanelPlan {
-  int64_t cap = 0;            // nonzeros per panel (shared-memory products)
-  int64_t rcap = 0;           // rows per panel
-  int64_t n_panels = 0;
-  uint32_t *row = nullptr;    // n_panels + 1 panel row bounds, then n_panels + 1 first nonzeros
-  uint32_t *ptr = nullptr;
-  uint32_t *col = nullptr;    // nnz: columns in per-panel sorted order
-  uint16_t *pos = nullptr;    // nnz: position of the entry inside its panel
-  double *val64 = nullptr;    // nnz: values in the same order
-  float *val32 = nullptr;     // optional
-  bool built = false;
-};
-
-// layouts of whole-matrix launches (csrk_matrix_set_layout)
-constexpr int kLayoutStream = 0, kLayoutPanels = 1, kLayoutAuto = 2;
-
 // the holes (uint2 pairs) follow the work order at an 8-byte boundary
 inline const uint2 *long_holes(const TilePlan &pl) {
   return reinterpret_cast<const uint2 *>(pl.long_rows + ((pl.n_long + 1) & ~int64_t(1)));
@@ -150,8 +128,6 @@ struct csrk_matrix {
   uint32_t *sr_ptr = nullptr;   // n_sr + 1 (k >= 2)
   uint32_t *ssr_ptr = nullptr;  // n_ssr + 1 (k == 3)
   csrk::TilePlan plan;          // current streaming plan
-  csrk::PanelPlan panel;        // column-sorted panels (irregular rows)
-  int layout = csrk::kLayoutAuto;
   int sm_count = 0;
   // host-API staging and the overlapped host pipeline (csrk_spmv_host)
   struct Pipe {
@@ -236,11 +212,6 @@ int ensure_plan(csrk_matrix *m, int64_t tile_cost, int64_t cap, int64_t stages,
 // before a whole-matrix launch: re-plan for the launch's order when the plan
 // is automatic (cached; rebuilds only when the tile cost changes)
 int prepare_plan(const csrk_matrix *m, int value_type, int variant, int nx);
-// whether a whole-matrix launch uses the column-sorted panels, and their
-// construction (prepare_plan builds them when they will be used)
-bool panels_wanted(const csrk_matrix *m);
-int ensure_panels(csrk_matrix *m, int value_type, cudaStream_t s);
-void free_panels(csrk_matrix *m);
 int launch_spmv(const csrk_matrix *m, int value_type, int variant, int nx,
                 const void *x, void *y, cudaStream_t stream, int64_t t0 = 0,
                 int64_t t1 = -1);

@@ -739,311 +739,6 @@ int launch_long_rows(const csrk_matrix *m, const V *vals, const V *x, V *y, cuda
   return CSRK_OK;
 }
 
-// ---- column-sorted panels (irregular rows) ---------------------------------
-//
-// On a matrix whose rows read x at scattered columns (C5: ~10 random columns
-// within +-65536 of the row) the streaming kernel is bound by the L1TEX
-// unit: each of a warp's 32 gathers hits its own 128-byte line, one line per
-// cycle per SM (profiles/r01_gather_probe.txt: 0.93 gathers / SM-cycle).
-// The same gathers issued in column order within a panel of ~1-2 k rows land
-// a warp's lanes on few lines: 2.1x the gather rate at 2000-row panels,
-// 2.9x at 4000 (profiles/r02_sorted_gather_probe.txt).  The order of the
-// gathers is free -- only each row's SUM order is fixed -- so a panel's
-// entries are stored a second time sorted by column with their position in
-// the panel; phase A gathers x in that order, multiplies (__dmul_rn) and
-// drops each product into shared memory at its CSR position; phase B sums
-// every row from shared memory left to right (or in the strided order) --
-// bit for bit the reference's chain.  +2 bytes per nonzero of HBM traffic
-// (the positions) buy the gather rate.
-
-template <int NX, int NCT, typename V, typename RowPtr>
-__device__ __forceinline__ void sum_panel_rows(uint32_t r0, uint32_t r1, const double *prod,
-                                               RowPtr srp, V *__restrict__ y, int ct) {
-  if constexpr (NX == 0) {
-    for (uint32_t r = r0 + ct; r < r1; r += NCT)
-      y[r] = Elem<V>::out(row_products<double>(prod, srp(r), srp(r + 1)));
-  } else {
-    constexpr int P = pow2_ceil(NX);
-    constexpr int kSubPerWarp = 32 / P;
-    constexpr int kSubs = NCT / P;
-    const int lane = ct % P;
-    const int sub = ct / P;
-    const int warp_first = (ct / 32) * kSubPerWarp;
-    for (uint32_t base = r0 + warp_first; base < r1; base += kSubs) {
-      const uint32_t r = base + (sub - warp_first);
-      double acc = 0.0;
-      if (r < r1) acc = lane_products<NX, double>(prod, srp(r), srp(r + 1), lane);
-      acc = subwarp_tree<P>(acc);
-      if (r < r1 && lane == 0) y[r] = Elem<V>::out(acc);
-    }
-  }
-}
-
-// Panel kernel geometry: a ring of kPanelStages chunks of kPanelChunk sorted
-// entries (column, value, position, plus the chunk's panel meta), two
-// row-pointer buffers (the current panel's and the next one's) and the
-// panel's products.
-constexpr int kPanelChunk = 1024;
-constexpr int kPanelStages = 4;
-constexpr int kPanelDepth = kPanelStages - 1;  // chunks whose gathers are in flight
-
-template <typename V>
-struct PanelGeo {
-  uint32_t pcap, rcap;
-  uint32_t col_off, val_off, pos_off, stage_bytes, rows_off, rows_bytes, prod_off, total;
-  __host__ __device__ PanelGeo(uint32_t pcap_, uint32_t rcap_) : pcap(pcap_), rcap(rcap_) {
-    col_off = 0;
-    val_off = round_up(kPanelChunk * 4, 128);
-    pos_off = val_off + round_up(kPanelChunk * sizeof(V), 128);
-    stage_bytes = pos_off + round_up(kPanelChunk * 2, 128);
-    rows_off = 1024 + kPanelStages * stage_bytes;  // (1 KB of barriers / meta first)
-    rows_bytes = round_up((rcap + 1 + 8) * 4, 128);
-    prod_off = rows_off + 2 * rows_bytes;
-    total = prod_off + round_up(pcap * 8, 128);
-  }
-};
-
-struct PanelMeta {
-  uint32_t r0, r1, q0, q1, ra0;
-};
-
-struct ChunkMeta {
-  uint32_t a, q0, q1, n8;  // first entry (8-aligned), the panel's entries, entries loaded
-};
-
-// Warp-specialised like the streaming kernel.  Warp 0 streams, per panel,
-// its row pointers (double-buffered) and its sorted entries (a ring of
-// 1-k-entry chunks, at least one chunk per panel) into shared memory with
-// TMA bulk copies.  The consumer warps walk the CTA's chunk sequence with
-// kPanelDepth chunks of gathers in flight: a chunk is "issued" (columns read
-// from its stage, x gathered into registers) and retired kPanelDepth steps
-// later (values and positions re-read from the stage -- it is still held --,
-// products dropped into shared memory at their CSR positions, stage
-// released).  When the chunk being retired starts a new panel, the previous
-// panel's rows are summed from shared memory first -- while the newer
-// chunks' gathers are still in flight.
-template <typename V, int NX, int NCW>
-__global__ void __launch_bounds__(32 * (NCW + 1), 1)
-    csrk_panel_kernel(const uint32_t *__restrict__ row_ptr, const uint32_t *__restrict__ pcol,
-                      const V *__restrict__ pval, const uint16_t *__restrict__ ppos,
-                      const V *__restrict__ x, V *__restrict__ y,
-                      const uint32_t *__restrict__ prow, const uint32_t *__restrict__ pptr,
-                      uint32_t n_panels, uint32_t pcap, uint32_t rcap) {
-  constexpr int NCT = NCW * 32;
-  constexpr int PER = kPanelChunk / NCT;  // entries per consumer thread per chunk
-  constexpr int D = kPanelDepth;
-  extern __shared__ __align__(128) unsigned char smem[];
-  const PanelGeo<V> geo(pcap, rcap);
-  uint64_t *full = reinterpret_cast<uint64_t *>(smem);
-  uint64_t *empty = full + kPanelStages;
-  uint64_t *rfull = empty + kPanelStages;
-  uint64_t *rempty = rfull + 2;
-  PanelMeta *pmeta = reinterpret_cast<PanelMeta *>(rempty + 2);  // [2]
-  ChunkMeta *cmeta = reinterpret_cast<ChunkMeta *>(pmeta + 2);  // [kPanelStages]
-  double *prod = reinterpret_cast<double *>(smem + geo.prod_off);
-  const int tid = threadIdx.x;
-  if (tid == 0) {
-    for (int i = 0; i < kPanelStages; ++i) {
-      mbar_init(&full[i], 1);
-      mbar_init(&empty[i], NCW);
-    }
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&rfull[i], 1);
-      mbar_init(&rempty[i], NCW);
-    }
-    fence_barrier_init();
-  }
-  __syncthreads();
-  const uint32_t grid = gridDim.x;
-  if (tid < 32) {
-    // ---------------- producer ----------------
-    if (tid != 0) return;
-    const uint64_t policy = evict_first_policy();
-    uint32_t ci = 0, pi = 0;
-    for (uint32_t t = blockIdx.x; t < n_panels; t += grid, ++pi) {
-      const uint32_t r0 = prow[t], r1 = prow[t + 1], q0 = pptr[t], q1 = pptr[t + 1];
-      const uint32_t slot = pi & 1;
-      if (pi >= 2) mbar_wait(&rempty[slot], ((pi / 2) + 1) & 1);
-      const uint32_t ra0 = r0 & ~3u, ra1 = round_up(r1 + 1, 4);
-      pmeta[slot] = PanelMeta{r0, r1, q0, q1, ra0};
-      mbar_arrive_expect_tx(&rfull[slot], (ra1 - ra0) * 4u);
-      tma_bulk_load(smem + geo.rows_off + slot * geo.rows_bytes, row_ptr + ra0, (ra1 - ra0) * 4u,
-                    &rfull[slot], policy);
-      const uint32_t qend = round_up(q1, 8);
-      uint32_t a = q0 & ~7u;
-      do {  // at least one chunk per panel (an empty one carries the panel)
-        const uint32_t s = ci % kPanelStages;
-        if (ci >= kPanelStages) mbar_wait(&empty[s], ((ci / kPanelStages) + 1) & 1);
-        const uint32_t n8 = a < q1 ? min(a + kPanelChunk, qend) - a : 0u;
-        cmeta[s] = ChunkMeta{a, q0, q1, n8};
-        unsigned char *st = smem + 1024 + s * geo.stage_bytes;
-        if (n8) {
-          mbar_arrive_expect_tx(&full[s], n8 * (4u + static_cast<uint32_t>(sizeof(V)) + 2u));
-          tma_bulk_load(st + geo.col_off, pcol + a, n8 * 4u, &full[s], policy);
-          tma_bulk_load(st + geo.val_off, pval + a, n8 * static_cast<uint32_t>(sizeof(V)),
-                        &full[s], policy);
-          tma_bulk_load(st + geo.pos_off, ppos + a, n8 * 2u, &full[s], policy);
-        } else {
-          mbar_arrive(&full[s]);
-        }
-        a += kPanelChunk;
-        ++ci;
-      } while (a < q1);
-    }
-    return;
-  }
-  // ---------------- consumers ----------------
-  const int ct = tid - 32;
-  // the CTA's chunk sequence (the producer's): panels blockIdx.x, + grid,
-  // ...; a panel's chunks run until the next start passes its last entry
-  uint32_t nt = blockIdx.x, npi = 0;
-  uint32_t issue_ci = 0;  // ring index of the next chunk to issue
-  struct Ref {
-    uint32_t s, pi;
-    bool valid;
-  };
-  Ref ref[D];
-  double xr[D][PER];
-#pragma unroll
-  for (int d = 0; d < D; ++d) ref[d].valid = false;
-  int64_t cur_pi = -1;  // panel whose products are being accumulated
-
-  auto finish_panel = [&](uint32_t pi) {
-    asm volatile("bar.sync 1, %0;" ::"n"(NCT) : "memory");  // all products stored
-    const uint32_t slot = pi & 1;
-    mbar_wait(&rfull[slot], (pi / 2) & 1);
-    const PanelMeta pm = pmeta[slot];
-    const uint32_t *sr = reinterpret_cast<const uint32_t *>(smem + geo.rows_off +
-                                                            slot * geo.rows_bytes) - pm.ra0;
-    sum_panel_rows<NX, NCT, V>(pm.r0, pm.r1, prod, [&](uint32_t r) { return sr[r] - pm.q0; },
-                               y, ct);
-    __syncwarp();
-    if ((ct & 31) == 0) mbar_arrive(&rempty[slot]);
-    asm volatile("bar.sync 1, %0;" ::"n"(NCT) : "memory");  // products are reused
-  };
-
-  auto issue = [&](Ref &rf, double (&xv)[PER]) {
-    rf.valid = nt < n_panels;
-    if (!rf.valid) return;
-    rf.pi = npi;
-    rf.s = issue_ci % kPanelStages;
-    mbar_wait(&full[rf.s], (issue_ci / kPanelStages) & 1);
-    ++issue_ci;
-    const ChunkMeta cm = cmeta[rf.s];
-    const uint32_t *scol =
-        reinterpret_cast<const uint32_t *>(smem + 1024 + rf.s * geo.stage_bytes + geo.col_off);
-#pragma unroll
-    for (int k = 0; k < PER; ++k) {
-      const uint32_t i = ct + k * NCT;
-      const uint32_t q = cm.a + i;
-      const uint32_t c = (i < cm.n8 && q >= cm.q0 && q < cm.q1) ? scol[i] : 0u;
-      xv[k] = Elem<V>::load_x(x, c);  // spare lanes gather x[0] (one line)
-    }
-    if (cm.a + kPanelChunk >= cm.q1) {  // the panel's last chunk
-      nt += grid;
-      ++npi;
-    }
-  };
-
-  auto retire = [&](const Ref &rf, const double (&xv)[PER]) {
-    if (static_cast<int64_t>(rf.pi) != cur_pi) {
-      if (cur_pi >= 0) finish_panel(static_cast<uint32_t>(cur_pi));
-      cur_pi = rf.pi;
-    }
-    const ChunkMeta cm = cmeta[rf.s];
-    const unsigned char *st = smem + 1024 + rf.s * geo.stage_bytes;
-    const V *sval = reinterpret_cast<const V *>(st + geo.val_off);
-    const uint16_t *spos = reinterpret_cast<const uint16_t *>(st + geo.pos_off);
-#pragma unroll
-    for (int k = 0; k < PER; ++k) {
-      const uint32_t i = ct + k * NCT;
-      const uint32_t q = cm.a + i;
-      if (i < cm.n8 && q >= cm.q0 && q < cm.q1)
-        prod[spos[i]] = __dmul_rn(static_cast<double>(sval[i]), xv[k]);
-    }
-    __syncwarp();
-    if ((ct & 31) == 0) mbar_arrive(&empty[rf.s]);
-  };
-
-  // prologue: D chunks in flight
-#pragma unroll
-  for (int d = 0; d < D; ++d) issue(ref[d], xr[d]);
-  while (ref[0].valid) {
-#pragma unroll
-    for (int d = 0; d < D; ++d) {
-      if (ref[d].valid) {
-        retire(ref[d], xr[d]);
-        issue(ref[d], xr[d]);
-      }
-    }
-  }
-  // (ref[0] invalid: the remaining valid slots, if any, are newer)
-#pragma unroll
-  for (int d = 1; d < D; ++d)
-    if (ref[d].valid) retire(ref[d], xr[d]);
-  if (cur_pi >= 0) finish_panel(static_cast<uint32_t>(cur_pi));
-}
-
-// prow[t] = first row whose cost row_ptr[r] + w * r reaches t * pitch
-__global__ void panel_bounds_kernel(const uint32_t *__restrict__ row_ptr, int64_t n_rows,
-                                    int64_t w, int64_t pitch, int64_t n_panels,
-                                    uint32_t *__restrict__ prow) {
-  const int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  if (t > n_panels) return;
-  if (t == n_panels) {
-    prow[t] = static_cast<uint32_t>(n_rows);
-    return;
-  }
-  const int64_t target = t * pitch;
-  int64_t lo = 0, hi = n_rows;
-  while (lo < hi) {
-    const int64_t mid = (lo + hi) / 2;
-    if (static_cast<int64_t>(row_ptr[mid]) + w * mid >= target)
-      hi = mid;
-    else
-      lo = mid + 1;
-  }
-  prow[t] = static_cast<uint32_t>(lo);
-}
-
-__global__ void panel_keys_kernel(const uint32_t *__restrict__ col_idx, int64_t nnz,
-                                  const uint32_t *__restrict__ pptr, int64_t n_panels,
-                                  int col_bits, uint64_t *__restrict__ keys,
-                                  uint32_t *__restrict__ vals) {
-  for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < nnz;
-       p += int64_t(gridDim.x) * blockDim.x) {
-    int64_t lo = 0, hi = n_panels - 1;  // last panel whose first nonzero <= p
-    while (lo < hi) {
-      const int64_t mid = (lo + hi + 1) / 2;
-      if (pptr[mid] <= static_cast<uint64_t>(p))
-        lo = mid;
-      else
-        hi = mid - 1;
-    }
-    keys[p] = (static_cast<uint64_t>(lo) << col_bits) | col_idx[p];
-    vals[p] = static_cast<uint32_t>(p);
-  }
-}
-
-template <typename V>
-__global__ void panel_fill_kernel(const uint64_t *__restrict__ keys,
-                                  const uint32_t *__restrict__ src, int64_t nnz, int col_bits,
-                                  const uint32_t *__restrict__ pptr, const double *__restrict__ v64,
-                                  const float *__restrict__ v32, uint32_t *__restrict__ pcol,
-                                  uint16_t *__restrict__ ppos, double *__restrict__ o64,
-                                  float *__restrict__ o32) {
-  const uint64_t cmask = (uint64_t(1) << col_bits) - 1;
-  for (int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; j < nnz;
-       j += int64_t(gridDim.x) * blockDim.x) {
-    const uint64_t k = keys[j];
-    const uint32_t p = src[j];
-    pcol[j] = static_cast<uint32_t>(k & cmask);
-    ppos[j] = static_cast<uint16_t>(p - pptr[k >> col_bits]);
-    if (o64) o64[j] = v64[p];
-    if (o32) o32[j] = v32[p];
-  }
-}
-
 // ---- tile plan -------------------------------------------------------------
 
 __device__ __forceinline__ uint32_t group_start(const uint32_t *sr_ptr,
@@ -1671,7 +1366,6 @@ int prepare_plan(const csrk_matrix *cm, int value_type, int variant, int nx) {
   csrk_matrix *m = const_cast<csrk_matrix *>(cm);  // the plan is a cache
   if (m->n_rows == 0) return CSRK_OK;
   if (!m->plan.row_stats) CSRK_TRY(ensure_plan(m, 0, 0, 0, m->stream));
-  if (panels_wanted(m)) CSRK_TRY(ensure_panels(m, value_type, m->stream));
   if (!m->plan.auto_tile) return CSRK_OK;
   const int64_t tc = auto_tile_cost(m->plan.mean_short, variant, nx);
   if (tc != m->plan.tile_cost) {
@@ -1691,212 +1385,6 @@ int chunk_max_cols(const csrk_matrix *m, const uint32_t *row_cut_dev, int chunks
   return CSRK_OK;
 }
 
-// ---- panels: plan, build, launch ------------------------------------------
-
-// panel capacity (nonzeros: shared-memory products of 8 B each), consumer
-// warps per CTA and CTAs per SM; CSRK_PANEL_CAP / _WARPS / _CTAS override
-// (sweeps).  A panel also holds at most cap / kPanelRowWeight rows (its row
-// pointers are staged next to the products).
-constexpr int64_t kPanelRowWeight = 2;
-static int64_t panel_cap_default() {
-  static const int64_t v = [] {
-    const char *e = std::getenv("CSRK_PANEL_CAP");
-    return e ? std::max<int64_t>(1024, std::min<int64_t>(std::atoll(e), 13312)) : int64_t(10240);
-  }();
-  return v;
-}
-static int panel_warps_default() {
-  static const int v = [] {
-    const char *e = std::getenv("CSRK_PANEL_WARPS");
-    return e && std::atoi(e) == 8 ? 8 : 16;
-  }();
-  return v;
-}
-static int panel_ctas_default() {
-  static const int v = [] {
-    const char *e = std::getenv("CSRK_PANEL_CTAS");
-    return e ? std::max(1, std::min(std::atoi(e), 4)) : 1;
-  }();
-  return v;
-}
-
-// Auto: irregular rows (variance > 10, the paper's class boundary, where
-// the gathers scatter) without rows the long-row kernel owns.  Stencils keep
-// the streaming kernel: their gathers already fall on shared lines and the
-// positions would add 2 bytes per nonzero to an HBM-bound kernel.
-bool panels_wanted(const csrk_matrix *m) {
-  if (m->n_rows == 0 || !m->plan.row_stats || m->plan.n_long > 0) return false;
-  if (m->layout == kLayoutPanels) return true;
-  if (m->layout == kLayoutStream) return false;
-  return m->plan.row_var > 10.0;
-}
-
-void free_panels(csrk_matrix *m) {
-  PanelPlan &pn = m->panel;
-  cudaFree(pn.row);
-  cudaFree(pn.col);
-  cudaFree(pn.pos);
-  cudaFree(pn.val64);
-  cudaFree(pn.val32);
-  pn = PanelPlan();
-}
-
-int ensure_panels(csrk_matrix *m, int value_type, cudaStream_t s) {
-  PanelPlan &pn = m->panel;
-  const bool need32 = value_type == CSRK_F32;
-  if (pn.built && (!need32 || pn.val32)) return CSRK_OK;
-  if (pn.built) free_panels(m);  // rebuilt with the f32 copy as well
-  const int64_t cap = panel_cap_default();
-  const int64_t w = kPanelRowWeight;
-  // rows <= kLongRow nonzeros here (n_long == 0): a panel's cost (nonzeros
-  // + w rows) stays below pitch + kLongRow + w, so its nonzeros fit `cap`
-  // and its rows cap / w
-  const int64_t pitch = cap - (kLongRow + w);
-  const int64_t total = m->nnz + w * m->n_rows;
-  const int64_t n_panels = std::max<int64_t>(1, (total + pitch - 1) / pitch);
-  CSRK_CUDA_TRY(cudaMalloc(&pn.row, 2 * (n_panels + 1) * sizeof(uint32_t)));
-  pn.ptr = pn.row + (n_panels + 1);
-  const unsigned b = static_cast<unsigned>((n_panels + 1 + 255) / 256);
-  panel_bounds_kernel<<<b, 256, 0, s>>>(m->row_ptr, m->n_rows, w, pitch, n_panels, pn.row);
-  tile_ptr_kernel<<<b, 256, 0, s>>>(m->row_ptr, pn.row, n_panels, pn.ptr);
-  CSRK_CUDA_TRY(cudaGetLastError());
-  const int64_t nnz = m->nnz;
-  int col_bits = 1;
-  while ((int64_t(1) << col_bits) < m->n_cols) ++col_bits;
-  int panel_bits = 1;
-  while ((int64_t(1) << panel_bits) < n_panels) ++panel_bits;
-  if (col_bits + panel_bits > 64) {
-    set_error("panel keys do not fit 64 bits");
-    return CSRK_EINVAL;
-  }
-  // (+kPanelChunk: a panel's last chunk is read whole by the consumers)
-  const int64_t padded = padded_nnz(nnz) + kPanelChunk;
-  CSRK_CUDA_TRY(cudaMalloc(&pn.col, padded * sizeof(uint32_t)));
-  CSRK_CUDA_TRY(cudaMalloc(&pn.pos, padded * sizeof(uint16_t)));
-  CSRK_CUDA_TRY(cudaMemsetAsync(pn.col, 0, padded * sizeof(uint32_t), s));
-  CSRK_CUDA_TRY(cudaMemsetAsync(pn.pos, 0, padded * sizeof(uint16_t), s));
-  if (m->vals64) {
-    CSRK_CUDA_TRY(cudaMalloc(&pn.val64, padded * sizeof(double)));
-    CSRK_CUDA_TRY(cudaMemsetAsync(pn.val64, 0, padded * sizeof(double), s));
-  }
-  if (m->vals32) {
-    CSRK_CUDA_TRY(cudaMalloc(&pn.val32, padded * sizeof(float)));
-    CSRK_CUDA_TRY(cudaMemsetAsync(pn.val32, 0, padded * sizeof(float), s));
-  }
-  if (nnz > 0) {
-    uint64_t *keys = nullptr;
-    uint32_t *vals = nullptr;
-    keep_async_pool();
-    CSRK_CUDA_TRY(cudaMallocAsync(&keys, 2 * nnz * sizeof(uint64_t), s));
-    CSRK_CUDA_TRY(cudaMallocAsync(&vals, 2 * nnz * sizeof(uint32_t), s));
-    const unsigned g = static_cast<unsigned>(std::min<int64_t>((nnz + 255) / 256, 148 * 32));
-    panel_keys_kernel<<<g, 256, 0, s>>>(m->col_idx, nnz, pn.ptr, n_panels, col_bits, keys, vals);
-    CSRK_CUDA_TRY(cudaGetLastError());
-    const int end_bit = ((col_bits + panel_bits + 7) / 8) * 8;
-    int rc = radix_sort_pairs(keys, vals, keys + nnz, vals + nnz, nnz, 0, end_bit, s);
-    if (rc == CSRK_OK) {
-      panel_fill_kernel<double><<<g, 256, 0, s>>>(keys, vals, nnz, col_bits, pn.ptr, m->vals64,
-                                                  m->vals32, pn.col, pn.pos, pn.val64, pn.val32);
-      rc = cudaGetLastError() == cudaSuccess ? CSRK_OK : CSRK_ECUDA;
-    }
-    cudaFreeAsync(keys, s);
-    cudaFreeAsync(vals, s);
-    CSRK_TRY(rc);
-  }
-  CSRK_CUDA_TRY(cudaStreamSynchronize(s));
-  pn.cap = cap;
-  pn.rcap = cap / w;
-  pn.n_panels = n_panels;
-  pn.built = true;
-  return CSRK_OK;
-}
-
-namespace {
-
-template <typename V, int NX, int NCW>
-int launch_panels_nx(const csrk_matrix *m, const V *pval, const V *x, V *y, cudaStream_t s) {
-  const PanelPlan &pn = m->panel;
-  const PanelGeo<V> geo(static_cast<uint32_t>(pn.cap), static_cast<uint32_t>(pn.rcap));
-  const size_t smem = geo.total;
-  auto kern = csrk_panel_kernel<V, NX, NCW>;
-  static thread_local size_t cached_smem = 0;
-  static thread_local int cached_per_sm = 0, cached_device = -1;
-  int dev = 0;
-  CSRK_CUDA_TRY(cudaGetDevice(&dev));
-  if (cached_smem != smem || cached_device != dev) {
-    CSRK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem)));
-    int smem_sm = 0;
-    CSRK_CUDA_TRY(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor,
-                                         dev));
-    const int ctas = panel_ctas_default();
-    int pct = static_cast<int>(ctas * (smem + 1024) * 100.0 / smem_sm + 0.999);
-    pct = pct < 1 ? 1 : (pct > 100 ? 100 : pct);
-    CSRK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
-    int per_sm = 0;
-    CSRK_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * (NCW + 1),
-                                                                smem));
-    cached_per_sm = std::min(per_sm, ctas);
-    cached_smem = smem;
-    cached_device = dev;
-  }
-  if (cached_per_sm < 1) {
-    set_error("panel kernel does not fit on an SM (%zu bytes of shared memory)", smem);
-    return CSRK_EINVAL;
-  }
-  const int64_t grid = std::min<int64_t>(int64_t(cached_per_sm) * m->sm_count, pn.n_panels);
-  kern<<<static_cast<unsigned>(grid), 32 * (NCW + 1), smem, s>>>(
-      m->row_ptr, pn.col, pval, pn.pos, x, y, pn.row, pn.ptr, static_cast<uint32_t>(pn.n_panels),
-      static_cast<uint32_t>(pn.cap), static_cast<uint32_t>(pn.rcap));
-  CSRK_CUDA_TRY(cudaGetLastError());
-  return CSRK_OK;
-}
-
-template <typename V, int NX>
-int launch_panels_w(const csrk_matrix *m, const V *pval, const V *x, V *y, cudaStream_t s) {
-  return panel_warps_default() == 8 ? launch_panels_nx<V, NX, 8>(m, pval, x, y, s)
-                                    : launch_panels_nx<V, NX, 16>(m, pval, x, y, s);
-}
-
-template <typename V>
-int launch_panels(const csrk_matrix *m, int variant, int nx, const V *pval, const V *x, V *y,
-                  cudaStream_t s) {
-  if (variant == CSRK_SERIAL) return launch_panels_w<V, 0>(m, pval, x, y, s);
-  switch (nx) {
-#define CSRK_PANEL_CASE(N) \
-  case N:                  \
-    return launch_panels_w<V, N>(m, pval, x, y, s);
-    CSRK_PANEL_CASE(1)
-    CSRK_PANEL_CASE(2)
-    CSRK_PANEL_CASE(3)
-    CSRK_PANEL_CASE(4)
-    CSRK_PANEL_CASE(5)
-    CSRK_PANEL_CASE(6)
-    CSRK_PANEL_CASE(7)
-    CSRK_PANEL_CASE(8)
-    CSRK_PANEL_CASE(9)
-    CSRK_PANEL_CASE(10)
-    CSRK_PANEL_CASE(11)
-    CSRK_PANEL_CASE(12)
-    CSRK_PANEL_CASE(13)
-    CSRK_PANEL_CASE(14)
-    CSRK_PANEL_CASE(15)
-    CSRK_PANEL_CASE(16)
-    CSRK_PANEL_CASE(20)
-    CSRK_PANEL_CASE(24)
-    CSRK_PANEL_CASE(28)
-    CSRK_PANEL_CASE(32)
-#undef CSRK_PANEL_CASE
-    default:
-      set_error("strided SpMV supports nx in 1..16, 20, 24, 28, 32; got %d "
-                "(use the listing-4 kernel for other block dimensions)",
-                nx);
-      return CSRK_EINVAL;
-  }
-}
-
-}  // namespace
-
 int launch_spmv(const csrk_matrix *m, int value_type, int variant, int nx,
                 const void *x, void *y, cudaStream_t stream, int64_t t0,
                 int64_t t1) {
@@ -1908,16 +1396,6 @@ int launch_spmv(const csrk_matrix *m, int value_type, int variant, int nx,
   if (!m->plan.tile_row) {
     set_error("matrix has no tile plan");
     return CSRK_EINVAL;
-  }
-  // whole-matrix launches on the column-sorted panels (built by prepare_plan)
-  const bool whole = t0 <= 0 && (t1 < 0 || t1 >= m->plan.n_tiles);
-  if (whole && m->panel.built && panels_wanted(m)) {
-    if (value_type == CSRK_F64 && m->panel.val64)
-      return launch_panels<double>(m, variant, nx, m->panel.val64, static_cast<const double *>(x),
-                                   static_cast<double *>(y), stream);
-    if (value_type == CSRK_F32 && m->panel.val32)
-      return launch_panels<float>(m, variant, nx, m->panel.val32, static_cast<const float *>(x),
-                                  static_cast<float *>(y), stream);
   }
   if (value_type == CSRK_F64) {
     if (!m->vals64) {

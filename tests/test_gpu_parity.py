@@ -546,57 +546,3 @@ def test_tile_range_and_cut_mode_argument_checks():
         dev.set_cut_mode(3)
     tr = dev.tile_rows()
     assert tr[0] == 0 and tr[-1] == 2000 and len(tr) == nt + 1 and np.all(np.diff(tr) >= 0)
-
-
-@pytest.mark.parametrize("layout", [0, 1, 2])
-@pytest.mark.parametrize("kind", ["irregular", "stencil", "empty_rows"])
-def test_panel_layout_bitwise(layout, kind):
-    """Whole-matrix launches on the column-sorted panels (gathers in column
-    order, products to shared memory at their CSR positions, rows summed in
-    the reference's order) give the oracle's bits in both orders, f64 and
-    (within the scaled bound) f32; tile-range launches keep streaming."""
-    torch = pytest.importorskip("torch")
-    rng = np.random.default_rng(40 + layout + len(kind))
-    if kind == "irregular":
-        r, c, v = synthetic.irregular_triplets(120000, seed=5)
-        a = ck.csr_from_arrays(120000, 120000, r, c, v)
-    elif kind == "stencil":
-        n, rp, ci, va = synthetic.stencil_arrays((30, 31, 32), 27, values="uniform")
-        a = ck.CsrMatrix(n, n, rp, ci, va)
-    else:
-        n = 50000
-        lens = rng.integers(1, 60, n)
-        lens[::4] = 0
-        rows = np.repeat(np.arange(n), lens)
-        a = ck.csr_from_arrays(n, n, rows, rng.integers(0, n, len(rows)),
-                               rng.uniform(-1, 1, len(rows)))
-    res = ck.band_k(a, 3, [7, 11])
-    m = ck.pack_csrk(a, res.perm, res.level_group_sizes)
-    b = m.base
-    x = rng.uniform(-1.0, 1.0, b.n_rows)
-    dev = m.device()
-    dev.set_layout(layout)
-    np.testing.assert_array_equal(ck.spmv_csr3(m, x), O.spmv_serial(b.row_ptr, b.col_idx,
-                                                                    b.vals, x))
-    plan = dev.plan()
-    irregular = ck.compute_stats(b).variance > 10.0  # the auto rule's class boundary
-    assert plan["panels"] == int(layout == 1 or (layout == 2 and irregular))
-    if plan["panels"]:
-        assert plan["n_panels"] >= 1
-    xd = torch.from_numpy(x).cuda()
-    for nx in (2, 4, 16):
-        want = O.spmv_strided(b.row_ptr, b.col_idx, b.vals, x, nx)
-        y = ck.spmv_device(m, xd, dims=ck.BlockDims(nx, 1, 1), variant="strided")
-        np.testing.assert_array_equal(y.cpu().numpy(), want)
-    want = O.spmv_serial(b.row_ptr, b.col_idx, b.vals, x)
-    y32 = ck.spmv_device(m, xd.float()).double().cpu().numpy()
-    scale = O.abs_row_dot(b.row_ptr, b.col_idx, b.vals, x)
-    assert np.all(np.abs(y32 - want) <= 1e-5 * scale + 1e-300)
-    # a tile range (streaming kernel) gives the same bits
-    yd = torch.full_like(xd, float("nan"))
-    nt = plan["n_tiles"]
-    s = torch.cuda.current_stream().cuda_stream
-    dev.spmv_tiles_ptr(xd.data_ptr(), yd.data_ptr(), 0, nt // 2, s)
-    dev.spmv_tiles_ptr(xd.data_ptr(), yd.data_ptr(), nt // 2, nt, s)
-    torch.cuda.synchronize()
-    np.testing.assert_array_equal(yd.cpu().numpy(), want)
