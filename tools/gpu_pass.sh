@@ -14,3 +14,5 @@ timeout 600 python bench.py > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TA
 cat gpurun_out/bench_$TAG.json
 CSRK_DIST=1 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node=1 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 1 > gpurun_out/bench_dist1_$TAG.json 2> gpurun_out/bench_dist1_$TAG.err; echo "dist1 rc=$?"
 cat gpurun_out/bench_dist1_$TAG.json
+timeout 1200 python bench.py --impl reference > gpurun_out/bench_ref_$TAG.json 2> gpurun_out/bench_ref_$TAG.err; echo "ref rc=$?"
+cat gpurun_out/bench_ref_$TAG.json
