@@ -47,6 +47,7 @@ extern "C" {
 #define CSRK_EINVAL 1 /* maps to ValueError */
 #define CSRK_ECUDA 2  /* maps to RuntimeError */
 #define CSRK_ENOMEM 3 /* maps to MemoryError */
+#define CSRK_ENCCL 4  /* maps to RuntimeError (multi-GPU entry points) */
 
 /* value storage types for csrk_matrix_upload(value_types) bitmask and for
  * the `value_type` argument of the SpMV entry points */
@@ -172,6 +173,15 @@ int csrk_spmv_listing3(const csrk_matrix *m, int dx, int dy, const double *x,
 int csrk_spmv_listing4(const csrk_matrix *m, int dx, int dy, int dz,
                        const double *x, double *y, int64_t *trace,
                        void *stream);
+
+/* Diagnostic (no reference counterpart; SURVEY.md 8(d) "a gather-only kernel
+ * variant to isolate x"): walks col_idx in the streaming kernel's chunk
+ * distribution; mode 0 reads col_idx only, mode 1 also gathers
+ * x[col_idx[p]] (f64).  The difference of the two launches' ncu sector
+ * counters is the x gathers' own L2 / L1 hit rate.  out: 1 double (written
+ * only to keep the loads alive). */
+int csrk_probe_gather(const csrk_matrix *m, int mode, const double *x, double *out,
+                      void *stream);
 
 /* ---- construction on device ------------------------------------------------
  * csrk_pack: replaces pack_csrk (format.py:347-393) + _permute_symmetric
@@ -347,6 +357,62 @@ int csrk_graph_sizes(const csrk_graph *g, int64_t out[3]);
 int csrk_graph_get(const csrk_graph *g, int64_t *adj_ptr, int64_t *adj_idx,
                    int64_t *edge_weight, int64_t *node_weight, int64_t *f2c);
 int csrk_graph_free(csrk_graph *g);
+
+/* ---- multi-GPU row blocks (SURVEY.md 8(b) csrk_mg_*, 8(e)) -----------------
+ * The reference has no multi-GPU path; these generalise its static chunks
+ * (kernels.py:150-155, _static_chunks: contiguous group ranges per worker)
+ * from equal group counts to equal nonzeros, across one process per GPU.
+ *
+ * Host planning (no GPU; mirrors paper_2203_05096_b200.dist):
+ *   csrk_mg_partition  -- cuts (parts + 1 global rows) on super-super-row
+ *                         boundaries balancing nonzeros: part g starts at the
+ *                         first SSR whose first nonzero offset reaches
+ *                         ceil(g * nnz / parts) (dist.partition_by_nnz);
+ *   csrk_mg_footprints -- per part the column window [lo, hi) its rows read
+ *                         (fps: parts x 2; lo = hi = first row if empty);
+ *   csrk_mg_plan       -- the transfers (src, dst, lo, hi), dst needing
+ *                         x[lo, hi) owned by src (dist.halo_plan); out holds
+ *                         cap x 4 entries, *count the full number.
+ * Exchange + SpMV (NCCL loaded at run time from libnccl.so.2):
+ *   csrk_mg_unique_id  -- rank 0 creates the communicator id (128 bytes) and
+ *                         passes it to the other ranks by its own means;
+ *   csrk_mg_create     -- rank `rank` of `world`: `block` is its rows
+ *                         [cuts[rank], cuts[rank+1]) as a k = 3 csrk_matrix
+ *                         (local rows / groups) whose columns are local to
+ *                         x_local = x[x0, x0 + block->n_cols) (borrowed; it
+ *                         must outlive the handle; NULL for a rank without
+ *                         rows); mode CSRK_MG_HALO or CSRK_MG_ALLGATHER;
+ *                         id NULL: no communicator -- the caller fills the
+ *                         halo of x_local itself before csrk_mg_spmv;
+ *   csrk_mg_spmv       -- y_own = A[r0:r1, :] x on `stream`: the exchange of
+ *                         x_local's halo on an internal stream (NCCL send /
+ *                         recv of exactly the windows each rank reads, or the
+ *                         north-star all-gather), the interior tiles meanwhile,
+ *                         the boundary tiles after it; x_local's owned slice
+ *                         must be written (stream-ordered) before the call;
+ *                         y_own is bitwise the single-GPU y;
+ *   csrk_mg_info       -- out[9] = interior rows a, b, interior tiles t_lo,
+ *                         t_hi, n_tiles, elements sent / received per step,
+ *                         number of sends / receives. */
+#define CSRK_MG_HALO 0
+#define CSRK_MG_ALLGATHER 1
+#define CSRK_MG_ID_BYTES 128
+typedef struct csrk_mg csrk_mg;
+int csrk_mg_partition(const uint32_t *row_ptr, const uint32_t *sr_ptr,
+                      const uint32_t *ssr_ptr, int64_t n_ssr, int parts,
+                      int64_t *cuts);
+int csrk_mg_footprints(const uint32_t *row_ptr, const uint32_t *col_idx,
+                       const int64_t *cuts, int parts, int64_t *fps);
+int csrk_mg_plan(int world, const int64_t *cuts, const int64_t *fps,
+                 int64_t *out, int64_t cap, int64_t *count);
+int csrk_mg_unique_id(unsigned char *id);
+int csrk_mg_create(int rank, int world, const unsigned char *id,
+                   const int64_t *cuts, const int64_t *fps, csrk_matrix *block,
+                   int64_t x0, int mode, csrk_mg **out);
+int csrk_mg_spmv(csrk_mg *h, int value_type, int variant, int nx, void *x_local,
+                 void *y_own, void *stream);
+int csrk_mg_info(const csrk_mg *h, int64_t *out);
+int csrk_mg_destroy(csrk_mg *h);
 
 #ifdef __cplusplus
 }

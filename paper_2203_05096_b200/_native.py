@@ -16,7 +16,8 @@ import numpy as np
 _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "lib", "libcsrk_cuda.so")
 
-CSRK_OK, CSRK_EINVAL, CSRK_ECUDA, CSRK_ENOMEM = 0, 1, 2, 3
+CSRK_OK, CSRK_EINVAL, CSRK_ECUDA, CSRK_ENOMEM, CSRK_ENCCL = 0, 1, 2, 3, 4
+CSRK_MG_HALO, CSRK_MG_ALLGATHER, CSRK_MG_ID_BYTES = 0, 1, 128
 CSRK_F64, CSRK_F32 = 1, 2
 CSRK_SERIAL, CSRK_STRIDED = 0, 1
 
@@ -57,6 +58,7 @@ _SIGNATURES = {
     "csrk_last_kernel_ms": ([P, C.POINTER(C.c_float)], C.c_int),
     "csrk_spmv_listing3": ([P, C.c_int, C.c_int, P, P, P, P], C.c_int),
     "csrk_spmv_listing4": ([P, C.c_int, C.c_int, C.c_int, P, P, P, P], C.c_int),
+    "csrk_probe_gather": ([P, C.c_int, P, P, P], C.c_int),
     "csrk_pack": ([C.c_int, I64, I64, U32P, U32P, F64P, I64P, I64P, C.c_int, I64,
                    I64P, I64, I64P, C.POINTER(P)], C.c_int),
     "csrk_gather_f64": ([I64, P, P, P, P], C.c_int),
@@ -96,6 +98,15 @@ _SIGNATURES = {
     "csrk_graph_sizes": ([P, I64P], C.c_int),
     "csrk_graph_get": ([P, I64P, I64P, I64P, I64P, I64P], C.c_int),
     "csrk_graph_free": ([P], C.c_int),
+    "csrk_mg_partition": ([U32P, U32P, U32P, I64, C.c_int, I64P], C.c_int),
+    "csrk_mg_footprints": ([U32P, U32P, I64P, C.c_int, I64P], C.c_int),
+    "csrk_mg_plan": ([C.c_int, I64P, I64P, I64P, I64, I64P], C.c_int),
+    "csrk_mg_unique_id": ([C.c_char_p], C.c_int),
+    "csrk_mg_create": ([C.c_int, C.c_int, C.c_char_p, I64P, I64P, P, I64, C.c_int,
+                        C.POINTER(P)], C.c_int),
+    "csrk_mg_spmv": ([P, C.c_int, C.c_int, C.c_int, P, P, P], C.c_int),
+    "csrk_mg_info": ([P, I64P], C.c_int),
+    "csrk_mg_destroy": ([P], C.c_int),
 }
 
 EXPORTED = tuple(_SIGNATURES)

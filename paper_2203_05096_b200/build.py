@@ -23,7 +23,7 @@ BUILD = os.path.join(PKG, "_build")
 LIB_DIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIB_DIR, "libcsrk_cuda.so")
 
-CUDA_SOURCES = ["abi.cu", "spmv.cu", "listing.cu", "construct.cu", "cg.cu", "sort.cu", "graph.cu", "rcm.cu", "coarsen.cu", "bandk_dev.cu"]
+CUDA_SOURCES = ["abi.cu", "spmv.cu", "listing.cu", "construct.cu", "cg.cu", "sort.cu", "graph.cu", "rcm.cu", "coarsen.cu", "bandk_dev.cu", "mg.cu"]
 CXX_SOURCES = ["bandk.cpp", "mmio.cpp"]
 HEADERS = [os.path.join(CSRC, "internal.h"), os.path.join(REPO, "include", "csrk.h")]
 
@@ -80,7 +80,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         list(pool.map(lambda c: _run(c, verbose), jobs))
     if force or jobs or _stale(LIB, objs):
         _run([nvcc, *ARCH, "-shared", "-o", LIB, *objs, "-Xcompiler", "-fopenmp",
-              "-lgomp"], verbose)
+              "-lgomp", "-ldl"], verbose)
     return LIB
 
 

@@ -779,4 +779,19 @@ int csrk_spmv_listing4(const csrk_matrix *m, int dx, int dy, int dz,
                          static_cast<cudaStream_t>(stream));
 }
 
+int csrk_probe_gather(const csrk_matrix *m, int mode, const double *x, double *out,
+                      void *stream) {
+  if (!m || !out || (mode != 0 && !x)) {
+    set_error("null argument");
+    return CSRK_EINVAL;
+  }
+  if (mode != 0 && mode != 1) {
+    set_error("probe mode must be 0 (col_idx only) or 1 (col_idx + x gathers)");
+    return CSRK_EINVAL;
+  }
+  CSRK_LOCK(m);
+  CSRK_CUDA_TRY(cudaSetDevice(m->device));
+  return launch_gather_probe(m, mode, x, out, static_cast<cudaStream_t>(stream));
+}
+
 }  // extern "C"

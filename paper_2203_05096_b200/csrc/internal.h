@@ -222,6 +222,8 @@ int launch_listing3(const csrk_matrix *m, int dx, int dy, const double *x,
 int launch_listing4(const csrk_matrix *m, int dx, int dy, int dz,
                     const double *x, double *y, int64_t *trace,
                     cudaStream_t stream);
+int launch_gather_probe(const csrk_matrix *m, int mode, const double *x, double *out,
+                        cudaStream_t stream);
 int launch_f64_to_f32(const double *in, float *out, int64_t n, cudaStream_t s);
 int exclusive_scan_i64(const int64_t *in, int64_t n, int64_t *out, cudaStream_t s);
 int radix_sort_pairs(uint64_t *keys, uint32_t *vals, uint64_t *tmp_keys,

@@ -121,6 +121,37 @@ __global__ void f64_to_f32_kernel(const double *__restrict__ in,
 }
 
 
+// ---- x-isolation probe (diagnostic, not on the SpMV path) -----------------
+//
+// SURVEY.md 8(d) asks for the L2 hit rate of the x gathers alone.  ncu's
+// lts / l1tex hit rates of the SpMV kernel mix the streamed matrix (always a
+// miss) with the x gathers.  These two kernels walk col_idx in the streaming
+// kernel's distribution (2048-entry chunks, persistent CTAs, chunk
+// blockIdx.x + k * gridDim.x): MODE 0 reads col_idx only, MODE 1 reads
+// col_idx and gathers x[col_idx[p]].  The difference of their sector
+// counters (hits, lookups) is the x gathers' own.
+template <int MODE>
+__global__ void __launch_bounds__(256)
+    gather_probe_kernel(const uint32_t *__restrict__ col_idx,
+                        const double *__restrict__ x, int64_t nnz,
+                        double *__restrict__ out) {
+  constexpr int64_t kChunk = 2048;
+  const int64_t chunks = (nnz + kChunk - 1) / kChunk;
+  double acc = 0.0;
+  for (int64_t c = blockIdx.x; c < chunks; c += gridDim.x) {
+    const int64_t p1 = (c + 1) * kChunk < nnz ? (c + 1) * kChunk : nnz;
+#pragma unroll 4
+    for (int64_t p = c * kChunk + threadIdx.x; p < p1; p += 256) {
+      const uint32_t col = __ldcs(col_idx + p);
+      if constexpr (MODE == 0)
+        acc += static_cast<double>(col);
+      else
+        acc += __ldg(x + col);
+    }
+  }
+  if (acc == -1.0e300) out[0] = acc;  // keeps the loads; never true
+}
+
 }  // namespace
 
 int launch_listing3(const csrk_matrix *m, int dx, int dy, const double *x,
@@ -153,6 +184,18 @@ int launch_listing4(const csrk_matrix *m, int dx, int dy, int dz,
   listing4_kernel<<<static_cast<unsigned>(m->n_ssr), block, smem, stream>>>(
       m->row_ptr, m->col_idx, m->vals64, m->sr_ptr, m->ssr_ptr, x, y, trace,
       m->n_rows, pw, depth);
+  CSRK_CUDA_TRY(cudaGetLastError());
+  return CSRK_OK;
+}
+
+int launch_gather_probe(const csrk_matrix *m, int mode, const double *x, double *out,
+                        cudaStream_t stream) {
+  if (m->nnz == 0) return CSRK_OK;
+  const unsigned grid = 148 * 6;
+  if (mode == 0)
+    gather_probe_kernel<0><<<grid, 256, 0, stream>>>(m->col_idx, x, m->nnz, out);
+  else
+    gather_probe_kernel<1><<<grid, 256, 0, stream>>>(m->col_idx, x, m->nnz, out);
   CSRK_CUDA_TRY(cudaGetLastError());
   return CSRK_OK;
 }

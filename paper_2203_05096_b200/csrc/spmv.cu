@@ -81,6 +81,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
       : "memory");
 }
 
+__device__ __forceinline__ uint64_t evict_last_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
+// bulk prefetch of [src, src + bytes) into L2 (src, bytes 16-byte aligned)
+__device__ __forceinline__ void l2_prefetch_bulk(const void *src, uint32_t bytes,
+                                                 uint64_t policy) {
+  asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(src),
+               "r"(bytes), "l"(policy)
+               : "memory");
+}
+
 __device__ __forceinline__ uint64_t evict_first_policy() {
   uint64_t pol;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;"
@@ -411,7 +425,8 @@ __global__ void __launch_bounds__(kThreads, 2)
                        const uint32_t *__restrict__ tile_ptr, uint32_t n_tiles,
                        uint32_t cap, uint32_t rcap, uint32_t stages, uint32_t long_len,
                        const uint32_t *__restrict__ tile_long,
-                       const uint2 *__restrict__ holes) {
+                       const uint2 *__restrict__ holes, uint64_t x_bytes,
+                       uint32_t pf_chunk) {
   extern __shared__ __align__(128) unsigned char smem[];
   const Geometry geo(cap, rcap, stages, sizeof(V));
   uint64_t *full = reinterpret_cast<uint64_t *>(smem);
@@ -435,6 +450,19 @@ __global__ void __launch_bounds__(kThreads, 2)
     if (tid != 0) return;
     constexpr uint32_t VPV = Elem<V>::kPerVec;
     const uint64_t policy = evict_first_policy();
+    // x prefetch (small x only, see launch_stream): CTA b pulls slice b of x
+    // into L2 with evict_last, so the tiles' gathers hit L2 instead of
+    // waiting out HBM latency on first touch, and the evict_first matrix
+    // stream does not displace it
+    if (pf_chunk) {
+      const uint64_t off = static_cast<uint64_t>(blockIdx.x) * pf_chunk;
+      if (off < x_bytes) {
+        const uint64_t left = x_bytes - off;
+        const uint32_t b = static_cast<uint32_t>(left < pf_chunk ? left : pf_chunk) & ~15u;
+        if (b) l2_prefetch_bulk(reinterpret_cast<const unsigned char *>(x) + off, b,
+                                evict_last_policy());
+      }
+    }
     // the next tile's bounds (rows and their nonzero offsets, precomputed in
     // the plan) load while this tile waits for its stage: the producer never
     // spends a dependent global round trip between two TMA issues
@@ -865,6 +893,16 @@ bool long_beside(const csrk_matrix *m, int variant, int nx) {
 constexpr int kBesideBlocks = 2;
 constexpr size_t kLongBlockSmem = 8 * 128 * sizeof(double) + 1024;
 
+// x vectors up to this size are prefetched into L2 by the streaming kernel
+// (CSRK_X_PREFETCH=<MB> overrides; 0 disables)
+uint64_t x_prefetch_limit() {
+  static const uint64_t lim = [] {
+    const char *e = std::getenv("CSRK_X_PREFETCH");
+    return e ? static_cast<uint64_t>(std::atoll(e)) << 20 : (48ull << 20);
+  }();
+  return lim;
+}
+
 template <typename V, int NX, bool GF, int LB = 4>
 int launch_stream(const csrk_matrix *m, const V *vals, const V *x, V *y,
                   cudaStream_t stream, int64_t t0, int64_t t1) {
@@ -925,12 +963,23 @@ int launch_stream(const csrk_matrix *m, const V *vals, const V *x, V *y,
   int64_t grid = static_cast<int64_t>(per_sm) * m->sm_count;
   if (grid > count) grid = count;
   if (grid < 1) return CSRK_OK;
+  // x prefetch into L2 for whole-matrix launches whose x is small against
+  // the 126 MB L2 (x_prefetch_bytes(), CSRK_X_PREFETCH), from a 16-byte
+  // aligned x; slices of at least 4 KB
+  const uint64_t x_bytes = static_cast<uint64_t>(m->n_cols) * sizeof(V);
+  uint32_t pf_chunk = 0;
+  if (t0 == 0 && t1 == pl.n_tiles && (reinterpret_cast<uintptr_t>(x) & 15u) == 0 &&
+      x_bytes <= x_prefetch_limit()) {
+    uint64_t c = (x_bytes + grid - 1) / grid;
+    c = (c + 4095) / 4096 * 4096;
+    pf_chunk = static_cast<uint32_t>(c);
+  }
   kern<<<static_cast<unsigned>(grid), kThreads, smem, stream>>>(
       m->row_ptr, m->col_idx, vals, x, y, pl.tile_row + t0, pl.tile_ptr + t0,
       static_cast<uint32_t>(count), geo.cap, geo.rcap, geo.stages,
       m->plan.n_long > 0 ? static_cast<uint32_t>(kLongRow) : 0xffffffffu,
       m->plan.n_long > 0 ? pl.tile_long + t0 : nullptr,
-      long_holes(pl));
+      long_holes(pl), x_bytes, pf_chunk);
   CSRK_CUDA_TRY(cudaGetLastError());
   return CSRK_OK;
 }

@@ -711,6 +711,153 @@ class DistSpMV:
                 + (self.n_local_cols + self.n_own) * itemsize)
 
 
+def native_partition(m, parts: int) -> np.ndarray:
+    """partition_by_nnz through the C-ABI (csrk_mg_partition)."""
+    from . import _native as nat
+
+    rp = np.ascontiguousarray(m.base.row_ptr, dtype=np.uint32)
+    sp = np.ascontiguousarray(m.sr_ptr, dtype=np.uint32)
+    ssp = np.ascontiguousarray(m.ssr_ptr, dtype=np.uint32)
+    cuts = np.zeros(parts + 1, dtype=np.int64)
+    nat.call("csrk_mg_partition", nat.u32p(rp), nat.u32p(sp), nat.u32p(ssp), len(ssp) - 1,
+             parts, nat.i64p(cuts))
+    return cuts
+
+
+def native_footprints(row_ptr, col_idx, cuts) -> np.ndarray:
+    """footprints through the C-ABI (csrk_mg_footprints)."""
+    from . import _native as nat
+
+    rp = np.ascontiguousarray(row_ptr, dtype=np.uint32)
+    ci = np.ascontiguousarray(col_idx, dtype=np.uint32)
+    cu = np.ascontiguousarray(cuts, dtype=np.int64)
+    fps = np.zeros((len(cu) - 1, 2), dtype=np.int64)
+    nat.call("csrk_mg_footprints", nat.u32p(rp), nat.u32p(ci), nat.i64p(cu), len(cu) - 1,
+             nat.i64p(fps))
+    return fps
+
+
+def native_halo_plan(cuts, fps) -> list:
+    """halo_plan through the C-ABI (csrk_mg_plan)."""
+    import ctypes as C
+
+    from . import _native as nat
+
+    cu = np.ascontiguousarray(cuts, dtype=np.int64)
+    fp = np.ascontiguousarray(fps, dtype=np.int64)
+    count = C.c_int64()
+    nat.call("csrk_mg_plan", len(cu) - 1, nat.i64p(cu), nat.i64p(fp), None, 0, C.byref(count))
+    out = np.zeros((max(count.value, 1), 4), dtype=np.int64)
+    nat.call("csrk_mg_plan", len(cu) - 1, nat.i64p(cu), nat.i64p(fp), nat.i64p(out),
+             count.value, C.byref(count))
+    return [tuple(int(v) for v in row) for row in out[:count.value]]
+
+
+class NativeDistSpMV:
+    """DistSpMV behind the C-ABI (csrk_mg_create / csrk_mg_spmv, SURVEY.md
+    §8(b)): the same nnz-balanced SSR blocks, footprint-local x and halo /
+    all-gather exchange, with NCCL driven from the library (its own
+    communicator, created from a unique id rank 0 broadcasts over the
+    torch.distributed group) and the interior / boundary tile split done in
+    C++.  y_own is bitwise the single-GPU y."""
+
+    def __init__(self, m, rank: int, world: int, mode: str = "halo", group=None,
+                 device=None, f32: bool = False, variant: str = "serial", nx: int = 1,
+                 communicator: bool = True):
+        """communicator=False: no NCCL communicator; the caller fills the
+        halo of x_local itself before step() (tests on one GPU)."""
+        import ctypes as C
+
+        import torch
+
+        from . import _native as nat
+
+        if mode not in ("halo", "allgather"):
+            raise ValueError(f"unknown exchange mode {mode!r}")
+        b = m.base
+        self.cuts = native_partition(m, world)
+        self.fps = native_footprints(b.row_ptr, b.col_idx, self.cuts)
+        self.rank, self.world, self.f32 = rank, world, f32
+        self.r0, self.r1 = int(self.cuts[rank]), int(self.cuts[rank + 1])
+        lo, hi = (int(v) for v in self.fps[rank])
+        self.x0 = min(lo, self.r0) if hi > lo else self.r0
+        self.x1 = max(hi, self.r1) if hi > lo else self.r1
+        self.n_own = self.r1 - self.r0
+        self.n_local_cols = self.x1 - self.x0
+        self.var = nat.CSRK_STRIDED if variant == "strided" else nat.CSRK_SERIAL
+        self.nx = int(nx) if variant == "strided" else 1
+        self.dev = None
+        if self.n_own > 0:
+            blk = local_block(m, self.r0, self.r1, col0=self.x0)
+            self.dev = nat.DeviceMatrix.upload(
+                blk.row_ptr, blk.col_idx, blk.vals, self.n_own, self.n_local_cols, k=3,
+                sr_ptr=blk.sr_ptr, ssr_ptr=blk.ssr_ptr, device=device, f32=f32)
+            self.dev.prepare(self.var, self.nx, f32)
+        uid = C.create_string_buffer(nat.CSRK_MG_ID_BYTES)
+        if communicator and rank == 0:
+            nat.call("csrk_mg_unique_id", uid)
+        if communicator and world > 1:
+            import torch.distributed as dist
+
+            on = "cuda" if dist.get_backend(group) == "nccl" else "cpu"
+            t = torch.frombuffer(bytearray(uid.raw), dtype=torch.uint8).to(on)
+            dist.broadcast(t, src=0, group=group)
+            uid = C.create_string_buffer(bytes(t.cpu().numpy().tobytes()),
+                                         nat.CSRK_MG_ID_BYTES)
+        self._cuts_c = np.ascontiguousarray(self.cuts, dtype=np.int64)
+        self._fps_c = np.ascontiguousarray(self.fps, dtype=np.int64)
+        out = C.c_void_p()
+        nat.call("csrk_mg_create", rank, world, uid if communicator else None,
+                 nat.i64p(self._cuts_c),
+                 nat.i64p(self._fps_c), self.dev.ptr if self.dev is not None else None,
+                 self.x0, nat.CSRK_MG_ALLGATHER if mode == "allgather" else nat.CSRK_MG_HALO,
+                 C.byref(out))
+        self.ptr = out
+
+    @property
+    def own(self) -> slice:
+        return slice(self.r0 - self.x0, self.r1 - self.x0)
+
+    def new_x_local(self, dtype=None, device=None):
+        import torch
+
+        dtype = dtype or (torch.float32 if self.f32 else torch.float64)
+        return torch.zeros(max(1, self.n_local_cols), dtype=dtype, device=device or "cuda")
+
+    def info(self) -> dict:
+        from . import _native as nat
+
+        out = np.zeros(9, dtype=np.int64)
+        nat.call("csrk_mg_info", self.ptr, nat.i64p(out))
+        keys = ("interior_a", "interior_b", "t_lo", "t_hi", "n_tiles", "sent", "received",
+                "n_sends", "n_recvs")
+        return dict(zip(keys, (int(v) for v in out)))
+
+    def step(self, x_local, y_own):
+        import torch
+
+        from . import _native as nat
+
+        s = torch.cuda.current_stream(x_local.device).cuda_stream
+        nat.call("csrk_mg_spmv", self.ptr, nat.CSRK_F32 if self.f32 else nat.CSRK_F64,
+                 self.var, self.nx, x_local.data_ptr(),
+                 y_own.data_ptr() if y_own is not None and y_own.numel() else None, s)
+        return y_own
+
+    def close(self):
+        from . import _native as nat
+
+        if getattr(self, "ptr", None) is not None and self.ptr.value:
+            nat.call("csrk_mg_destroy", self.ptr)
+            self.ptr = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def _collective_warmup(group=None) -> None:
     """One collective over the group before any point-to-point batch: with
     NCCL the first batch_isend_irecv must otherwise involve every rank, and

@@ -538,3 +538,66 @@ def test_bench_gpus_flag_relaunches_under_torchrun():
     assert len(lines) == 1
     line = json.loads(lines[0])
     assert line["world_size"] == 3 and line["n_gpus"] == 3 and line["torchrun"]
+
+
+# ---- the multi-GPU C-ABI (csrk_mg_*) -----------------------
+
+@pytest.mark.parametrize("parts", [1, 2, 3, 5, 8])
+def test_native_mg_planning_matches_dist(parts):
+    """csrk_mg_partition / csrk_mg_footprints / csrk_mg_plan (host C++, no
+    GPU) equal dist.partition_by_nnz / footprints / halo_plan."""
+    for shape, points, targets in (((20, 20, 20), 7, (8, 8)), ((12, 12, 12), 27, (4, 8))):
+        m = _packed(shape, points, targets)
+        b = m.base
+        cuts = D.partition_by_nnz(b.row_ptr, m.sr_ptr, m.ssr_ptr, parts)
+        np.testing.assert_array_equal(D.native_partition(m, parts), cuts)
+        fps = D.footprints(b.row_ptr, b.col_idx, cuts)
+        np.testing.assert_array_equal(D.native_footprints(b.row_ptr, b.col_idx, cuts), fps)
+        assert D.native_halo_plan(cuts, fps) == D.halo_plan(cuts, fps)
+
+
+def test_native_mg_partition_rejects_bad_parts():
+    m = _packed((8, 8, 8), 7, (4, 4))
+    with pytest.raises(ValueError, match="parts"):
+        D.native_partition(m, 0)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("variant,nx", [("serial", 1), ("strided", 4)])
+def test_native_mg_blocks_bitwise(variant, nx):
+    """csrk_mg_* on one GPU: world 1 with its own NCCL communicator (no
+    transfers) equals the single-GPU y; world 2 / 3 / 8 rank by rank without
+    a communicator (halo pre-filled, as the exchange delivers it) -- same
+    interior tile split as DistSpMV, slices reassemble the y bit for bit."""
+    n, rp, ci, va = synthetic.stencil_arrays((40, 40, 40), 7, values="uniform")
+    a = ck.CsrMatrix(n, n, rp, ci, va)
+    res = ck.band_k(a, 3, [8, 8])
+    m = ck.pack_csrk(a, res.perm, res.level_group_sizes)
+    b = m.base
+    x = np.random.default_rng(7).uniform(-1, 1, n)
+    want = (O.spmv_serial(b.row_ptr, b.col_idx, b.vals, x) if variant == "serial"
+            else O.spmv_strided(b.row_ptr, b.col_idx, b.vals, x, nx))
+    op = D.NativeDistSpMV(m, 0, 1, variant=variant, nx=nx)
+    xl = torch.from_numpy(x).cuda()
+    y = torch.empty(n, dtype=torch.float64, device="cuda")
+    op.step(xl, y)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(y.cpu().numpy(), want)
+    assert op.info()["sent"] == 0 and op.info()["t_hi"] == op.info()["n_tiles"]
+    op.close()
+    for parts in (2, 3, 8):
+        got = []
+        for g in range(parts):
+            nd = D.NativeDistSpMV(m, g, parts, variant=variant, nx=nx, communicator=False)
+            py = D.DistSpMV(m, g, parts, variant=variant, nx=nx)
+            xl = torch.from_numpy(x[nd.x0:nd.x1]).cuda()
+            yo = torch.full((nd.n_own,), float("nan"), dtype=torch.float64, device="cuda")
+            nd.step(xl, yo)
+            torch.cuda.synchronize()
+            info = nd.info()
+            assert (info["t_lo"], info["t_hi"], info["n_tiles"]) == (py.t_lo, py.t_hi,
+                                                                     py.n_tiles)
+            assert info["received"] == sum(hi - lo for _, lo, hi in py.exchange.recvs)
+            got.append(yo.cpu().numpy())
+            nd.close()
+        np.testing.assert_array_equal(np.concatenate(got), want)
