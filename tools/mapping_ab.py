@@ -123,6 +123,19 @@ def main():
                         dev.set_plan(tc, 0, 0)
                     except ValueError:
                         continue
+                    # a group larger than the stage runs its tile from global
+                    # memory ("direct" mode, reachable only with cut mode 2):
+                    # one timed trial, skipped when it is 3x the row-cut time
+                    e0 = torch.cuda.Event(enable_timing=True)
+                    e1 = torch.cuda.Event(enable_timing=True)
+                    e0.record()
+                    run()
+                    e1.record()
+                    e1.synchronize()
+                    if e0.elapsed_time(e1) > 3 * ms + 0.05:
+                        rec.setdefault("groups_skipped_tiles", []).append(
+                            [tc, round(e0.elapsed_time(e1), 3)])
+                        continue
                     ms_g = median_ms(run, flush)
                     same = bool(torch.equal(yd, want))
                     pl = dev.plan()
