@@ -180,6 +180,28 @@ struct StageMeta {
 
 // ---- per-row arithmetic ---------------------------------------------------
 
+// fp32 values (a device-only extension; the reference is f64): a batch of
+// up to B products is summed left to right in fp32 with fused multiply-adds
+// and the batch sum is added to the row's fp64 accumulator, so the error is
+// at most B unit roundoffs of the batch's |A||x| (B <= 8: 4.8e-7 of the row's
+// |A||x|, inside north_star's 1e-5 for any row length) at one conversion and
+// one fp64 add per batch instead of two conversions, a DMUL and a DADD per
+// nonzero (the f32 kernels were issue-bound on F2F.F64.F32: C2 f32 ncu r02).
+template <int B>
+__device__ __forceinline__ float chunk_f32(const float (&v)[B], const float (&xv)[B],
+                                           uint32_t count) {
+  float part = 0.0f;
+#pragma unroll
+  for (int j = 0; j < B; ++j)
+    if (static_cast<uint32_t>(j) < count) part = __fmaf_rn(v[j], xv[j], part);
+  return part;
+}
+template <int B>
+__device__ __forceinline__ float chunk_f32(const double (&)[B], const double (&)[B],
+                                           uint32_t) {
+  return 0.0f;  // (f64 instantiations never call it)
+}
+
 // Serial left-to-right row sum.  Every batch issues all of its x gathers
 // before the ordered adds: lanes past the row end load x[0] (their result is
 // discarded), so the loads are unconditional and independent -- predicating
@@ -198,18 +220,22 @@ __device__ __forceinline__ double row_serial(const V *__restrict__ sv,
   const uint32_t last = e - 1;
   for (uint32_t p = s; p < e; p += B) {
     uint32_t c[B];
-    double v[B], xv[B];
+    V v[B], xv[B];
 #pragma unroll
     for (int j = 0; j < B; ++j) {
       const uint32_t q = min(p + j, last);
       c[j] = p + j <= last ? sc[q] : 0u;
-      v[j] = static_cast<double>(sv[q]);
+      v[j] = sv[q];
     }
 #pragma unroll
-    for (int j = 0; j < B; ++j) xv[j] = Elem<V>::load_x(x, c[j]);
+    for (int j = 0; j < B; ++j) xv[j] = __ldg(x + c[j]);
+    if constexpr (sizeof(V) == 8) {
 #pragma unroll
-    for (int j = 0; j < B; ++j)
-      if (p + j < e) acc = __dadd_rn(acc, __dmul_rn(v[j], xv[j]));
+      for (int j = 0; j < B; ++j)
+        if (p + j < e) acc = __dadd_rn(acc, __dmul_rn(v[j], xv[j]));
+    } else {
+      acc = __dadd_rn(acc, static_cast<double>(chunk_f32<B>(v, xv, e - p)));
+    }
   }
   return acc;
 }
@@ -228,18 +254,22 @@ __device__ __forceinline__ double lane_partial(const V *__restrict__ sv,
   const uint32_t last = first + (count - 1) * NX;
   for (uint32_t p = first; p < e; p += B * NX) {
     uint32_t c[B];
-    double v[B], xv[B];
+    V v[B], xv[B];
 #pragma unroll
     for (int j = 0; j < B; ++j) {
       const uint32_t q = min(p + j * NX, last);
       c[j] = p + j * NX <= last ? sc[q] : 0u;
-      v[j] = static_cast<double>(sv[q]);
+      v[j] = sv[q];
     }
 #pragma unroll
-    for (int j = 0; j < B; ++j) xv[j] = Elem<V>::load_x(x, c[j]);
+    for (int j = 0; j < B; ++j) xv[j] = __ldg(x + c[j]);
+    if constexpr (sizeof(V) == 8) {
 #pragma unroll
-    for (int j = 0; j < B; ++j)
-      if (p + j * NX < e) acc = __dadd_rn(acc, __dmul_rn(v[j], xv[j]));
+      for (int j = 0; j < B; ++j)
+        if (p + j * NX < e) acc = __dadd_rn(acc, __dmul_rn(v[j], xv[j]));
+    } else {
+      acc = __dadd_rn(acc, static_cast<double>(chunk_f32<B>(v, xv, (e - p + NX - 1) / NX)));
+    }
   }
   return acc;
 }
@@ -1366,8 +1396,14 @@ int ensure_plan(csrk_matrix *m, int64_t tile_cost, int64_t cap, int64_t stages,
   // (cap - tile_cost) covers the row that crosses a boundary.
   // (a group larger than the tile: one group per tile, direct mode when it
   // exceeds the stage -- reachable only with cut mode 2)
-  const int64_t pitch =
-      cut_k == 1 ? tile_cost : std::max<int64_t>(tile_cost - max_group, 1);
+  // (a group of more than 3/4 of a tile cannot share a stage with its
+  // neighbours: such tiles run direct, and the pitch stays at least one
+  // tile so the tile count does not explode -- a pitch of 1 made C3's
+  // 200-row SSRs 196 M mostly empty tiles)
+  int64_t pitch = tile_cost;
+  if (cut_k != 1)
+    pitch = tile_cost - max_group >= tile_cost / 4 ? tile_cost - max_group
+                                                   : std::max(tile_cost, max_group);
   const int64_t total_cost = m->nnz + m->n_rows;
   int64_t n_tiles = (total_cost + pitch - 1) / pitch;
   if (n_tiles > 0x7fffffffLL) {

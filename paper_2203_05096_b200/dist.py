@@ -787,8 +787,10 @@ class NativeDistSpMV:
         self.var = nat.CSRK_STRIDED if variant == "strided" else nat.CSRK_SERIAL
         self.nx = int(nx) if variant == "strided" else 1
         self.dev = None
+        self.nnz_local = 0
         if self.n_own > 0:
             blk = local_block(m, self.r0, self.r1, col0=self.x0)
+            self.nnz_local = int(blk.row_ptr[-1])
             self.dev = nat.DeviceMatrix.upload(
                 blk.row_ptr, blk.col_idx, blk.vals, self.n_own, self.n_local_cols, k=3,
                 sr_ptr=blk.sr_ptr, ssr_ptr=blk.ssr_ptr, device=device, f32=f32)
@@ -832,6 +834,36 @@ class NativeDistSpMV:
         keys = ("interior_a", "interior_b", "t_lo", "t_hi", "n_tiles", "sent", "received",
                 "n_sends", "n_recvs")
         return dict(zip(keys, (int(v) for v in out)))
+
+    @property
+    def exchange(self):
+        """bytes_received / bytes_sent per step, like XExchange."""
+        info = self.info()
+
+        class _Bytes:
+            @staticmethod
+            def bytes_received(itemsize: int = 8) -> int:
+                return info["received"] * itemsize
+
+            @staticmethod
+            def bytes_sent(itemsize: int = 8) -> int:
+                return info["sent"] * itemsize
+        return _Bytes
+
+    @property
+    def launches_per_step(self) -> int:
+        if self.dev is None:
+            return 0
+        i = self.info()
+        if i["n_tiles"] < 0:  # plan not read yet (before the first step)
+            i["t_lo"], i["t_hi"], i["n_tiles"] = 0, 1, 1
+        n_long = 1 if self.dev.plan()["n_long"] > 0 else 0
+        parts = [i["t_hi"] > i["t_lo"], i["t_lo"] > 0, i["t_hi"] < i["n_tiles"]]
+        return sum(parts) * (1 + n_long)
+
+    def local_bytes(self, itemsize: int) -> int:
+        return (self.nnz_local * (itemsize + 4) + 4 * (self.n_own + 1)
+                + (self.n_local_cols + self.n_own) * itemsize)
 
     def step(self, x_local, y_own):
         import torch
@@ -1154,7 +1186,9 @@ def bench_blocks(args, log, rank: int, world: int, local: int, sampler=None, pea
     dtype = torch.float32 if f32 else torch.float64
     vb = 4 if f32 else 8
     mode = getattr(args, "exchange", None) or os.environ.get("CSRK_EXCHANGE", "halo")
-    op = DistSpMV(m, rank, world, mode=mode, device=local, f32=f32, variant=variant, nx=nx)
+    native = getattr(args, "mg", "torch") == "native"
+    cls = NativeDistSpMV if native else DistSpMV
+    op = cls(m, rank, world, mode=mode, device=local, f32=f32, variant=variant, nx=nx)
     x_local = op.new_x_local(dtype)
     x_local[op.own] = torch.from_numpy(xp[op.r0:op.r1]).to("cuda", dtype)
     # columns outside the owned slice are the exchange's job: poison them
@@ -1278,7 +1312,9 @@ def bench_blocks(args, log, rank: int, world: int, local: int, sampler=None, pea
                              + (f", nx={nx})" if variant == "strided" else ")"),
                    "parallelism": f"row blocks of whole super-super-rows x{world}, "
                                   f"balanced by nonzeros; {mode} x exchange over NCCL "
-                                  "overlapped with the interior tiles",
+                                  "overlapped with the interior tiles"
+                                  + ("; C-ABI csrk_mg_* (NCCL driven from the library)"
+                                     if native else "; torch.distributed NCCL"),
                    "exchange_bytes_per_rank_max": ex_max,
                    "l2": "inputs larger than L2; no flush" if algo >= 4 * 126e6 / world
                          else "per-rank inputs may fit L2 at this N"},
@@ -1297,7 +1333,8 @@ def bench_blocks(args, log, rank: int, world: int, local: int, sampler=None, pea
         "e2e": {"value": round(2.0 * nnz / e2e_s / 1e9, 2), "unit": "GFLOP/s",
                 "h2d_bytes_per_step": n * vb, "d2h_bytes_per_step": n * vb,
                 "ms_per_step": round(e2e_s * 1e3, 3),
-                "call": "dist.DistSpMV.step per rank with its pinned host x / y slices"},
+                "call": f"dist.{cls.__name__}.step per rank with its pinned host x / y "
+                        "slices" + (" (C-ABI csrk_mg_spmv)" if native else "")},
         "cpu_baseline": None,
         "gpu_launches": args.steps * launches,
         "clocks": clk_ctx.summary() if clk_ctx is not None else None,

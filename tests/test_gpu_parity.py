@@ -516,6 +516,9 @@ def test_cut_modes_bitwise(cut_mode, kind):
         if cut_mode == 2 and plan["n_long"] == 0:
             assert plan["group_aligned"] == 1
             assert set(dev.tile_rows().tolist()) <= ssr_rows
+            # groups larger than the tile: the pitch stays >= a tile (it
+            # used to drop to 1 and multiply the tile count by the tile cost)
+            assert plan["n_tiles"] <= 4 * (b.nnz + b.n_rows) // plan["tile_cost"] + 8
         yd = torch.full_like(xd, float("nan"))
         nt = plan["n_tiles"]
         cut = nt // 3
