@@ -14,7 +14,8 @@ import threading
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "lib", "libcsrk_cuda.so")
+# CSRK_LIB: an alternative build of the same library (A/B experiments, tools/build_variant.sh)
+LIB_PATH = os.environ.get("CSRK_LIB") or os.path.join(_PKG, "lib", "libcsrk_cuda.so")
 
 CSRK_OK, CSRK_EINVAL, CSRK_ECUDA, CSRK_ENOMEM, CSRK_ENCCL = 0, 1, 2, 3, 4
 CSRK_MG_HALO, CSRK_MG_ALLGATHER, CSRK_MG_ID_BYTES = 0, 1, 128

@@ -35,6 +35,10 @@
 namespace csrk {
 namespace {
 
+#ifndef CSRK_PRED_LDS
+#define CSRK_PRED_LDS 1
+#endif
+constexpr bool kPredLds = CSRK_PRED_LDS != 0;
 constexpr int kConsumerWarps = 8;
 constexpr int kConsumers = 32 * kConsumerWarps;
 constexpr int kThreads = kConsumers + 32;
@@ -223,9 +227,17 @@ __device__ __forceinline__ double row_serial(const V *__restrict__ sv,
     V v[B], xv[B];
 #pragma unroll
     for (int j = 0; j < B; ++j) {
-      const uint32_t q = min(p + j, last);
-      c[j] = p + j <= last ? sc[q] : 0u;
-      v[j] = sv[q];
+      if (kPredLds) {
+        // lanes past the row end issue no shared loads (their bank traffic
+        // was a third of C5's shared wavefronts: rows of 1..19 in batches of 8)
+        const bool in = p + j <= last;
+        c[j] = in ? sc[p + j] : 0u;
+        v[j] = in ? sv[p + j] : V(0);
+      } else {
+        const uint32_t q = min(p + j, last);
+        c[j] = p + j <= last ? sc[q] : 0u;
+        v[j] = sv[q];
+      }
     }
 #pragma unroll
     for (int j = 0; j < B; ++j) xv[j] = __ldg(x + c[j]);
@@ -257,9 +269,15 @@ __device__ __forceinline__ double lane_partial(const V *__restrict__ sv,
     V v[B], xv[B];
 #pragma unroll
     for (int j = 0; j < B; ++j) {
-      const uint32_t q = min(p + j * NX, last);
-      c[j] = p + j * NX <= last ? sc[q] : 0u;
-      v[j] = sv[q];
+      if (kPredLds) {
+        const bool in = p + j * NX <= last;
+        c[j] = in ? sc[p + j * NX] : 0u;
+        v[j] = in ? sv[p + j * NX] : V(0);
+      } else {
+        const uint32_t q = min(p + j * NX, last);
+        c[j] = p + j * NX <= last ? sc[q] : 0u;
+        v[j] = sv[q];
+      }
     }
 #pragma unroll
     for (int j = 0; j < B; ++j) xv[j] = __ldg(x + c[j]);
