@@ -118,13 +118,38 @@ __device__ __forceinline__ void tma_bulk_load(void *dst, const void *src,
       : "memory");
 }
 
+// x[c] through the read-only path with a 32-bit index: one IMAD.WIDE.U32
+// for the address (the plain x + c of a predicated-loaded index compiled to
+// a zeroed 64-bit pair, LEA and LEA.HI.X per gather)
+#ifndef CSRK_LDG_ASM
+#define CSRK_LDG_ASM 1
+#endif
+__device__ __forceinline__ double ldg_x(const double *x, uint32_t c) {
+  if (!CSRK_LDG_ASM) return __ldg(x + c);
+  double v;
+  asm("{\n\t.reg .u64 a;\n\tmul.wide.u32 a, %1, 8;\n\tadd.u64 a, a, %2;\n\t"
+      "ld.global.nc.f64 %0, [a];\n\t}"
+      : "=d"(v)
+      : "r"(c), "l"(x));
+  return v;
+}
+__device__ __forceinline__ float ldg_x(const float *x, uint32_t c) {
+  if (!CSRK_LDG_ASM) return __ldg(x + c);
+  float v;
+  asm("{\n\t.reg .u64 a;\n\tmul.wide.u32 a, %1, 4;\n\tadd.u64 a, a, %2;\n\t"
+      "ld.global.nc.f32 %0, [a];\n\t}"
+      : "=f"(v)
+      : "r"(c), "l"(x));
+  return v;
+}
+
 template <typename V>
 struct Elem;
 template <>
 struct Elem<double> {
   static constexpr uint32_t kPerVec = 2;  // elements per 16 bytes
   __device__ static double load_x(const double *x, uint32_t c) {
-    return __ldg(x + c);
+    return ldg_x(x, c);
   }
   __device__ static double out(double acc) { return acc; }
 };
@@ -132,7 +157,7 @@ template <>
 struct Elem<float> {
   static constexpr uint32_t kPerVec = 4;
   __device__ static double load_x(const float *x, uint32_t c) {
-    return static_cast<double>(__ldg(x + c));
+    return static_cast<double>(ldg_x(x, c));
   }
   __device__ static float out(double acc) { return __double2float_rn(acc); }
 };
@@ -240,7 +265,7 @@ __device__ __forceinline__ double row_serial(const V *__restrict__ sv,
       }
     }
 #pragma unroll
-    for (int j = 0; j < B; ++j) xv[j] = __ldg(x + c[j]);
+    for (int j = 0; j < B; ++j) xv[j] = ldg_x(x, c[j]);
     if constexpr (sizeof(V) == 8) {
 #pragma unroll
       for (int j = 0; j < B; ++j)
@@ -280,7 +305,7 @@ __device__ __forceinline__ double lane_partial(const V *__restrict__ sv,
       }
     }
 #pragma unroll
-    for (int j = 0; j < B; ++j) xv[j] = __ldg(x + c[j]);
+    for (int j = 0; j < B; ++j) xv[j] = ldg_x(x, c[j]);
     if constexpr (sizeof(V) == 8) {
 #pragma unroll
       for (int j = 0; j < B; ++j)
