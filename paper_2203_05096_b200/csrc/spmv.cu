@@ -499,7 +499,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                        uint32_t cap, uint32_t rcap, uint32_t stages, uint32_t long_len,
                        const uint32_t *__restrict__ tile_long,
                        const uint2 *__restrict__ holes, uint64_t x_bytes,
-                       uint32_t pf_chunk, uint64_t pf_nnz, uint64_t pf_rows) {
+                       uint32_t pf_chunk) {
   extern __shared__ __align__(128) unsigned char smem[];
   const Geometry geo(cap, rcap, stages, sizeof(V));
   uint64_t *full = reinterpret_cast<uint64_t *>(smem);
@@ -535,27 +535,6 @@ __global__ void __launch_bounds__(kThreads, 2)
         if (b) l2_prefetch_bulk(reinterpret_cast<const unsigned char *>(x) + off, b,
                                 evict_last_policy());
       }
-    }
-    // small matrices (working set well inside L2, launch_stream): the whole
-    // matrix is pulled into L2 at kernel start, CTA b a 1 / grid slice of
-    // each array, so HBM streams at full rate from the first microsecond
-    // instead of one tile round trip at a time per CTA; the tiles' TMA
-    // copies then hit L2 (same bytes from HBM, once)
-    if (pf_nnz) {
-      auto slice = [&](const void *base, uint64_t bytes) {
-        const uint64_t c = ((bytes + grid - 1) / grid + 15) & ~15ull;
-        const uint64_t off = static_cast<uint64_t>(blockIdx.x) * c;
-        if (off < bytes) {
-          const uint64_t b = ((bytes - off < c ? bytes - off : c) + 15) & ~15ull;
-          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
-                           reinterpret_cast<const unsigned char *>(base) + off),
-                       "r"(static_cast<uint32_t>(b))
-                       : "memory");
-        }
-      };
-      slice(vals, pf_nnz * sizeof(V));
-      slice(col_idx, pf_nnz * 4);
-      slice(row_ptr, (pf_rows + 1) * 4);
     }
     // the next tile's bounds (rows and their nonzero offsets, precomputed in
     // the plan) load while this tile waits for its stage: the producer never
@@ -999,16 +978,6 @@ uint64_t x_prefetch_limit() {
   return lim;
 }
 
-// launches whose working set is at most this are prefetched into L2 whole
-// (CSRK_MAT_PREFETCH=<MB> overrides; 0 disables)
-uint64_t matrix_prefetch_limit() {
-  static const uint64_t lim = [] {
-    const char *e = std::getenv("CSRK_MAT_PREFETCH");
-    return e ? static_cast<uint64_t>(std::atoll(e)) << 20 : (96ull << 20);
-  }();
-  return lim;
-}
-
 template <typename V, int NX, bool GF, int LB = 4>
 int launch_stream(const csrk_matrix *m, const V *vals, const V *x, V *y,
                   cudaStream_t stream, int64_t t0, int64_t t1) {
@@ -1080,24 +1049,12 @@ int launch_stream(const csrk_matrix *m, const V *vals, const V *x, V *y,
     c = (c + 4095) / 4096 * 4096;
     pf_chunk = static_cast<uint32_t>(c);
   }
-  // whole-matrix L2 prefetch when the launch's working set (matrix, x, y)
-  // is within matrix_prefetch_limit() (CSRK_MAT_PREFETCH=<MB>; 0 disables)
-  uint64_t pf_nnz = 0, pf_rows = 0;
-  {
-    const uint64_t ws = static_cast<uint64_t>(m->nnz) * (sizeof(V) + 4) +
-                        static_cast<uint64_t>(m->n_rows + 1) * 4 + x_bytes +
-                        static_cast<uint64_t>(m->n_rows) * sizeof(V);
-    if (t0 == 0 && t1 == pl.n_tiles && m->nnz > 0 && ws <= matrix_prefetch_limit()) {
-      pf_nnz = static_cast<uint64_t>(m->nnz);
-      pf_rows = static_cast<uint64_t>(m->n_rows);
-    }
-  }
   kern<<<static_cast<unsigned>(grid), kThreads, smem, stream>>>(
       m->row_ptr, m->col_idx, vals, x, y, pl.tile_row + t0, pl.tile_ptr + t0,
       static_cast<uint32_t>(count), geo.cap, geo.rcap, geo.stages,
       m->plan.n_long > 0 ? static_cast<uint32_t>(kLongRow) : 0xffffffffu,
       m->plan.n_long > 0 ? pl.tile_long + t0 : nullptr,
-      long_holes(pl), x_bytes, pf_chunk, pf_nnz, pf_rows);
+      long_holes(pl), x_bytes, pf_chunk);
   CSRK_CUDA_TRY(cudaGetLastError());
   return CSRK_OK;
 }
