@@ -419,9 +419,12 @@ def run_loop(args, log):
     ms = ev0.elapsed_time(ev1) / args.steps
     spmv_flops = 2.0 * nnz * iters
     gflops = spmv_flops / (ms * 1e-3) / 1e9
-    # bytes per iteration: the SpMV plus the vector kernels (CG: p.Ap reads 2n,
-    # update reads 4n writes 2n, direction reads 2n writes n; power: 2n + 2n)
-    vec_words = 11 * n if args.loop == "cg" else 4 * n
+    # bytes per iteration: the SpMV plus the vector kernels (CG: update reads
+    # 4n writes 2n, direction reads 2n writes n, and p.Ap -- fused into the
+    # SpMV's epilogue for this serial-order launch, csrk_cg, so it reads no
+    # vector of its own -- power: 2n + 2n)
+    fused_dot = args.loop == "cg" and os.environ.get("CSRK_NO_FUSED_DOT") is None
+    vec_words = (9 * n if fused_dot else 11 * n) if args.loop == "cg" else 4 * n
     it_bytes = spmv_bytes(n, n, nnz, vb) + vec_words * vb
     gbs = it_bytes * iters / (ms * 1e-3) / 1e9
     peak, peak_src = measured_peak()
@@ -464,7 +467,7 @@ def run_loop(args, log):
                 "h2d_bytes_per_step": n * vb, "d2h_bytes_per_step": n * vb,
                 "ms_per_step": round(e2e_s * 1e3, 3),
                 "call": f"paper_2203_05096_b200.cg.{'cg' if args.loop == 'cg' else 'power_iterations'}"},
-        "gpu_launches": args.steps * iters * (5 if args.loop == "cg" else 3),
+        "gpu_launches": args.steps * iters * ((4 if fused_dot else 5) if args.loop == "cg" else 3),
         "clocks": clk.summary(),
     }
 

@@ -316,9 +316,18 @@ int cg_run(const csrk_matrix *m, int value_type, int variant, int nx, const T *b
     cg_init_scalar_kernel<<<1, 32, 0, s>>>(w.rr_part, w.sc);
   }
   for (int it = 0; rc == CSRK_OK && it < iters; ++it) {
-    rc = launch_spmv(m, value_type, variant, nx, p, ap, s);
+    // Ap = A p with the p . Ap partials fused into the SpMV when the launch
+    // allows it (serial inline order, no long rows): saves re-reading p and
+    // Ap; otherwise the separate dot kernel
+    bool fused = false;
+    rc = launch_spmv_dot(m, value_type, variant, nx, p, ap, s, w.pap_part, kRedBlocks,
+                         &fused);
+    if (rc == CSRK_OK && !fused) {
+      rc = launch_spmv(m, value_type, variant, nx, p, ap, s);
+      if (rc == CSRK_OK)
+        dot_partial_kernel<T><<<kRedBlocks, kRedThreads, 0, s>>>(p, ap, n, w.pap_part);
+    }
     if (rc != CSRK_OK) break;
-    dot_partial_kernel<T><<<kRedBlocks, kRedThreads, 0, s>>>(p, ap, n, w.pap_part);
     cg_update_kernel<T><<<kRedBlocks, kRedThreads, 0, s>>>(x, r, p, ap, n, w.pap_part,
                                                           w.sc, w.rr_part);
     cg_direction_kernel<T><<<kRedBlocks, kRedThreads, 0, s>>>(p, r, n, w.rr_part, w.sc);

@@ -215,6 +215,9 @@ int prepare_plan(const csrk_matrix *m, int value_type, int variant, int nx);
 int launch_spmv(const csrk_matrix *m, int value_type, int variant, int nx,
                 const void *x, void *y, cudaStream_t stream, int64_t t0 = 0,
                 int64_t t1 = -1);
+int launch_spmv_dot(const csrk_matrix *m, int value_type, int variant, int nx,
+                    const void *x, void *y, cudaStream_t stream, double *dot_part,
+                    int64_t dot_slots, bool *fused);
 int chunk_max_cols(const csrk_matrix *m, const uint32_t *row_cut_dev, int chunks,
                    uint32_t *out_dev, cudaStream_t s);
 int launch_listing3(const csrk_matrix *m, int dx, int dy, const double *x,

@@ -413,21 +413,29 @@ __device__ __forceinline__ double subwarp_tree(double acc) {
 // rows [r0, r1) with staged (or global) arrays; `srp(r)` yields row_ptr[r]
 // Rows longer than `long_len` nonzeros are skipped: the long-row kernel
 // (below) sums them with a whole warp each.
-template <typename V, int NX, bool PROD = false, int LB = 4, typename RowPtr>
+template <typename V, int NX, bool PROD = false, int LB = 4, bool DOT = false,
+          typename RowPtr>
 __device__ __forceinline__ void compute_rows(uint32_t r0, uint32_t r1,
                                              const V *__restrict__ sv,
                                              const uint32_t *__restrict__ sc,
                                              RowPtr srp, const V *__restrict__ x,
                                              V *__restrict__ y, int ct,
-                                             uint32_t long_len = 0xffffffffu) {
+                                             uint32_t long_len = 0xffffffffu,
+                                             double *dot = nullptr) {
   if constexpr (NX == 0) {
     for (uint32_t r = r0 + ct; r < r1; r += kConsumers) {
       const uint32_t s = srp(r), e = srp(r + 1);
       if (e - s > long_len) continue;
+      V yr;
       if constexpr (PROD)
-        y[r] = Elem<V>::out(row_products<V>(sv, s, e));
+        yr = Elem<V>::out(row_products<V>(sv, s, e));
       else
-        y[r] = Elem<V>::out(row_serial<LB == 2 ? 4 : 8, V>(sv, sc, s, e, x));
+        yr = Elem<V>::out(row_serial<LB == 2 ? 4 : 8, V>(sv, sc, s, e, x));
+      y[r] = yr;
+      // fused x . y partial (the CG's p . Ap): x[r] * (stored y[r]) in f64
+      if constexpr (DOT)
+        *dot = __dadd_rn(*dot, __dmul_rn(static_cast<double>(ldg_x(x, r)),
+                                          static_cast<double>(yr)));
     }
   } else {
     constexpr int P = pow2_ceil(NX);
@@ -458,13 +466,14 @@ __device__ __forceinline__ void compute_rows(uint32_t r0, uint32_t r1,
 
 // a tile whose rows do not fit a stage: SERIAL rows are summed by whole
 // warps (products in parallel, ordered adds through shuffles)
-template <typename V, int NX>
+template <typename V, int NX, bool DOT = false>
 __device__ void compute_direct(uint32_t r0, uint32_t r1,
                                const uint32_t *__restrict__ row_ptr,
                                const uint32_t *__restrict__ col_idx,
                                const V *__restrict__ vals,
                                const V *__restrict__ x, V *__restrict__ y,
-                               int ct, uint32_t long_len = 0xffffffffu) {
+                               int ct, uint32_t long_len = 0xffffffffu,
+                               double *dot = nullptr) {
   if constexpr (NX == 0) {
     const int lane = ct & 31, warp = ct >> 5;
     for (uint32_t r = r0 + warp; r < r1; r += kConsumerWarps) {
@@ -481,7 +490,13 @@ __device__ void compute_direct(uint32_t r0, uint32_t r1,
         for (uint32_t j = 0; j < cnt; ++j)
           acc = __dadd_rn(acc, __shfl_sync(0xffffffffu, prod, j));
       }
-      if (lane == 0) y[r] = Elem<V>::out(acc);
+      if (lane == 0) {
+        const V yr = Elem<V>::out(acc);
+        y[r] = yr;
+        if constexpr (DOT)
+          *dot = __dadd_rn(*dot, __dmul_rn(static_cast<double>(ldg_x(x, r)),
+                                            static_cast<double>(yr)));
+      }
     }
   } else {
     compute_rows<V, NX>(r0, r1, vals, col_idx,
@@ -489,7 +504,7 @@ __device__ void compute_direct(uint32_t r0, uint32_t r1,
   }
 }
 
-template <typename V, int NX, bool GF, int LB = 4>
+template <typename V, int NX, bool GF, int LB = 4, bool DOT = false>
 __global__ void __launch_bounds__(kThreads, 2)
     csrk_stream_kernel(const uint32_t *__restrict__ row_ptr,
                        const uint32_t *__restrict__ col_idx,
@@ -499,7 +514,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                        uint32_t cap, uint32_t rcap, uint32_t stages, uint32_t long_len,
                        const uint32_t *__restrict__ tile_long,
                        const uint2 *__restrict__ holes, uint64_t x_bytes,
-                       uint32_t pf_chunk) {
+                       uint32_t pf_chunk, double *__restrict__ dot_part) {
   extern __shared__ __align__(128) unsigned char smem[];
   const Geometry geo(cap, rcap, stages, sizeof(V));
   uint64_t *full = reinterpret_cast<uint64_t *>(smem);
@@ -619,6 +634,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 
   // ---------------- consumer warps ----------------
   const int ct = tid - 32;
+  double dot = 0.0;  // DOT: this thread's x . y partial over its rows
   uint32_t s = 0, ph = 0;
   for (uint32_t t = blockIdx.x; t < n_tiles;
        t += grid, s = (s + 1 == stages) ? 0 : s + 1, ph ^= (s == 0)) {
@@ -641,15 +657,28 @@ __global__ void __launch_bounds__(kThreads, 2)
         // generic-proxy writes to the stage precede the next TMA fill of it
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       } else {
-        compute_rows<V, NX, false, LB>(md.r0, md.r1, sv, sc,
-                                       [&](uint32_t r) { return sr[r]; }, x, y, ct,
-                                       long_len);
+        compute_rows<V, NX, false, LB, DOT>(md.r0, md.r1, sv, sc,
+                                            [&](uint32_t r) { return sr[r]; }, x, y, ct,
+                                            long_len, &dot);
       }
     } else {
-      compute_direct<V, NX>(md.r0, md.r1, row_ptr, col_idx, vals, x, y, ct, long_len);
+      compute_direct<V, NX, DOT>(md.r0, md.r1, row_ptr, col_idx, vals, x, y, ct, long_len,
+                                 &dot);
     }
     __syncwarp();
     if ((ct & 31) == 0) mbar_arrive(&empty[s]);
+  }
+  if constexpr (DOT) {
+    // the CTA's partial in a fixed order: warp trees, then warps 0..7
+    __shared__ double red[kConsumerWarps];
+    for (int o = 16; o > 0; o >>= 1) dot = __dadd_rn(dot, __shfl_down_sync(0xffffffffu, dot, o));
+    if ((ct & 31) == 0) red[ct >> 5] = dot;
+    asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory");
+    if (ct == 0) {
+      double v = 0.0;
+      for (int w = 0; w < kConsumerWarps; ++w) v = __dadd_rn(v, red[w]);
+      dot_part[blockIdx.x] = v;
+    }
   }
 }
 
@@ -978,14 +1007,15 @@ uint64_t x_prefetch_limit() {
   return lim;
 }
 
-template <typename V, int NX, bool GF, int LB = 4>
+template <typename V, int NX, bool GF, int LB = 4, bool DOT = false>
 int launch_stream(const csrk_matrix *m, const V *vals, const V *x, V *y,
-                  cudaStream_t stream, int64_t t0, int64_t t1) {
+                  cudaStream_t stream, int64_t t0, int64_t t1,
+                  double *dot_part = nullptr, int64_t dot_slots = 0) {
   const TilePlan &pl = m->plan;
   const Geometry geo(static_cast<uint32_t>(pl.cap), static_cast<uint32_t>(pl.rcap),
                      static_cast<uint32_t>(pl.stages), sizeof(V));
   const size_t smem = geo.total_bytes();
-  auto kern = csrk_stream_kernel<V, NX, GF, LB>;
+  auto kern = csrk_stream_kernel<V, NX, GF, LB, DOT>;
   // attribute + occupancy queries cost host time per launch; cache them per
   // instantiation and shared-memory size (the chunked host pipeline launches
   // the kernel many times per SpMV)
@@ -1038,6 +1068,11 @@ int launch_stream(const csrk_matrix *m, const V *vals, const V *x, V *y,
   int64_t grid = static_cast<int64_t>(per_sm) * m->sm_count;
   if (grid > count) grid = count;
   if (grid < 1) return CSRK_OK;
+  if (DOT && grid > dot_slots) {
+    set_error("fused dot needs %lld partial slots, has %lld", static_cast<long long>(grid),
+              static_cast<long long>(dot_slots));
+    return CSRK_EINVAL;
+  }
   // x prefetch into L2 for whole-matrix launches whose x is small against
   // the 126 MB L2 (x_prefetch_bytes(), CSRK_X_PREFETCH), from a 16-byte
   // aligned x; slices of at least 4 KB
@@ -1054,7 +1089,7 @@ int launch_stream(const csrk_matrix *m, const V *vals, const V *x, V *y,
       static_cast<uint32_t>(count), geo.cap, geo.rcap, geo.stages,
       m->plan.n_long > 0 ? static_cast<uint32_t>(kLongRow) : 0xffffffffu,
       m->plan.n_long > 0 ? pl.tile_long + t0 : nullptr,
-      long_holes(pl), x_bytes, pf_chunk);
+      long_holes(pl), x_bytes, pf_chunk, dot_part);
   CSRK_CUDA_TRY(cudaGetLastError());
   return CSRK_OK;
 }
@@ -1522,6 +1557,39 @@ int chunk_max_cols(const csrk_matrix *m, const uint32_t *row_cut_dev, int chunks
   chunk_max_col_kernel<<<chunks, 256, 0, s>>>(m->row_ptr, m->col_idx, row_cut_dev,
                                              out_dev);
   CSRK_CUDA_TRY(cudaGetLastError());
+  return CSRK_OK;
+}
+
+// y = A x with the CTA partials of x . y written to dot_part[0, grid) (the
+// CG's p . Ap): fused into the streaming kernel for whole
+// launches in the serial order with inline gathers and no long rows -- the
+// dot kernel then need not re-read x and y (2 n values per iteration).
+// *fused = false (and nothing launched) otherwise; the caller runs the
+// plain SpMV and its own dot.
+int launch_spmv_dot(const csrk_matrix *m, int value_type, int variant, int nx,
+                    const void *x, void *y, cudaStream_t stream, double *dot_part,
+                    int64_t dot_slots, bool *fused) {
+  *fused = false;
+  if (variant != CSRK_SERIAL || m->n_rows == 0 || !m->plan.tile_row || m->plan.n_long > 0 ||
+      std::getenv("CSRK_NO_FUSED_DOT"))
+    return CSRK_OK;
+  if (value_type == CSRK_F64) {
+    if (!m->vals64) return CSRK_OK;
+    const int g = m->plan.gather_first;
+    if (g == 1 || (g == kGatherAuto && auto_gather(variant, nx, m->plan.mean_row, m->plan.row_var)))
+      return CSRK_OK;
+    *fused = true;
+    return launch_stream<double, 0, false, 4, true>(
+        m, m->vals64, static_cast<const double *>(x), static_cast<double *>(y), stream, 0,
+        m->plan.n_tiles, dot_part, dot_slots);
+  }
+  if (value_type == CSRK_F32) {
+    if (!m->vals32) return CSRK_OK;
+    *fused = true;
+    return launch_stream<float, 0, false, 4, true>(
+        m, m->vals32, static_cast<const float *>(x), static_cast<float *>(y), stream, 0,
+        m->plan.n_tiles, dot_part, dot_slots);
+  }
   return CSRK_OK;
 }
 

@@ -152,3 +152,24 @@ def test_long_rows_in_cg_graph_and_power(variant, nx):
               else O.spmv_strided(rp, ci, va, v, nx))
         v = yv * (1.0 / np.abs(yv).max())
     np.testing.assert_array_equal(xp.cpu().numpy(), v)
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_cg_fused_dot_matches_separate_dot(dtype, monkeypatch):
+    """p . Ap fused into the SpMV epilogue (per-CTA partials, fixed order)
+    against the separate dot kernel (CSRK_NO_FUSED_DOT=1): same iterates up
+    to the reduction order, deterministic run to run."""
+    a, res, m = _laplacian((28, 28, 28))
+    n = a.n_rows
+    b = torch.from_numpy(np.random.default_rng(4).uniform(-1, 1, n)).cuda()
+    if dtype == "f32":
+        b = b.float()
+    x_f, info_f = cg.cg(m, b, iters=40)
+    x_f2, _ = cg.cg(m, b, iters=40)
+    assert torch.equal(x_f, x_f2)
+    monkeypatch.setenv("CSRK_NO_FUSED_DOT", "1")
+    x_s, info_s = cg.cg(m, b, iters=40)
+    tol = 1e-9 if dtype == "f64" else 1e-3
+    assert (x_f.double() - x_s.double()).abs().max().item() <= tol * x_s.double().abs().max().item()
+    if dtype == "f64":
+        assert info_f["rr"] == pytest.approx(info_s["rr"], rel=1e-6)
