@@ -35,5 +35,10 @@ for c in "C2" "C2 --fp32" "C3" "C5" "C1"; do
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:csrk_stream -s 3 -c 1 \
     -o $O/${tag}_full python bench.py --config $c --steps 1 --warmup 3 --cpu-budget 0.2 > /dev/null 2>&1
   echo "ncu $c rc=$?"
+  # summaries on the box (gpurun brings back at most 64 MiB): key metrics,
+  # stall reasons, source-level hot spots; the report itself only for C2 / C5
+  python tools/ncu_summary.py $O/${tag}_full.ncu-rep > $O/${tag}_stream_ncu_full.txt 2>&1
+  ncu -i $O/${tag}_full.ncu-rep --page raw --csv > $O/${tag}_raw.csv 2>/dev/null
+  if [ "$tag" != "C2" ] && [ "$tag" != "C5" ]; then rm -f $O/${tag}_full.ncu-rep; fi
 done
 for f in $O/bench_*.json; do echo "== $f"; head -c 400 $f; echo; done
