@@ -28,7 +28,7 @@ for cfg in C1 C3 C5; do
   timeout 900 python bench.py --impl reference --config $cfg > $O/bench_reference_$cfg.json 2> $O/bench_reference_$cfg.err; echo "ref $cfg rc=$?"
 done
 # launch list of the default bench command (cold-cache, serialised per-launch times)
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches_C2_bench.csv \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"csrk_stream|long_rows" -c 60 --csv --log-file $O/launches_C2_bench.csv \
   python bench.py --steps 2 --warmup 1 --cpu-budget 0.5 > /dev/null 2>&1; echo "ncu launches rc=$?"
 for c in "C2" "C2 --fp32" "C3" "C5" "C1"; do
   tag=$(echo $c | tr -d ' -')
