@@ -671,9 +671,12 @@ def main(argv=None):
     ap.add_argument("--partition", choices=("blocks", "slab"), default="blocks",
                     help="N > 1, C2: SSR row blocks of the CSR-k matrix (strong scaling, "
                          "default) or round 1's weak-scaling z-slabs")
-    ap.add_argument("--mg", choices=("torch", "native"), default="torch",
+    ap.add_argument("--mg", choices=("torch", "native"), default="native",
                     help="N > 1, SSR blocks: exchange through torch.distributed (DistSpMV) "
                          "or the library's C-ABI (csrk_mg_*, NativeDistSpMV)")
+    ap.add_argument("--no-graph", dest="graph", action="store_false",
+                    help="N > 1 with --mg native: time eager steps instead of one CUDA "
+                         "graph of the K steps")
     ap.add_argument("--probe-launch", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args(argv)
     world_env = os.environ.get("WORLD_SIZE")

@@ -1240,13 +1240,41 @@ def bench_blocks(args, log, rank: int, world: int, local: int, sampler=None, pea
     torch.cuda.synchronize()
     if clk_ctx is not None:
         time.sleep(0.3)
+    # host enqueue cost of one step (Python + NCCL + launches): at N = 8 a
+    # C2 block takes ~35 us on the GPU, so a step that costs the host more
+    # than that starves the device
+    torch.cuda.synchronize()
+    th = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    host_us = (time.perf_counter() - th) / args.steps * 1e6
+    torch.cuda.synchronize()
+    # the C-ABI path: the K timed steps captured once into a CUDA graph
+    # (NCCL send / recv, the interior / boundary launches and their events
+    # are all stream-ordered), replayed in the timed region
+    graph = None
+    if native and getattr(args, "graph", True):
+        try:
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                for _ in range(args.steps):
+                    step()
+            graph.replay()
+            torch.cuda.synchronize()
+        except Exception as exc:  # capture unsupported here: time eager steps
+            log(f"[bench] CUDA graph capture of the native steps failed ({exc}); eager steps")
+            graph = None
+            torch.cuda.synchronize()
     dist.barrier()
     torch.cuda.synchronize()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     ev0.record()
-    for _ in range(args.steps):
-        step()
+    if graph is not None:
+        graph.replay()
+    else:
+        for _ in range(args.steps):
+            step()
     ev1.record()
     torch.cuda.synchronize()
     dist.barrier()
@@ -1254,6 +1282,7 @@ def bench_blocks(args, log, rank: int, world: int, local: int, sampler=None, pea
         clk_ctx.__exit__(None, None, None)
     ms_rank = ev0.elapsed_time(ev1) / args.steps
     ms = _max_over_ranks(ms_rank)
+    host_us = _max_over_ranks(host_us)
     # parity of this rank's rows against the oracle (the timed output)
     ok = True
     max_diff = 0.0
@@ -1327,6 +1356,8 @@ def bench_blocks(args, log, rank: int, world: int, local: int, sampler=None, pea
                      "algorithmic_bytes_per_launch": op.local_bytes(vb)},
         "t1_ms": round(t1_ms, 4) if t1_ms else None,
         "efficiency_t1_over_n_tn": round(t1_ms / (world * ms), 4) if t1_ms else None,
+        "host_enqueue_us_per_step_max": round(host_us, 1),
+        "timed_as": "one CUDA graph of the K steps" if graph is not None else "K eager steps",
         "parity": {"kind": "scaled 1e-5" if f32 else "bitwise", "ok": bool(ok_all),
                    "against": "oracle/csrk_oracle.c on the same CSR-k matrix and x",
                    "max_abs_diff_rank0": max_diff},

@@ -463,7 +463,7 @@ def test_dist_cg_over_gloo(world):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("config", ["C2", "C2-native", "C2-slab", "C4"])
+@pytest.mark.parametrize("config", ["C2", "C2-torch", "C2-slab", "C4"])
 def test_bench_multi_gpu_path_one_rank(config):
     """bench.py's torchrun path (NCCL process group, SSR row blocks with the
     halo exchange and the oracle parity check, the slab partition, the
@@ -480,8 +480,8 @@ def test_bench_multi_gpu_path_one_rank(config):
            "--steps", "3", "--warmup", "3", "--config", config.split("-")[0]]
     if config == "C2-slab":
         cmd += ["--partition", "slab"]
-    if config == "C2-native":
-        cmd += ["--mg", "native"]
+    if config == "C2-torch":
+        cmd += ["--mg", "torch"]
     if config == "C4":
         cmd += ["--side", "96", "--iters", "10"]
     env = dict(os.environ, CSRK_DIST="1")
@@ -493,7 +493,7 @@ def test_bench_multi_gpu_path_one_rank(config):
         assert key in line, key
     assert line["n_gpus"] == 1 and line["value"] > 0
     assert line["scaling"] == ("weak" if config == "C2-slab" else "strong")
-    if config in ("C2", "C2-native"):
+    if config in ("C2", "C2-torch"):
         assert line["parity"]["ok"] and line["efficiency_t1_over_n_tn"] > 0
     assert line["e2e"]["h2d_bytes_per_step"] > 0
 
