@@ -495,6 +495,9 @@ def test_bench_multi_gpu_path_one_rank(config):
     assert line["scaling"] == ("weak" if config == "C2-slab" else "strong")
     if config in ("C2", "C2-torch"):
         assert line["parity"]["ok"] and line["efficiency_t1_over_n_tn"] > 0
+        # default: the C-ABI path with its timed steps in one CUDA graph
+        assert line["timed_as"] == ("K eager steps" if config == "C2-torch"
+                                    else "one CUDA graph of the K steps")
     assert line["e2e"]["h2d_bytes_per_step"] > 0
 
 
