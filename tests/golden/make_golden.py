@@ -9,6 +9,8 @@ the committed files this script writes):
     python tests/golden/make_golden.py large      # ~20 min -> configs.json
     python tests/golden/make_golden.py b200 [C2 C3 C5 C1]   # adds runs at the
                                                   # B200 profile's targets
+    python tests/golden/make_golden.py mm         # ~20 s  -> mm.json (Matrix
+                                                  # Market ingest, mm_cases.py)
 
 ``small`` stores full arrays for many small matrices (the shapes of the
 reference's own sweep, pkg/tests/test_acceptance.py:86-154, plus the kernel
@@ -360,6 +362,38 @@ def configs(which):
     print(f"wrote {path}")
 
 
+def mm():
+    """Matrix Market ingest (io.py:96-206), writer (209-230) and permutation
+    files (278-299) of the reference on the deterministic cases of
+    mm_cases.py: digests of the CSR arrays it reads, of the text it writes
+    back, and of a permutation file."""
+    import io as _io
+
+    sys.path.insert(0, HERE)
+    import mm_cases
+
+    out = {}
+    for name in mm_cases.CASES:
+        t0 = time.time()
+        a = ref.io.read_matrix_market(_io.StringIO(mm_cases.mm_text(name)))
+        w = _io.StringIO()
+        ref.io.write_matrix_market(a, w)
+        perm = ref.Permutation.from_forward(mm_cases.perm_of(a.n_rows))
+        pf = _io.StringIO()
+        ref.io.write_permutation_file(perm, pf)
+        out[name] = {"n_rows": a.n_rows, "n_cols": a.n_cols, "nnz": a.nnz,
+                     "row_ptr": digest(a.row_ptr, "<u4"), "col_idx": digest(a.col_idx, "<u4"),
+                     "vals": digest(a.vals, "<f8"),
+                     "written": hashlib.sha256(w.getvalue().encode()).hexdigest(),
+                     "perm_file": hashlib.sha256(pf.getvalue().encode()).hexdigest()}
+        print(f"{name}: nnz {a.nnz} ({time.time() - t0:.1f}s)", flush=True)
+    path = os.path.join(HERE, "mm.json")
+    with open(path, "w") as fh:
+        json.dump(out, fh, indent=1, sort_keys=True)
+        fh.write("\n")
+    print(f"wrote {path}")
+
+
 if __name__ == "__main__":
     mode = sys.argv[1] if len(sys.argv) > 1 else "small"
     if mode == "small":
@@ -368,5 +402,7 @@ if __name__ == "__main__":
         configs(mode)
     elif mode == "b200":
         add_b200_runs()
+    elif mode == "mm":
+        mm()
     else:
         raise SystemExit(f"unknown mode {mode}")

@@ -200,3 +200,64 @@ def test_native_matrix_market_body_equals_python_loop(tmp_path, monkeypatch, fie
         native, python = both()
         assert native == python
         assert isinstance(native, str) and native.startswith(f"line {k + 1}:")
+
+
+def _mm_golden():
+    import json
+    import os
+    import sys
+
+    here = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+    sys.path.insert(0, here)
+    import mm_cases
+    with open(os.path.join(here, "mm.json")) as fh:
+        return mm_cases, json.load(fh)
+
+
+def _sha(b: bytes) -> str:
+    import hashlib
+    return hashlib.sha256(b).hexdigest()
+
+
+def _check_mm_case(tmp_path, name, mm_cases, want):
+    import io as _io
+
+    from paper_2203_05096_b200 import io as mio
+    path = tmp_path / f"{name}.mtx"
+    path.write_text(mm_cases.mm_text(name))
+    a = mio.read_matrix_market(str(path))
+    assert (a.n_rows, a.n_cols, a.nnz) == (want["n_rows"], want["n_cols"], want["nnz"])
+    assert _sha(np.ascontiguousarray(a.row_ptr, dtype="<u4").tobytes()) == want["row_ptr"]
+    assert _sha(np.ascontiguousarray(a.col_idx, dtype="<u4").tobytes()) == want["col_idx"]
+    assert _sha(np.ascontiguousarray(a.vals, dtype="<f8").tobytes()) == want["vals"]
+    w = _io.StringIO()
+    mio.write_matrix_market(a, w)
+    assert _sha(w.getvalue().encode()) == want["written"]
+    pf = _io.StringIO()
+    mio.write_permutation_file(ck.Permutation.from_forward(mm_cases.perm_of(a.n_rows)), pf)
+    assert _sha(pf.getvalue().encode()) == want["perm_file"]
+
+
+@pytest.mark.parametrize("native", [False, True])
+def test_matrix_market_ingest_equals_reference_goldens(tmp_path, monkeypatch, native):
+    """Matrix Market -> canonical CSR (symmetric / skew / pattern expansion,
+    duplicates summed), the writer and permutation files: digests the
+    unmodified reference wrote (tests/golden/mm.json, make_golden.py mm).
+    The body is parsed by the native parser (csrk_mm_parse, all host
+    cores) or the line loop; canonicalisation on the host here."""
+    from paper_2203_05096_b200 import format as F
+    from paper_2203_05096_b200 import io as mio
+    monkeypatch.setattr(F, "DEVICE_COO_MIN", 1 << 62)
+    monkeypatch.setattr(mio, "NATIVE_MIN_ENTRIES", 1 if native else 1 << 62)
+    mm_cases, gold = _mm_golden()
+    for name in mm_cases.CASES:
+        _check_mm_case(tmp_path, name, mm_cases, gold[name])
+
+
+@pytest.mark.gpu
+def test_matrix_market_ingest_on_device_equals_reference_goldens(tmp_path):
+    """The same with the default thresholds: the large cases canonicalise
+    on the GPU (csrk_coo_to_csr, >= 64 K triplets after expansion)."""
+    mm_cases, gold = _mm_golden()
+    for name in mm_cases.CASES:
+        _check_mm_case(tmp_path, name, mm_cases, gold[name])
