@@ -261,3 +261,19 @@ def test_matrix_market_ingest_on_device_equals_reference_goldens(tmp_path):
     mm_cases, gold = _mm_golden()
     for name in mm_cases.CASES:
         _check_mm_case(tmp_path, name, mm_cases, gold[name])
+
+
+def test_packaged_manifest_equals_reference():
+    """load_manifest() with no argument reads the packaged manifest of the
+    paper's 64 matrices (data/manifest.csv, generated from PAPER.md's
+    benchmark-suite table by tools/make_manifest.py): entry for entry what
+    the reference's load_manifest() returns (digest in mm.json)."""
+    import hashlib
+
+    from paper_2203_05096_b200 import io as mio
+    _, gold = _mm_golden()
+    ents = mio.load_manifest()
+    assert len(ents) == gold["_manifest"]["count"] == 64
+    got = hashlib.sha256(repr([tuple(e.__dict__.values()) for e in ents]).encode()).hexdigest()
+    assert got == gold["_manifest"]["entries"]
+    assert sum(e.matrix_class == "regular" for e in ents) == 35
