@@ -1088,13 +1088,34 @@ def bench_cg_slabs(args, log, rank: int, world: int, local: int, sampler=None, p
                torch.empty_like(b))
     iters = args.iters
 
-    def step():
+    def eager_step():
         x.zero_()
         solver.run(b, x, iters, scratch=scratch)
 
     for _ in range(max(3, args.warmup)):
-        step()
+        eager_step()
     torch.cuda.synchronize()
+    # one step = one replay of the whole run captured as a CUDA graph (SpMV
+    # launches, halo point-to-point, all-reduces and step kernels): the host
+    # enqueues ~10 operations per iteration, which at N = 8 (0.5 ms of GPU
+    # work per iteration) it could otherwise only just keep ahead of
+    graph = None
+    if getattr(args, "graph", True):
+        try:
+            graph = solver.graphed(b, x, iters, scratch=scratch)
+            graph.replay()
+            torch.cuda.synchronize()
+        except Exception as exc:
+            log(f"[bench] CUDA graph capture of the distributed CG failed ({exc}); eager")
+            graph = None
+            torch.cuda.synchronize()
+
+    def step():
+        if graph is not None:
+            graph.replay()
+        else:
+            eager_step()
+
     dist.barrier()
     clk_ctx = sampler(torch.cuda.current_device()) if (sampler and rank == 0) else None
     if clk_ctx is not None:
@@ -1154,7 +1175,8 @@ def bench_cg_slabs(args, log, rank: int, world: int, local: int, sampler=None, p
                 "d2h_bytes_per_step": lay.n_own * vb * world,
                 "ms_per_step": round(e2e_s * 1e3, 3), "call": "dist.DistCG.run per rank"},
         "cpu_baseline": None,
-        "gpu_launches": args.steps * iters * op.launches_per_step,
+        "gpu_launches": args.steps * iters * solver.launches_per_iteration(),
+        "timed_as": "one CUDA graph per step" if graph is not None else "eager steps",
         "clocks": clk_ctx.summary() if clk_ctx is not None else None,
     }
 

@@ -499,6 +499,8 @@ def test_bench_multi_gpu_path_one_rank(config):
         assert line["timed_as"] == ("K eager steps" if config == "C2-torch"
                                     else "one CUDA graph of the K steps")
     assert line["e2e"]["h2d_bytes_per_step"] > 0
+    if config == "C4":
+        assert line["timed_as"] == "one CUDA graph per step"
 
 
 @pytest.mark.gpu
@@ -606,3 +608,22 @@ def test_native_mg_blocks_bitwise(variant, nx):
             got.append(yo.cpu().numpy())
             nd.close()
         np.testing.assert_array_equal(np.concatenate(got), want)
+
+
+@pytest.mark.gpu
+def test_dist_cg_graph_replay_equals_eager_one_rank():
+    """DistCG.graphed (SpMV launches, step kernels and, at N > 1, the halo
+    and the all-reduces captured into one CUDA graph) gives the eager run's
+    bits; one rank, no process group."""
+    op = D.SlabSpMV((24, 24, 24), 7, 0, 1)
+    n = op.lay.n_own
+    b = torch.from_numpy(np.random.default_rng(9).uniform(-1, 1, n)).cuda()
+    solver = D.DistCG(op)
+    x_e = torch.zeros_like(b)
+    solver.run(b, x_e, 20)
+    x_g = torch.zeros_like(b)
+    g = solver.graphed(b, x_g, 20)
+    x_g.fill_(123.0)
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(x_g, x_e)
