@@ -430,7 +430,7 @@ __device__ __forceinline__ void compute_rows(uint32_t r0, uint32_t r1,
       if constexpr (PROD)
         yr = Elem<V>::out(row_products<V>(sv, s, e));
       else
-        yr = Elem<V>::out(row_serial<LB == 2 ? 4 : 8, V>(sv, sc, s, e, x));
+        yr = Elem<V>::out(row_serial<LB == 2 ? 4 : (LB == 7 ? 7 : 8), V>(sv, sc, s, e, x));
       y[r] = yr;
       // fused x . y partial (the CG's p . Ap): x[r] * (stored y[r]) in f64
       if constexpr (DOT)
@@ -1193,6 +1193,7 @@ int dispatch_main(const csrk_matrix *m, int variant, int nx, const V *vals,
       return e ? std::atoi(e) : 8;
     }();
     if (sb == 4) return launch_stream<V, 0, GF, 2>(m, vals, x, y, s, t0, t1);
+    if (sb == 7) return launch_stream<V, 0, GF, 7>(m, vals, x, y, s, t0, t1);
     return launch_stream<V, 0, GF>(m, vals, x, y, s, t0, t1);
   }
   // Lanes gather LB of their strided elements per batch: 8 when a lane holds
