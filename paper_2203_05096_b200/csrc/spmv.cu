@@ -143,6 +143,135 @@ __device__ __forceinline__ float ldg_x(const float *x, uint32_t c) {
   return v;
 }
 
+// x gathers of one batch: slot j loads x[c[j]] when j < cnt (the lanes past
+// the row end issue no load -- each cost an extra 128-byte line of the
+// L1TEX data pipe, x[0], per load instruction: ~9 % of C5's gather
+// wavefronts).  One asm block per batch, so all of its loads are issued
+// back to back, each into its own register (predicating them in C++ let
+// ptxas split the batch and serialise the loads).  Batches of other sizes
+// use the per-slot form.
+#ifndef CSRK_PRED_LDG
+#define CSRK_PRED_LDG 1
+#endif
+template <int B, typename V>
+__device__ __forceinline__ void gather_batch(const V *x, const uint32_t (&c)[B], uint32_t cnt,
+                                             V (&xv)[B]) {
+#pragma unroll
+  for (int j = 0; j < B; ++j) xv[j] = ldg_x(x, static_cast<uint32_t>(j) < cnt ? c[j] : 0u);
+}
+template <>
+__device__ __forceinline__ void gather_batch<8, double>(const double *x, const uint32_t (&c)[8], uint32_t cnt,
+                                             double (&xv)[8]) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j) xv[j] = 0.0;
+  asm("{\n\t.reg .pred q<8>;\n\t.reg .u64 a<8>;\n\t"
+      "setp.gt.u32 q0, %17, 0;\n\t"
+      "setp.gt.u32 q1, %17, 1;\n\t"
+      "setp.gt.u32 q2, %17, 2;\n\t"
+      "setp.gt.u32 q3, %17, 3;\n\t"
+      "setp.gt.u32 q4, %17, 4;\n\t"
+      "setp.gt.u32 q5, %17, 5;\n\t"
+      "setp.gt.u32 q6, %17, 6;\n\t"
+      "setp.gt.u32 q7, %17, 7;\n\t"
+      "mul.wide.u32 a0, %8, 8;\n\tadd.u64 a0, a0, %16;\n\t"
+      "mul.wide.u32 a1, %9, 8;\n\tadd.u64 a1, a1, %16;\n\t"
+      "mul.wide.u32 a2, %10, 8;\n\tadd.u64 a2, a2, %16;\n\t"
+      "mul.wide.u32 a3, %11, 8;\n\tadd.u64 a3, a3, %16;\n\t"
+      "mul.wide.u32 a4, %12, 8;\n\tadd.u64 a4, a4, %16;\n\t"
+      "mul.wide.u32 a5, %13, 8;\n\tadd.u64 a5, a5, %16;\n\t"
+      "mul.wide.u32 a6, %14, 8;\n\tadd.u64 a6, a6, %16;\n\t"
+      "mul.wide.u32 a7, %15, 8;\n\tadd.u64 a7, a7, %16;\n\t"
+      "@q0 ld.global.nc.f64 %0, [a0];\n\t"
+      "@q1 ld.global.nc.f64 %1, [a1];\n\t"
+      "@q2 ld.global.nc.f64 %2, [a2];\n\t"
+      "@q3 ld.global.nc.f64 %3, [a3];\n\t"
+      "@q4 ld.global.nc.f64 %4, [a4];\n\t"
+      "@q5 ld.global.nc.f64 %5, [a5];\n\t"
+      "@q6 ld.global.nc.f64 %6, [a6];\n\t"
+      "@q7 ld.global.nc.f64 %7, [a7];\n\t"
+      "}"
+      : "+d"(xv[0]), "+d"(xv[1]), "+d"(xv[2]), "+d"(xv[3]), "+d"(xv[4]), "+d"(xv[5]), "+d"(xv[6]), "+d"(xv[7])
+      : "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(c[5]), "r"(c[6]), "r"(c[7]), "l"(x), "r"(cnt));
+}
+template <>
+__device__ __forceinline__ void gather_batch<8, float>(const float *x, const uint32_t (&c)[8], uint32_t cnt,
+                                             float (&xv)[8]) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j) xv[j] = 0.0f;
+  asm("{\n\t.reg .pred q<8>;\n\t.reg .u64 a<8>;\n\t"
+      "setp.gt.u32 q0, %17, 0;\n\t"
+      "setp.gt.u32 q1, %17, 1;\n\t"
+      "setp.gt.u32 q2, %17, 2;\n\t"
+      "setp.gt.u32 q3, %17, 3;\n\t"
+      "setp.gt.u32 q4, %17, 4;\n\t"
+      "setp.gt.u32 q5, %17, 5;\n\t"
+      "setp.gt.u32 q6, %17, 6;\n\t"
+      "setp.gt.u32 q7, %17, 7;\n\t"
+      "mul.wide.u32 a0, %8, 4;\n\tadd.u64 a0, a0, %16;\n\t"
+      "mul.wide.u32 a1, %9, 4;\n\tadd.u64 a1, a1, %16;\n\t"
+      "mul.wide.u32 a2, %10, 4;\n\tadd.u64 a2, a2, %16;\n\t"
+      "mul.wide.u32 a3, %11, 4;\n\tadd.u64 a3, a3, %16;\n\t"
+      "mul.wide.u32 a4, %12, 4;\n\tadd.u64 a4, a4, %16;\n\t"
+      "mul.wide.u32 a5, %13, 4;\n\tadd.u64 a5, a5, %16;\n\t"
+      "mul.wide.u32 a6, %14, 4;\n\tadd.u64 a6, a6, %16;\n\t"
+      "mul.wide.u32 a7, %15, 4;\n\tadd.u64 a7, a7, %16;\n\t"
+      "@q0 ld.global.nc.f32 %0, [a0];\n\t"
+      "@q1 ld.global.nc.f32 %1, [a1];\n\t"
+      "@q2 ld.global.nc.f32 %2, [a2];\n\t"
+      "@q3 ld.global.nc.f32 %3, [a3];\n\t"
+      "@q4 ld.global.nc.f32 %4, [a4];\n\t"
+      "@q5 ld.global.nc.f32 %5, [a5];\n\t"
+      "@q6 ld.global.nc.f32 %6, [a6];\n\t"
+      "@q7 ld.global.nc.f32 %7, [a7];\n\t"
+      "}"
+      : "+f"(xv[0]), "+f"(xv[1]), "+f"(xv[2]), "+f"(xv[3]), "+f"(xv[4]), "+f"(xv[5]), "+f"(xv[6]), "+f"(xv[7])
+      : "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(c[5]), "r"(c[6]), "r"(c[7]), "l"(x), "r"(cnt));
+}
+template <>
+__device__ __forceinline__ void gather_batch<4, double>(const double *x, const uint32_t (&c)[4], uint32_t cnt,
+                                             double (&xv)[4]) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) xv[j] = 0.0;
+  asm("{\n\t.reg .pred q<4>;\n\t.reg .u64 a<4>;\n\t"
+      "setp.gt.u32 q0, %9, 0;\n\t"
+      "setp.gt.u32 q1, %9, 1;\n\t"
+      "setp.gt.u32 q2, %9, 2;\n\t"
+      "setp.gt.u32 q3, %9, 3;\n\t"
+      "mul.wide.u32 a0, %4, 8;\n\tadd.u64 a0, a0, %8;\n\t"
+      "mul.wide.u32 a1, %5, 8;\n\tadd.u64 a1, a1, %8;\n\t"
+      "mul.wide.u32 a2, %6, 8;\n\tadd.u64 a2, a2, %8;\n\t"
+      "mul.wide.u32 a3, %7, 8;\n\tadd.u64 a3, a3, %8;\n\t"
+      "@q0 ld.global.nc.f64 %0, [a0];\n\t"
+      "@q1 ld.global.nc.f64 %1, [a1];\n\t"
+      "@q2 ld.global.nc.f64 %2, [a2];\n\t"
+      "@q3 ld.global.nc.f64 %3, [a3];\n\t"
+      "}"
+      : "+d"(xv[0]), "+d"(xv[1]), "+d"(xv[2]), "+d"(xv[3])
+      : "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "l"(x), "r"(cnt));
+}
+template <>
+__device__ __forceinline__ void gather_batch<4, float>(const float *x, const uint32_t (&c)[4], uint32_t cnt,
+                                             float (&xv)[4]) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) xv[j] = 0.0f;
+  asm("{\n\t.reg .pred q<4>;\n\t.reg .u64 a<4>;\n\t"
+      "setp.gt.u32 q0, %9, 0;\n\t"
+      "setp.gt.u32 q1, %9, 1;\n\t"
+      "setp.gt.u32 q2, %9, 2;\n\t"
+      "setp.gt.u32 q3, %9, 3;\n\t"
+      "mul.wide.u32 a0, %4, 4;\n\tadd.u64 a0, a0, %8;\n\t"
+      "mul.wide.u32 a1, %5, 4;\n\tadd.u64 a1, a1, %8;\n\t"
+      "mul.wide.u32 a2, %6, 4;\n\tadd.u64 a2, a2, %8;\n\t"
+      "mul.wide.u32 a3, %7, 4;\n\tadd.u64 a3, a3, %8;\n\t"
+      "@q0 ld.global.nc.f32 %0, [a0];\n\t"
+      "@q1 ld.global.nc.f32 %1, [a1];\n\t"
+      "@q2 ld.global.nc.f32 %2, [a2];\n\t"
+      "@q3 ld.global.nc.f32 %3, [a3];\n\t"
+      "}"
+      : "+f"(xv[0]), "+f"(xv[1]), "+f"(xv[2]), "+f"(xv[3])
+      : "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "l"(x), "r"(cnt));
+}
+
 template <typename V>
 struct Elem;
 template <>
@@ -264,8 +393,12 @@ __device__ __forceinline__ double row_serial(const V *__restrict__ sv,
         v[j] = sv[q];
       }
     }
+    if (CSRK_PRED_LDG) {
+      gather_batch<B, V>(x, c, e - p, xv);
+    } else {
 #pragma unroll
-    for (int j = 0; j < B; ++j) xv[j] = ldg_x(x, c[j]);
+      for (int j = 0; j < B; ++j) xv[j] = ldg_x(x, c[j]);
+    }
     if constexpr (sizeof(V) == 8) {
 #pragma unroll
       for (int j = 0; j < B; ++j)
@@ -304,8 +437,12 @@ __device__ __forceinline__ double lane_partial(const V *__restrict__ sv,
         v[j] = sv[q];
       }
     }
+    if (CSRK_PRED_LDG) {
+      gather_batch<B, V>(x, c, (e - p + NX - 1) / NX, xv);
+    } else {
 #pragma unroll
-    for (int j = 0; j < B; ++j) xv[j] = ldg_x(x, c[j]);
+      for (int j = 0; j < B; ++j) xv[j] = ldg_x(x, c[j]);
+    }
     if constexpr (sizeof(V) == 8) {
 #pragma unroll
       for (int j = 0; j < B; ++j)
