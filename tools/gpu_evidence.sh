@@ -29,7 +29,7 @@ for cfg in C1 C3 C5; do
 done
 # launch list of the default bench command (cold-cache, serialised per-launch times)
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"csrk_stream|long_rows" -c 60 --csv --log-file $O/launches_C2_bench.csv \
-  python bench.py --steps 2 --warmup 1 --cpu-budget 0.5 > /dev/null 2>&1; echo "ncu launches rc=$?"
+  python bench.py --steps 20 --warmup 5 --cpu-budget 0.5 > /dev/null 2>&1; echo "ncu launches rc=$?"
 for c in "C2" "C2 --fp32" "C3" "C5" "C1"; do
   tag=$(echo $c | tr -d ' -')
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:csrk_stream -s 3 -c 1 \
