@@ -160,8 +160,8 @@ __device__ __forceinline__ void gather_batch(const V *x, const uint32_t (&c)[B],
   for (int j = 0; j < B; ++j) xv[j] = ldg_x(x, static_cast<uint32_t>(j) < cnt ? c[j] : 0u);
 }
 template <>
-__device__ __forceinline__ void gather_batch<8, double>(const double *x, const uint32_t (&c)[8], uint32_t cnt,
-                                             double (&xv)[8]) {
+__device__ __forceinline__ void gather_batch<8, double>(
+    const double *x, const uint32_t (&c)[8], uint32_t cnt, double (&xv)[8]) {
 #pragma unroll
   for (int j = 0; j < 8; ++j) xv[j] = 0.0;
   asm("{\n\t.reg .pred q<8>;\n\t.reg .u64 a<8>;\n\t"
@@ -190,12 +190,14 @@ __device__ __forceinline__ void gather_batch<8, double>(const double *x, const u
       "@q6 ld.global.nc.f64 %6, [a6];\n\t"
       "@q7 ld.global.nc.f64 %7, [a7];\n\t"
       "}"
-      : "+d"(xv[0]), "+d"(xv[1]), "+d"(xv[2]), "+d"(xv[3]), "+d"(xv[4]), "+d"(xv[5]), "+d"(xv[6]), "+d"(xv[7])
-      : "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(c[5]), "r"(c[6]), "r"(c[7]), "l"(x), "r"(cnt));
+      : "+d"(xv[0]), "+d"(xv[1]), "+d"(xv[2]), "+d"(xv[3]), "+d"(xv[4]), "+d"(xv[5]),
+        "+d"(xv[6]), "+d"(xv[7])
+      : "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(c[5]), "r"(c[6]), "r"(c[7]),
+        "l"(x), "r"(cnt));
 }
 template <>
-__device__ __forceinline__ void gather_batch<8, float>(const float *x, const uint32_t (&c)[8], uint32_t cnt,
-                                             float (&xv)[8]) {
+__device__ __forceinline__ void gather_batch<8, float>(
+    const float *x, const uint32_t (&c)[8], uint32_t cnt, float (&xv)[8]) {
 #pragma unroll
   for (int j = 0; j < 8; ++j) xv[j] = 0.0f;
   asm("{\n\t.reg .pred q<8>;\n\t.reg .u64 a<8>;\n\t"
@@ -224,12 +226,14 @@ __device__ __forceinline__ void gather_batch<8, float>(const float *x, const uin
       "@q6 ld.global.nc.f32 %6, [a6];\n\t"
       "@q7 ld.global.nc.f32 %7, [a7];\n\t"
       "}"
-      : "+f"(xv[0]), "+f"(xv[1]), "+f"(xv[2]), "+f"(xv[3]), "+f"(xv[4]), "+f"(xv[5]), "+f"(xv[6]), "+f"(xv[7])
-      : "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(c[5]), "r"(c[6]), "r"(c[7]), "l"(x), "r"(cnt));
+      : "+f"(xv[0]), "+f"(xv[1]), "+f"(xv[2]), "+f"(xv[3]), "+f"(xv[4]), "+f"(xv[5]),
+        "+f"(xv[6]), "+f"(xv[7])
+      : "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(c[5]), "r"(c[6]), "r"(c[7]),
+        "l"(x), "r"(cnt));
 }
 template <>
-__device__ __forceinline__ void gather_batch<4, double>(const double *x, const uint32_t (&c)[4], uint32_t cnt,
-                                             double (&xv)[4]) {
+__device__ __forceinline__ void gather_batch<4, double>(
+    const double *x, const uint32_t (&c)[4], uint32_t cnt, double (&xv)[4]) {
 #pragma unroll
   for (int j = 0; j < 4; ++j) xv[j] = 0.0;
   asm("{\n\t.reg .pred q<4>;\n\t.reg .u64 a<4>;\n\t"
@@ -250,8 +254,8 @@ __device__ __forceinline__ void gather_batch<4, double>(const double *x, const u
       : "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "l"(x), "r"(cnt));
 }
 template <>
-__device__ __forceinline__ void gather_batch<4, float>(const float *x, const uint32_t (&c)[4], uint32_t cnt,
-                                             float (&xv)[4]) {
+__device__ __forceinline__ void gather_batch<4, float>(
+    const float *x, const uint32_t (&c)[4], uint32_t cnt, float (&xv)[4]) {
 #pragma unroll
   for (int j = 0; j < 4; ++j) xv[j] = 0.0f;
   asm("{\n\t.reg .pred q<4>;\n\t.reg .u64 a<4>;\n\t"
