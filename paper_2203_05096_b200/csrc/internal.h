@@ -19,21 +19,41 @@ void set_error(const char *fmt, ...);
 
 // A tile plan of the streaming kernel: tile t covers rows
 // [tile_row[t], tile_row[t+1]) made of whole groups.
-constexpr int64_t kDefaultTileCost = 2048;  // nonzeros + rows per tile
+constexpr int64_t kDefaultTileCost = 2048;  // nonzeros + rows per tile (round-1 plan)
+constexpr int64_t kDeepRingTileCost = 1536; // tile of the 3-stage ring (regular rows)
 constexpr int64_t kDefaultStages = 2;       // TMA ring depth per CTA (plan sweep)
 constexpr int64_t kDefaultCtasPerSm = 3;    // resident streaming CTAs per SM
 constexpr int kGatherAuto = 2;
 constexpr int64_t kLongRow = 128;  // rows longer than this are summed a warp each
 
-// Auto schedule (round-1 plan sweeps, profiles/r01_sched_sweep.txt):
-//  * regular rows: 3 CTAs per SM in f64, 4 in f32 (half the bytes per
-//    nonzero, so more tiles in flight: C2 f32 +9 %);
-//  * irregular rows (variance > 10, the paper's class boundary) are bound by
-//    random x gathers: 2 CTAs per SM, leaving ~120 KB of L1 (C5 +47 %);
+// Auto schedule (round-2 plan re-sweep on the final kernel,
+// profiles/r02l_*, r02m_plan_confirm.jsonl, r02n_*; round 1:
+// r01_sched_sweep.txt):
+//  * regular rows (variance <= 10, the paper's class boundary) without long
+//    rows: tiles of 1536 cost units and a 3-stage ring -- three stages still
+//    fit three f64 CTAs (196 KB) and the deeper ring hides the TMA round
+//    trip (interleaved in one process: C3 f64 0.390 -> 0.359 ms, C3 f32
+//    0.271 -> 0.246 at 4 CTAs, C2 f64 0.264 -> 0.258);
+//  * irregular rows or rows longer than kLongRow: tiles of 2048, 2 stages
+//    and 2 CTAs per SM (~120 KB of L1 for the random x gathers; the deeper
+//    plan lost 28 % on the power-law probe, where the long-row kernel also
+//    needs room beside the streaming kernel);
+//  * 3 CTAs per SM in f64 and 4 in f32 for regular rows (half the bytes per
+//    nonzero, so more tiles in flight);
 //  * the serial order over rows longer than 16 nonzeros gathers first
 //    (C3 +13 %); short rows keep the inline gathers (C2 -15 % otherwise).
 inline int auto_ctas(double row_var, int value_bytes) {
   return row_var > 10.0 ? 2 : (value_bytes == 4 ? 4 : 3);
+}
+#ifndef CSRK_OLD_AUTO
+// regular rows without long rows: 3-stage ring at tile 1536; otherwise the
+// round-1 plan (2 stages, tile 2048: auto_tile_cost below)
+inline bool deep_ring(double row_var, int64_t n_long) { return row_var <= 10.0 && n_long == 0; }
+#else
+inline bool deep_ring(double, int64_t) { return false; }
+#endif
+inline int64_t auto_stages(double row_var, int64_t n_long) {
+  return deep_ring(row_var, n_long) ? 3 : 2;
 }
 // Gather first in the serial order when rows are long (C3: 27-nonzero rows)
 // or their lengths spread wider than their mean (a thread per row then waits
@@ -59,19 +79,20 @@ inline bool auto_gather(int variant, int nx, double mean_row, double row_var) {
 // 74 rows = 1.2 passes of 64 -> 1684-cost tiles of ~61 rows, 5.1 -> 5.6 TB/s
 // (profiles/r01_sched_sweep.txt).  The serial order keeps 2048: short rows
 // fill 256 rows per tile, long rows gather first.
-inline int64_t auto_tile_cost(double mean_row, int variant, int nx) {
-  if (variant != CSRK_STRIDED) return kDefaultTileCost;
+inline int64_t auto_tile_cost(double mean_row, int variant, int nx,
+                              int64_t base = kDefaultTileCost) {
+  if (variant != CSRK_STRIDED) return base;
   int p = 1;
   while (p < nx) p <<= 1;
   const double per_row = mean_row + 1.0;
   const double slots = 256.0 / p;
-  const double rows = static_cast<double>(kDefaultTileCost) / per_row;
+  const double rows = static_cast<double>(base) / per_row;
   const double passes = rows / slots > 1.0 ? static_cast<double>(static_cast<int64_t>(rows / slots + 0.999999)) : 1.0;
-  if (rows / (passes * slots) >= 0.85) return kDefaultTileCost;
+  if (rows / (passes * slots) >= 0.85) return base;
   double full = static_cast<double>(static_cast<int64_t>(rows / slots));
   if (full < 1.0) full = 1.0;
   int64_t tc = static_cast<int64_t>(full * slots * per_row * 0.95);
-  if (tc > kDefaultTileCost) tc = kDefaultTileCost;
+  if (tc > base) tc = base;
   if (tc < 512) tc = 512;
   return tc;
 }

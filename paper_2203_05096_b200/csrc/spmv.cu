@@ -1684,10 +1684,13 @@ int prepare_plan(const csrk_matrix *cm, int value_type, int variant, int nx) {
   if (m->n_rows == 0) return CSRK_OK;
   if (!m->plan.row_stats) CSRK_TRY(ensure_plan(m, 0, 0, 0, m->stream));
   if (!m->plan.auto_tile) return CSRK_OK;
-  const int64_t tc = auto_tile_cost(m->plan.mean_short, variant, nx);
-  if (tc != m->plan.tile_cost) {
+  const bool deep = deep_ring(m->plan.row_var, m->plan.n_long);
+  const int64_t tc = auto_tile_cost(m->plan.mean_short, variant, nx,
+                                    deep ? kDeepRingTileCost : kDefaultTileCost);
+  const int64_t st = auto_stages(m->plan.row_var, m->plan.n_long);
+  if (tc != m->plan.tile_cost || st != m->plan.stages) {
     const bool keep = m->plan.auto_tile;
-    CSRK_TRY(ensure_plan(m, tc, 0, m->plan.stages, m->stream));
+    CSRK_TRY(ensure_plan(m, tc, 0, st, m->stream));
     m->plan.auto_tile = keep;
     CSRK_CUDA_TRY(cudaStreamSynchronize(m->stream));
   }
