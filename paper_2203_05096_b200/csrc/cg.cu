@@ -13,6 +13,7 @@
 // run.  Vectors are float64 or float32 (reductions always in float64).
 
 #include <cstdint>
+#include <type_traits>
 
 #include "internal.h"
 
@@ -53,21 +54,135 @@ __device__ __forceinline__ double fold_partials(const double *partials) {
   return s;
 }
 
-template <typename T>
+// fp32 vectors (round 2): 16-byte accesses and fp32 arithmetic.  The scalar
+// kernels converted every element to fp64 (F2F.F64.F32 on both sides of a
+// DFMA) and loaded 4 bytes per thread, which left the f32 CG loop short of
+// the HBM roofline; here x, r, p update with fp32 FMAs (alpha / beta rounded
+// to fp32 once) and each thread's 4-element batch of a reduction is summed in
+// fp32 before it is folded into the fp64 accumulator (one conversion per 4
+// elements; the batch error is at most 4 unit roundoffs of its sum of
+// magnitudes).  fp64 vectors keep the scalar kernels bit for bit.
+#ifndef CSRK_CG_VEC
+#define CSRK_CG_VEC 1
+#endif
+
+__device__ __forceinline__ float sq4(float4 v) {
+  return fmaf(v.w, v.w, fmaf(v.z, v.z, fmaf(v.y, v.y, v.x * v.x)));
+}
+__device__ __forceinline__ float dot4(float4 a, float4 b) {
+  return fmaf(a.w, b.w, fmaf(a.z, b.z, fmaf(a.y, b.y, a.x * b.x)));
+}
+__device__ __forceinline__ float4 axpy4(float a, float4 x, float4 y) {  // a x + y
+  return make_float4(fmaf(a, x.x, y.x), fmaf(a, x.y, y.y), fmaf(a, x.z, y.z),
+                     fmaf(a, x.w, y.w));
+}
+
+// vector part [0, n4) as float4, the last n % 4 elements by the first threads
+struct VecSpan {
+  int64_t n4, tid, stride;
+  __device__ VecSpan(int64_t n)
+      : n4(n >> 2), tid(blockIdx.x * int64_t(blockDim.x) + threadIdx.x),
+        stride(int64_t(gridDim.x) * blockDim.x) {}
+};
+
+inline bool vec16(const void *a, const void *b = nullptr, const void *c = nullptr,
+                  const void *d = nullptr) {
+  const uintptr_t m = reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b) |
+                      reinterpret_cast<uintptr_t>(c) | reinterpret_cast<uintptr_t>(d);
+  return CSRK_CG_VEC && (m & 15u) == 0;
+}
+
+// fp64 partial of a . b over this thread's elements (VEC: fp32 float4 batches)
+template <typename T, bool VEC>
+__device__ __forceinline__ double dot_thread(const T *__restrict__ a, const T *__restrict__ b,
+                                             int64_t n) {
+  double s = 0.0;
+  if constexpr (VEC) {
+    const VecSpan v(n);
+    const float4 *a4 = reinterpret_cast<const float4 *>(a);
+    const float4 *b4 = reinterpret_cast<const float4 *>(b);
+    for (int64_t i = v.tid; i < v.n4; i += v.stride)
+      s += static_cast<double>(dot4(a4[i], b4[i]));
+    for (int64_t i = (v.n4 << 2) + v.tid; i < n; i += v.stride)
+      s += static_cast<double>(a[i]) * static_cast<double>(b[i]);
+  } else {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x)
+      s += static_cast<double>(a[i]) * static_cast<double>(b[i]);
+  }
+  return s;
+}
+
+// x += alpha p; r -= alpha Ap; returns this thread's fp64 partial of r.r
+template <typename T, bool VEC>
+__device__ __forceinline__ double update_thread(T *__restrict__ x, T *__restrict__ r,
+                                                const T *__restrict__ p,
+                                                const T *__restrict__ ap, int64_t n,
+                                                double alpha) {
+  double s = 0.0;
+  if constexpr (VEC) {
+    const float af = static_cast<float>(alpha);
+    const VecSpan v(n);
+    float4 *x4 = reinterpret_cast<float4 *>(x);
+    float4 *r4 = reinterpret_cast<float4 *>(r);
+    const float4 *p4 = reinterpret_cast<const float4 *>(p);
+    const float4 *a4 = reinterpret_cast<const float4 *>(ap);
+    for (int64_t i = v.tid; i < v.n4; i += v.stride) {
+      const float4 pv = p4[i], av = a4[i], xv = x4[i], rv = r4[i];
+      x4[i] = axpy4(af, pv, xv);
+      const float4 rn = axpy4(-af, av, rv);
+      r4[i] = rn;
+      s += static_cast<double>(sq4(rn));
+    }
+    for (int64_t i = (v.n4 << 2) + v.tid; i < n; i += v.stride) {
+      x[i] = fmaf(af, p[i], x[i]);
+      const float ri = fmaf(-af, ap[i], r[i]);
+      r[i] = ri;
+      s += static_cast<double>(ri) * static_cast<double>(ri);
+    }
+  } else {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x) {
+      x[i] = static_cast<T>(static_cast<double>(x[i]) + alpha * static_cast<double>(p[i]));
+      const double ri = static_cast<double>(r[i]) - alpha * static_cast<double>(ap[i]);
+      r[i] = static_cast<T>(ri);
+      const double rv = static_cast<double>(static_cast<T>(ri));
+      s += rv * rv;
+    }
+  }
+  return s;
+}
+
+// p = r + beta p
+template <typename T, bool VEC>
+__device__ __forceinline__ void direction_thread(T *__restrict__ p, const T *__restrict__ r,
+                                                 int64_t n, double beta) {
+  if constexpr (VEC) {
+    const float bf = static_cast<float>(beta);
+    const VecSpan v(n);
+    float4 *p4 = reinterpret_cast<float4 *>(p);
+    const float4 *r4 = reinterpret_cast<const float4 *>(r);
+    for (int64_t i = v.tid; i < v.n4; i += v.stride) p4[i] = axpy4(bf, p4[i], r4[i]);
+    for (int64_t i = (v.n4 << 2) + v.tid; i < n; i += v.stride) p[i] = fmaf(bf, p[i], r[i]);
+  } else {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x)
+      p[i] = static_cast<T>(static_cast<double>(r[i]) + beta * static_cast<double>(p[i]));
+  }
+}
+
+template <typename T, bool VEC>
 __global__ void __launch_bounds__(kRedThreads)
     dot_partial_kernel(const T *__restrict__ a, const T *__restrict__ b, int64_t n,
                        double *__restrict__ partials) {
   __shared__ double red[32];
-  double s = 0.0;
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
-       i += int64_t(gridDim.x) * blockDim.x)
-    s += static_cast<double>(a[i]) * static_cast<double>(b[i]);
+  const double s = dot_thread<T, VEC>(a, b, n);
   const double t = block_sum<T>(s, red);
   if (threadIdx.x == 0) partials[blockIdx.x] = t;
 }
 
 // alpha = rr / pAp; x += alpha p; r -= alpha Ap; partial r.r
-template <typename T>
+template <typename T, bool VEC>
 __global__ void __launch_bounds__(kRedThreads)
     cg_update_kernel(T *__restrict__ x, T *__restrict__ r, const T *__restrict__ p,
                      const T *__restrict__ ap, int64_t n, const double *__restrict__ pap_part,
@@ -86,22 +201,13 @@ __global__ void __launch_bounds__(kRedThreads)
     }
   }
   __syncthreads();
-  const double alpha = s_alpha;
-  double s = 0.0;
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
-       i += int64_t(gridDim.x) * blockDim.x) {
-    x[i] = static_cast<T>(static_cast<double>(x[i]) + alpha * static_cast<double>(p[i]));
-    const double ri = static_cast<double>(r[i]) - alpha * static_cast<double>(ap[i]);
-    r[i] = static_cast<T>(ri);
-    const double rv = static_cast<double>(static_cast<T>(ri));
-    s += rv * rv;
-  }
+  const double s = update_thread<T, VEC>(x, r, p, ap, n, s_alpha);
   const double t = block_sum<T>(s, red);
   if (threadIdx.x == 0) rr_part[blockIdx.x] = t;
 }
 
 // beta = rr' / rr; p = r + beta p; rr = rr' (block 0 publishes)
-template <typename T>
+template <typename T, bool VEC>
 __global__ void __launch_bounds__(kRedThreads)
     cg_direction_kernel(T *__restrict__ p, const T *__restrict__ r, int64_t n,
                         const double *__restrict__ rr_part, CgScalars *__restrict__ sc) {
@@ -114,15 +220,12 @@ __global__ void __launch_bounds__(kRedThreads)
     }
   }
   __syncthreads();
-  const double beta = s_beta;
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
-       i += int64_t(gridDim.x) * blockDim.x)
-    p[i] = static_cast<T>(static_cast<double>(r[i]) + beta * static_cast<double>(p[i]));
+  direction_thread<T, VEC>(p, r, n, s_beta);
   // every block read sc->rr above; a grid-wide order is needed before the
   // write, so the publish happens in the next kernel (set_rr_kernel)
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     sc->rr_new = s_rr;
-    sc->beta = beta;
+    sc->beta = s_beta;
   }
 }
 
@@ -230,21 +333,18 @@ __device__ __forceinline__ void last_block_fold(const double *partials, unsigned
   }
 }
 
-template <typename T>
+template <typename T, bool VEC>
 __global__ void __launch_bounds__(kRedThreads)
     dist_dot_kernel(const T *__restrict__ a, const T *__restrict__ b, int64_t n,
                     double *__restrict__ partials, unsigned *counter, double *out) {
   __shared__ double red[32];
-  double s = 0.0;
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
-       i += int64_t(gridDim.x) * blockDim.x)
-    s += static_cast<double>(a[i]) * static_cast<double>(b[i]);
+  const double s = dot_thread<T, VEC>(a, b, n);
   const double t = block_sum<T>(s, red);
   if (threadIdx.x == 0) partials[blockIdx.x] = t;
   last_block_fold(partials, counter, out);
 }
 
-template <typename T>
+template <typename T, bool VEC>
 __global__ void __launch_bounds__(kRedThreads)
     dist_update_kernel(T *__restrict__ x, T *__restrict__ r, const T *__restrict__ p,
                        const T *__restrict__ ap, int64_t n, double *__restrict__ sc,
@@ -252,15 +352,7 @@ __global__ void __launch_bounds__(kRedThreads)
   __shared__ double red[32];
   const double pap = sc[kScPAP];
   const double alpha = pap != 0.0 ? sc[kScRR] / pap : 0.0;
-  double s = 0.0;
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
-       i += int64_t(gridDim.x) * blockDim.x) {
-    x[i] = static_cast<T>(static_cast<double>(x[i]) + alpha * static_cast<double>(p[i]));
-    const double ri = static_cast<double>(r[i]) - alpha * static_cast<double>(ap[i]);
-    r[i] = static_cast<T>(ri);
-    const double rv = static_cast<double>(static_cast<T>(ri));
-    s += rv * rv;
-  }
+  const double s = update_thread<T, VEC>(x, r, p, ap, n, alpha);
   const double t = block_sum<T>(s, red);
   if (threadIdx.x == 0) partials[blockIdx.x] = t;
   if (blockIdx.x == 0 && threadIdx.x == 0) sc[kScAlpha] = alpha;
@@ -268,15 +360,13 @@ __global__ void __launch_bounds__(kRedThreads)
 }
 
 // p = r + beta p with beta = rr' / rr; the last block publishes rr = rr'
-template <typename T>
+template <typename T, bool VEC>
 __global__ void __launch_bounds__(kRedThreads)
     dist_direction_kernel(T *__restrict__ p, const T *__restrict__ r, int64_t n,
                           double *__restrict__ sc, unsigned *counter) {
   const double rr = sc[kScRR], rr_new = sc[kScRRNew];
   const double beta = rr != 0.0 ? rr_new / rr : 0.0;
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
-       i += int64_t(gridDim.x) * blockDim.x)
-    p[i] = static_cast<T>(static_cast<double>(r[i]) + beta * static_cast<double>(p[i]));
+  direction_thread<T, VEC>(p, r, n, beta);
   __shared__ bool s_last;
   __syncthreads();
   if (threadIdx.x == 0) s_last = atomicAdd(counter, 1u) == gridDim.x - 1;
@@ -310,6 +400,8 @@ int cg_run(const csrk_matrix *m, int value_type, int variant, int nx, const T *b
   CSRK_CUDA_TRY(cudaMemsetAsync(w.pap_part, 0, kRedBlocks * sizeof(double), s));
   CSRK_CUDA_TRY(cudaMemsetAsync(w.rr_part, 0, kRedBlocks * sizeof(double), s));
   CSRK_CUDA_TRY(cudaMemsetAsync(w.sc, 0, sizeof(CgScalars), s));
+  // fp32 vectors aligned to 16 bytes take the float4 / fp32-arithmetic kernels
+  const bool vec = std::is_same<T, float>::value && vec16(x, r, p, ap);
   int rc = launch_spmv(m, value_type, variant, nx, x, ap, s);  // ap = A x0
   if (rc == CSRK_OK) {
     cg_init_kernel<T><<<kRedBlocks, kRedThreads, 0, s>>>(b, ap, r, p, n, w.rr_part);
@@ -324,13 +416,24 @@ int cg_run(const csrk_matrix *m, int value_type, int variant, int nx, const T *b
                          &fused);
     if (rc == CSRK_OK && !fused) {
       rc = launch_spmv(m, value_type, variant, nx, p, ap, s);
-      if (rc == CSRK_OK)
-        dot_partial_kernel<T><<<kRedBlocks, kRedThreads, 0, s>>>(p, ap, n, w.pap_part);
+      if (rc == CSRK_OK) {
+        if (vec)
+          dot_partial_kernel<T, true><<<kRedBlocks, kRedThreads, 0, s>>>(p, ap, n, w.pap_part);
+        else
+          dot_partial_kernel<T, false><<<kRedBlocks, kRedThreads, 0, s>>>(p, ap, n, w.pap_part);
+      }
     }
     if (rc != CSRK_OK) break;
-    cg_update_kernel<T><<<kRedBlocks, kRedThreads, 0, s>>>(x, r, p, ap, n, w.pap_part,
-                                                          w.sc, w.rr_part);
-    cg_direction_kernel<T><<<kRedBlocks, kRedThreads, 0, s>>>(p, r, n, w.rr_part, w.sc);
+    if (vec) {
+      cg_update_kernel<T, true><<<kRedBlocks, kRedThreads, 0, s>>>(x, r, p, ap, n, w.pap_part,
+                                                                  w.sc, w.rr_part);
+      cg_direction_kernel<T, true><<<kRedBlocks, kRedThreads, 0, s>>>(p, r, n, w.rr_part, w.sc);
+    } else {
+      cg_update_kernel<T, false><<<kRedBlocks, kRedThreads, 0, s>>>(x, r, p, ap, n, w.pap_part,
+                                                                   w.sc, w.rr_part);
+      cg_direction_kernel<T, false><<<kRedBlocks, kRedThreads, 0, s>>>(p, r, n, w.rr_part,
+                                                                      w.sc);
+    }
     set_rr_kernel<<<1, 1, 0, s>>>(w.sc);
   }
   cudaError_t e = cudaGetLastError();
@@ -450,12 +553,16 @@ int csrk_vec_dot(int value_type, int64_t n, const void *a, const void *b, double
   }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const unsigned g = red_grid(n);
-  if (value_type == CSRK_F32)
-    dist_dot_kernel<float><<<g, kRedThreads, 0, s>>>(static_cast<const float *>(a),
-                                                     static_cast<const float *>(b), n,
-                                                     partials, counter, out);
+  if (value_type == CSRK_F32 && vec16(a, b))
+    dist_dot_kernel<float, true><<<g, kRedThreads, 0, s>>>(static_cast<const float *>(a),
+                                                           static_cast<const float *>(b), n,
+                                                           partials, counter, out);
+  else if (value_type == CSRK_F32)
+    dist_dot_kernel<float, false><<<g, kRedThreads, 0, s>>>(static_cast<const float *>(a),
+                                                            static_cast<const float *>(b), n,
+                                                            partials, counter, out);
   else
-    dist_dot_kernel<double><<<g, kRedThreads, 0, s>>>(static_cast<const double *>(a),
+    dist_dot_kernel<double, false><<<g, kRedThreads, 0, s>>>(static_cast<const double *>(a),
                                                       static_cast<const double *>(b), n,
                                                       partials, counter, out);
   CSRK_CUDA_TRY(cudaGetLastError());
@@ -470,12 +577,16 @@ int csrk_cg_update(int value_type, int64_t n, void *x, void *r, const void *p, c
   }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const unsigned g = red_grid(n);
-  if (value_type == CSRK_F32)
-    dist_update_kernel<float><<<g, kRedThreads, 0, s>>>(
+  if (value_type == CSRK_F32 && vec16(x, r, p, ap))
+    dist_update_kernel<float, true><<<g, kRedThreads, 0, s>>>(
+        static_cast<float *>(x), static_cast<float *>(r), static_cast<const float *>(p),
+        static_cast<const float *>(ap), n, scalars, partials, counter);
+  else if (value_type == CSRK_F32)
+    dist_update_kernel<float, false><<<g, kRedThreads, 0, s>>>(
         static_cast<float *>(x), static_cast<float *>(r), static_cast<const float *>(p),
         static_cast<const float *>(ap), n, scalars, partials, counter);
   else
-    dist_update_kernel<double><<<g, kRedThreads, 0, s>>>(
+    dist_update_kernel<double, false><<<g, kRedThreads, 0, s>>>(
         static_cast<double *>(x), static_cast<double *>(r), static_cast<const double *>(p),
         static_cast<const double *>(ap), n, scalars, partials, counter);
   CSRK_CUDA_TRY(cudaGetLastError());
@@ -490,11 +601,14 @@ int csrk_cg_direction(int value_type, int64_t n, void *p, const void *r, double 
   }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const unsigned g = red_grid(n);
-  if (value_type == CSRK_F32)
-    dist_direction_kernel<float><<<g, kRedThreads, 0, s>>>(
+  if (value_type == CSRK_F32 && vec16(p, r))
+    dist_direction_kernel<float, true><<<g, kRedThreads, 0, s>>>(
+        static_cast<float *>(p), static_cast<const float *>(r), n, scalars, counter);
+  else if (value_type == CSRK_F32)
+    dist_direction_kernel<float, false><<<g, kRedThreads, 0, s>>>(
         static_cast<float *>(p), static_cast<const float *>(r), n, scalars, counter);
   else
-    dist_direction_kernel<double><<<g, kRedThreads, 0, s>>>(
+    dist_direction_kernel<double, false><<<g, kRedThreads, 0, s>>>(
         static_cast<double *>(p), static_cast<const double *>(r), n, scalars, counter);
   CSRK_CUDA_TRY(cudaGetLastError());
   return CSRK_OK;
