@@ -645,6 +645,39 @@ __device__ void compute_direct(uint32_t r0, uint32_t r1,
   }
 }
 
+// Per-CTA event timeline of the streaming kernel (diagnostic build only:
+// tools/build_variant.sh tl -DCSRK_TIMELINE=1, read by tools/timeline_probe.py
+// through csrk_debug_timeline).  Slot 0: %globaltimer at entry (aligns the
+// SMs); slots 1-5: SM clock cycles after entry at the producer's first TMA
+// issue, the consumers' first full stage, their last stage released, the
+// producer's exit, and the CTA's tile count.
+#ifndef CSRK_TIMELINE
+#define CSRK_TIMELINE 0
+#endif
+#if CSRK_TIMELINE
+constexpr int kTlSlots = 6, kTlCtas = 4096;
+__device__ unsigned long long g_timeline[kTlCtas * kTlSlots];
+__device__ __forceinline__ unsigned long long tl_gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define TL_ENTRY()                                                             \
+  const long long tl_c0 = clock64();                                           \
+  if (threadIdx.x == 0 && blockIdx.x < kTlCtas)                                \
+    g_timeline[blockIdx.x * kTlSlots] = tl_gtimer()
+#define TL_MARK(slot)                                                          \
+  if (blockIdx.x < kTlCtas)                                                    \
+  g_timeline[blockIdx.x * kTlSlots + (slot)] =                                 \
+      static_cast<unsigned long long>(clock64() - tl_c0)
+#define TL_SET(slot, v) \
+  if (blockIdx.x < kTlCtas) g_timeline[blockIdx.x * kTlSlots + (slot)] = (v)
+#else
+#define TL_ENTRY()
+#define TL_MARK(slot)
+#define TL_SET(slot, v)
+#endif
+
 template <typename V, int NX, bool GF, int LB = 4, bool DOT = false>
 __global__ void __launch_bounds__(kThreads, 2)
     csrk_stream_kernel(const uint32_t *__restrict__ row_ptr,
@@ -664,6 +697,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   unsigned char *stage0 = smem + geo.header_bytes;
 
   const int tid = threadIdx.x;
+  TL_ENTRY();
   if (tid == 0) {
     for (uint32_t s = 0; s < stages; ++s) {
       mbar_init(&full[s], 1);
@@ -769,17 +803,31 @@ __global__ void __launch_bounds__(kThreads, 2)
         md.mode = kDirect;
         mbar_arrive(&full[s]);
       }
+      if (i == 0) TL_MARK(1);
     }
+    TL_MARK(4);
+    TL_SET(5, i);
+    // every TMA of this CTA is issued: the next kernel on the stream (a
+    // repeated SpMV) may start its own prologue and matrix stream on the SMs
+    // this grid frees (programmatic dependent launch, launch_stream)
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     return;
   }
 
   // ---------------- consumer warps ----------------
+  // Under programmatic dependent launch the producer streams the matrix
+  // (read-only for the handle's lifetime) while the previous kernel on the
+  // stream is still running; x is read and y written only after that kernel
+  // has completed and its writes are visible.  A no-op without the launch
+  // attribute.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int ct = tid - 32;
   double dot = 0.0;  // DOT: this thread's x . y partial over its rows
   uint32_t s = 0, ph = 0;
   for (uint32_t t = blockIdx.x; t < n_tiles;
        t += grid, s = (s + 1 == stages) ? 0 : s + 1, ph ^= (s == 0)) {
     mbar_wait(&full[s], ph);
+    if (CSRK_TIMELINE && ct == 0 && t == blockIdx.x) TL_MARK(2);
     const StageMeta md = meta[s];
     if (md.mode == kStaged) {
       const unsigned char *st = stage0 + s * geo.stage_bytes;
@@ -809,6 +857,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     __syncwarp();
     if ((ct & 31) == 0) mbar_arrive(&empty[s]);
   }
+  if (CSRK_TIMELINE && ct == 0) TL_MARK(3);
   if constexpr (DOT) {
     // the CTA's partial in a fixed order: warp trees, then warps 0..7
     __shared__ double red[kConsumerWarps];
@@ -1225,12 +1274,32 @@ int launch_stream(const csrk_matrix *m, const V *vals, const V *x, V *y,
     c = (c + 4095) / 4096 * 4096;
     pf_chunk = static_cast<uint32_t>(c);
   }
-  kern<<<static_cast<unsigned>(grid), kThreads, smem, stream>>>(
-      m->row_ptr, m->col_idx, vals, x, y, pl.tile_row + t0, pl.tile_ptr + t0,
+  // Programmatic dependent launch (CSRK_PDL=0 disables): back-to-back
+  // SpMVs overlap the next launch's prologue and first TMA fills with the
+  // previous grid's last tiles (the kernel's griddepcontrol.wait orders
+  // every x read and y write after the previous kernel).  Only the matrix
+  // and plan arrays are read early; they are written before the handle's
+  // first launch and synchronised (upload, ensure_plan, prepare_plan).
+  static const bool pdl = [] {
+    const char *e = std::getenv("CSRK_PDL");
+    return !(e && e[0] == '0');
+  }();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(grid));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  CSRK_CUDA_TRY(cudaLaunchKernelEx(
+      &cfg, kern, m->row_ptr, m->col_idx, vals, x, y, pl.tile_row + t0, pl.tile_ptr + t0,
       static_cast<uint32_t>(count), geo.cap, geo.rcap, geo.stages,
       m->plan.n_long > 0 ? static_cast<uint32_t>(kLongRow) : 0xffffffffu,
-      m->plan.n_long > 0 ? pl.tile_long + t0 : nullptr,
-      long_holes(pl), x_bytes, pf_chunk, dot_part);
+      m->plan.n_long > 0 ? static_cast<const uint32_t *>(pl.tile_long + t0) : nullptr,
+      long_holes(pl), x_bytes, pf_chunk, dot_part));
   CSRK_CUDA_TRY(cudaGetLastError());
   return CSRK_OK;
 }
@@ -1778,3 +1847,15 @@ int launch_spmv(const csrk_matrix *m, int value_type, int variant, int nx,
 }
 
 }  // namespace csrk
+
+#if CSRK_TIMELINE
+extern "C" int csrk_debug_timeline(unsigned long long *out, int n_ctas) {
+  if (!out || n_ctas < 0) return CSRK_EINVAL;
+  if (n_ctas > csrk::kTlCtas) n_ctas = csrk::kTlCtas;
+  return cudaMemcpyFromSymbol(out, csrk::g_timeline,
+                              sizeof(unsigned long long) * csrk::kTlSlots * n_ctas) ==
+                 cudaSuccess
+             ? CSRK_OK
+             : CSRK_ECUDA;
+}
+#endif
