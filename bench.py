@@ -255,24 +255,66 @@ def run_ours(args, log):
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     algo_bytes = spmv_bytes(n, n, nnz, vbytes)
-    # inputs smaller than 4x the 126 MB L2 (C1: 80 MB) would be served from
-    # L2 by back-to-back launches: flush it with a 512 MB write before every
-    # step and time each step alone with its own events
+    # Inputs smaller than 4x the 126 MB L2 (C1: 80 MB) would be served from
+    # L2 by back-to-back launches on one copy.  The timed steps rotate
+    # instead through R resident replicas of the matrix, x and y (R x the
+    # algorithmic bytes >= 4 x L2: each step reads its replica cold from
+    # HBM -- "inputs larger than L2"), back to back like the larger configs.
+    # The single launch after a 512 MB L2 flush (write, then a read-only pass
+    # so the L2 holds no dirty lines), each with its own events, is reported
+    # beside it: that one also carries the launch and the cold prologue.
     flush = algo_bytes < 4 * 126e6
-    scrub = torch.empty(64 << 20, dtype=torch.float64, device="cuda") if flush else None
+    reps = None
+    if flush:
+        from paper_2203_05096_b200 import _native as nat
+
+        # x is prefetched into L2 with evict_last and y is written through
+        # L2, so the replicas' x + y (not only the whole working set) must
+        # exceed 4 x L2 for every step to read its x from HBM
+        xy_bytes = 2 * n * vbytes
+        n_rep = min(64, max(-(-int(4 * 126e6) // algo_bytes), -(-int(4 * 126e6) // xy_bytes)))
+        b = m.base
+        dev0 = m.device()
+        reps = [(dev0, xd, yd)]
+        for _ in range(n_rep - 1):
+            d = nat.DeviceMatrix.upload(b.row_ptr, b.col_idx, b.vals, n, n, k=m.k,
+                                        sr_ptr=m.group_ptrs[0],
+                                        ssr_ptr=m.group_ptrs[1] if m.k == 3 else None)
+            reps.append((d, xd.clone(), torch.empty_like(yd)))
+        for d, xr, yr in reps:
+            ck.spmv_device(d, xr, yr, dims=dims, variant=variant, stream=stream)
+        plan_keys = ("tile_cost", "stages", "n_tiles", "gather_first", "ctas_per_sm")
+        p0 = {k: dev0.plan()[k] for k in plan_keys}
+        assert all({k: d.plan()[k] for k in plan_keys} == p0 for d, _, _ in reps), \
+            "replica plans differ"
+        scrub = torch.empty(64 << 20, dtype=torch.float64, device="cuda")
+        scrub2 = torch.ones(64 << 20, dtype=torch.float64, device="cuda")
+        sink = torch.empty((), dtype=torch.float64, device="cuda")
     with ClockSampler(torch.cuda.current_device()) as clk:
         clk.load_until(step, torch.cuda.synchronize)
         torch.cuda.synchronize()
         if flush:
+            ev0.record(stream)
+            # replica 0 is the one the clock sampler's warm load just ran:
+            # the rotation starts at replica 1
+            for i in range(args.steps):
+                d, xr, yr = reps[(i + 1) % len(reps)]
+                ck.spmv_device(d, xr, yr, dims=dims, variant=variant, stream=stream)
+            ev1.record(stream)
+            torch.cuda.synchronize()
+            ms = ev0.elapsed_time(ev1) / args.steps
             evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                    for _ in range(args.steps)]
             for a_ev, b_ev in evs:
                 scrub.fill_(1.0)
+                sink.copy_(scrub2.sum())
                 a_ev.record(stream)
                 step()
                 b_ev.record(stream)
             torch.cuda.synchronize()
-            ms = sum(a_ev.elapsed_time(b_ev) for a_ev, b_ev in evs) / args.steps
+            ms_flushed = sum(a_ev.elapsed_time(b_ev) for a_ev, b_ev in evs) / args.steps
+            for _, _, yr in reps[1:]:
+                assert torch.equal(yr, yd), "replica outputs differ"
         else:
             ev0.record(stream)
             for _ in range(args.steps):
@@ -343,9 +385,19 @@ def run_ours(args, log):
                    "parallelism": "1 GPU",
                    "l2": ("inputs larger than L2 (algorithmic %.2f GB per step vs 126 MB "
                           "L2); no flush" % (algo_bytes / 1e9)) if not flush else
-                         ("L2 flushed before every step (512 MB write, outside the per-step "
-                          "events); algorithmic %.0f MB per step" % (algo_bytes / 1e6))},
+                         ("inputs larger than L2: the steps rotate through %d resident "
+                          "replicas of the matrix, x and y (%.0f MB per step, %.0f MB in "
+                          "all, x + y alone %.0f MB), back to back" % (
+                              len(reps), algo_bytes / 1e6, len(reps) * algo_bytes / 1e6,
+                              len(reps) * 2 * n * vbytes / 1e6))},
         "hbm_gbs": round(gbs, 1),
+        **({"single_launch_l2_flushed": {
+            "ms": round(ms_flushed, 4),
+            "gflops": round(2.0 * nnz / (ms_flushed * 1e-3) / 1e9, 2),
+            "frac": round(algo_bytes / (ms_flushed * 1e-3) / 1e9 / measured_peak()[0], 4),
+            "how": "each step alone between its own events after a 512 MB write + "
+                   "512 MB read L2 flush (includes the launch and the cold prologue)"}}
+           if flush else {}),
         "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": peak,
                      "unit": "GB/s", "frac": round(gbs / peak, 4),
                      "peak_source": peak_src,
