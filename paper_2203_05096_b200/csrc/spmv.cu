@@ -678,6 +678,28 @@ __device__ __forceinline__ unsigned long long tl_gtimer() {
 #define TL_SET(slot, v)
 #endif
 
+// The tiles a CTA of the persistent grid takes: [first, end) in steps of
+// `step`.  Round-robin (tile b, b + grid, ...) by default; CSRK_CONTIG_TILES=1
+// gives each CTA one contiguous run of tiles instead (successive tiles of
+// a CTA then gather from nearly the same window of x: the A/B of
+// DESIGN.md §4 "tile order").
+#ifndef CSRK_CONTIG_TILES
+#define CSRK_CONTIG_TILES 0
+#endif
+struct TileRun {
+  uint32_t first, end, step;
+};
+__device__ __forceinline__ TileRun tile_run(uint32_t n_tiles) {
+#if CSRK_CONTIG_TILES
+  const uint32_t g = gridDim.x, b = blockIdx.x;
+  const uint32_t q = n_tiles / g, r = n_tiles % g;
+  const uint32_t first = b * q + (b < r ? b : r);
+  return {first, first + q + (b < r ? 1u : 0u), 1u};
+#else
+  return {blockIdx.x, n_tiles, gridDim.x};
+#endif
+}
+
 template <typename V, int NX, bool GF, int LB = 4, bool DOT = false>
 __global__ void __launch_bounds__(kThreads, 2)
     csrk_stream_kernel(const uint32_t *__restrict__ row_ptr,
@@ -707,7 +729,6 @@ __global__ void __launch_bounds__(kThreads, 2)
   }
   __syncthreads();
 
-  const uint32_t grid = gridDim.x;
   if (tid < 32) {
     // ---------------- producer warp ----------------
     if (tid != 0) return;
@@ -729,31 +750,33 @@ __global__ void __launch_bounds__(kThreads, 2)
     // the next tile's bounds (rows and their nonzero offsets, precomputed in
     // the plan) load while this tile waits for its stage: the producer never
     // spends a dependent global round trip between two TMA issues
+    const TileRun run = tile_run(n_tiles);
     uint32_t nr0 = 0, nr1 = 0, np0 = 0, np1 = 0, nh0 = 0, nh1 = 0;
-    if (blockIdx.x < n_tiles) {
-      nr0 = tile_row[blockIdx.x];
-      nr1 = tile_row[blockIdx.x + 1];
-      np0 = tile_ptr[blockIdx.x];
-      np1 = tile_ptr[blockIdx.x + 1];
+    if (run.first < run.end) {
+      nr0 = tile_row[run.first];
+      nr1 = tile_row[run.first + 1];
+      np0 = tile_ptr[run.first];
+      np1 = tile_ptr[run.first + 1];
       if (tile_long) {
-        nh0 = tile_long[blockIdx.x];
-        nh1 = tile_long[blockIdx.x + 1];
+        nh0 = tile_long[run.first];
+        nh1 = tile_long[run.first + 1];
       }
     }
     // ring position: stage s and the parity of its fill (no integer
     // division per tile: it cost ~25 instructions per tile and warp)
     uint32_t i = 0, s = 0, ph = 0;
-    for (uint32_t t = blockIdx.x; t < n_tiles;
-         t += grid, ++i, s = (s + 1 == stages) ? 0 : s + 1, ph ^= (s == 0)) {
+    for (uint32_t t = run.first; t < run.end;
+         t += run.step, ++i, s = (s + 1 == stages) ? 0 : s + 1, ph ^= (s == 0)) {
       const uint32_t r0 = nr0, r1 = nr1, p0 = np0, p1 = np1, h0 = nh0, h1 = nh1;
-      if (t + grid < n_tiles) {
-        nr0 = tile_row[t + grid];
-        nr1 = tile_row[t + grid + 1];
-        np0 = tile_ptr[t + grid];
-        np1 = tile_ptr[t + grid + 1];
+      const uint32_t tn = t + run.step;
+      if (tn < run.end) {
+        nr0 = tile_row[tn];
+        nr1 = tile_row[tn + 1];
+        np0 = tile_ptr[tn];
+        np1 = tile_ptr[tn + 1];
         if (tile_long) {
-          nh0 = tile_long[t + grid];
-          nh1 = tile_long[t + grid + 1];
+          nh0 = tile_long[tn];
+          nh1 = tile_long[tn + 1];
         }
       }
       if (i >= stages) mbar_wait(&empty[s], ph ^ 1u);
@@ -824,10 +847,11 @@ __global__ void __launch_bounds__(kThreads, 2)
   const int ct = tid - 32;
   double dot = 0.0;  // DOT: this thread's x . y partial over its rows
   uint32_t s = 0, ph = 0;
-  for (uint32_t t = blockIdx.x; t < n_tiles;
-       t += grid, s = (s + 1 == stages) ? 0 : s + 1, ph ^= (s == 0)) {
+  const TileRun run = tile_run(n_tiles);
+  for (uint32_t t = run.first; t < run.end;
+       t += run.step, s = (s + 1 == stages) ? 0 : s + 1, ph ^= (s == 0)) {
     mbar_wait(&full[s], ph);
-    if (CSRK_TIMELINE && ct == 0 && t == blockIdx.x) TL_MARK(2);
+    if (CSRK_TIMELINE && ct == 0 && t == run.first) TL_MARK(2);
     const StageMeta md = meta[s];
     if (md.mode == kStaged) {
       const unsigned char *st = stage0 + s * geo.stage_bytes;
