@@ -294,11 +294,14 @@ def run_ours(args, log):
         clk.load_until(step, torch.cuda.synchronize)
         torch.cuda.synchronize()
         if flush:
+            # one untimed pass over every replica after the clock sampler's
+            # load (which ran replica 0 only): the timed steps continue the
+            # rotation, each replica last touched len(reps) steps earlier
+            for d, xr, yr in reps:
+                ck.spmv_device(d, xr, yr, dims=dims, variant=variant, stream=stream)
             ev0.record(stream)
-            # replica 0 is the one the clock sampler's warm load just ran:
-            # the rotation starts at replica 1
             for i in range(args.steps):
-                d, xr, yr = reps[(i + 1) % len(reps)]
+                d, xr, yr = reps[i % len(reps)]
                 ck.spmv_device(d, xr, yr, dims=dims, variant=variant, stream=stream)
             ev1.record(stream)
             torch.cuda.synchronize()
