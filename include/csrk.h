@@ -145,7 +145,12 @@ int csrk_matrix_prepare(csrk_matrix *m, int value_type, int variant, int nx);
  * arithmetic of emulate_gpu_spmv35 (kernels.py:284-324) with CSRK_STRIDED
  * and nx = dims.x (1..32).  value_type selects f64 x/y/vals or f32
  * x/y/vals (f32 products are accumulated in f64 and rounded once).
- * Asynchronous on `stream`. */
+ * Asynchronous on `stream`, launched with programmatic dependent launch
+ * (CSRK_PDL=0 disables it): the launch may begin streaming the handle's
+ * matrix arrays while the previous kernel on `stream` still runs, and it
+ * reads x and writes y only after that kernel has completed -- ordinary
+ * stream order for x and y; the matrix arrays must not be modified by
+ * kernels on `stream` between launches. */
 int csrk_spmv(const csrk_matrix *m, int value_type, int variant, int nx,
               const void *x, void *y, void *stream);
 /* Same, from host x to host y (H2D, kernel, D2H on an internal stream;
