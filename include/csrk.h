@@ -144,7 +144,8 @@ int csrk_matrix_prepare(csrk_matrix *m, int value_type, int variant, int nx);
  * spmv_csr3 (kernels.py:209-221, k=3) with variant CSRK_SERIAL, and the
  * arithmetic of emulate_gpu_spmv35 (kernels.py:284-324) with CSRK_STRIDED
  * and nx = dims.x (1..32).  value_type selects f64 x/y/vals or f32
- * x/y/vals (f32 products are accumulated in f64 and rounded once).
+ * x/y/vals (f32: batches of up to 8 products summed with fp32 FMAs, each
+ * batch folded into an f64 row accumulator, rounded to f32 once).
  * Asynchronous on `stream`, launched with programmatic dependent launch
  * (CSRK_PDL=0 disables it): the launch may begin streaming the handle's
  * matrix arrays while the previous kernel on `stream` still runs, and it
