@@ -24,7 +24,7 @@ for mg in torch native; do
     bench.py --gpus 1 --mg $mg > $O/bench_dist1_$mg.json 2> $O/bench_dist1_$mg.err; echo "dist1 $mg rc=$?"
 done
 timeout 1500 python bench.py --impl reference > $O/bench_reference.json 2> $O/bench_reference.err; echo "ref rc=$?"
-for cfg in C1 C3 C5; do
+for cfg in ${REF_CFGS-C1 C3 C5}; do
   timeout 900 python bench.py --impl reference --config $cfg > $O/bench_reference_$cfg.json 2> $O/bench_reference_$cfg.err; echo "ref $cfg rc=$?"
 done
 # launch list of the default bench command (cold-cache, serialised per-launch times)
