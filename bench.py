@@ -474,12 +474,16 @@ def run_loop(args, log):
     ms = ev0.elapsed_time(ev1) / args.steps
     spmv_flops = 2.0 * nnz * iters
     gflops = spmv_flops / (ms * 1e-3) / 1e9
-    # bytes per iteration: the SpMV plus the vector kernels (CG: update reads
-    # 4n writes 2n, direction reads 2n writes n, and p.Ap -- fused into the
-    # SpMV's epilogue for this serial-order launch, csrk_cg, so it reads no
-    # vector of its own -- power: 2n + 2n)
-    fused_dot = args.loop == "cg" and os.environ.get("CSRK_NO_FUSED_DOT") is None
-    vec_words = (9 * n if fused_dot else 11 * n) if args.loop == "cg" else 4 * n
+    # algorithmic bytes per iteration: the SpMV plus the vector work (CG:
+    # update reads 4n writes 2n, direction reads 2n writes n, and p.Ap needs
+    # no vector traffic of its own when fused into the SpMV's epilogue --
+    # power: 2n + 2n).  The count stays 9n whether or not this launch fuses
+    # p.Ap (fp64 does; fp32 runs the separate dot kernel, which re-reads p and
+    # Ap but is faster overall, csrc/spmv.cu launch_spmv_dot): the roofline is
+    # against the algorithm's bytes, not the implementation's.
+    fused_dot = (args.loop == "cg" and os.environ.get("CSRK_NO_FUSED_DOT") is None
+                 and (not f32 or os.environ.get("CSRK_FUSED_DOT_F32") == "1"))
+    vec_words = 9 * n if args.loop == "cg" else 4 * n
     it_bytes = spmv_bytes(n, n, nnz, vb) + vec_words * vb
     gbs = it_bytes * iters / (ms * 1e-3) / 1e9
     peak, peak_src = measured_peak()

@@ -65,6 +65,9 @@ __device__ __forceinline__ double fold_partials(const double *partials) {
 #ifndef CSRK_CG_VEC
 #define CSRK_CG_VEC 1
 #endif
+#ifndef CSRK_CG_UNROLL  // direction kernel: two float4 of p and r in flight
+#define CSRK_CG_UNROLL 1  // (C4 f32 270 -> 248 us, profiles/r02_c4_f32_split.txt)
+#endif
 
 __device__ __forceinline__ float sq4(float4 v) {
   return fmaf(v.w, v.w, fmaf(v.z, v.z, fmaf(v.y, v.y, v.x * v.x)));
@@ -162,7 +165,18 @@ __device__ __forceinline__ void direction_thread(T *__restrict__ p, const T *__r
     const VecSpan v(n);
     float4 *p4 = reinterpret_cast<float4 *>(p);
     const float4 *r4 = reinterpret_cast<const float4 *>(r);
+#if CSRK_CG_UNROLL
+    // two float4 of p and r in flight per thread before the stores
+    int64_t i = v.tid;
+    for (; i + v.stride < v.n4; i += 2 * v.stride) {
+      const float4 pa = p4[i], ra = r4[i], pb = p4[i + v.stride], rb = r4[i + v.stride];
+      p4[i] = axpy4(bf, pa, ra);
+      p4[i + v.stride] = axpy4(bf, pb, rb);
+    }
+    if (i < v.n4) p4[i] = axpy4(bf, p4[i], r4[i]);
+#else
     for (int64_t i = v.tid; i < v.n4; i += v.stride) p4[i] = axpy4(bf, p4[i], r4[i]);
+#endif
     for (int64_t i = (v.n4 << 2) + v.tid; i < n; i += v.stride) p[i] = fmaf(bf, p[i], r[i]);
   } else {
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;

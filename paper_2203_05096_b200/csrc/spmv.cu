@@ -1821,8 +1821,15 @@ int launch_spmv_dot(const csrk_matrix *m, int value_type, int variant, int nx,
         m, m->vals64, static_cast<const double *>(x), static_cast<double *>(y), stream, 0,
         m->plan.n_tiles, dot_part, dot_slots);
   }
+  // fp32: the separate dot kernel.  The fused epilogue's per-row fp64 work
+  // (two F2F.F64.F32, a DMUL, a DADD and the x[r] load) slows the fp32
+  // streaming kernel by more than the dot kernel's re-read of p and Ap
+  // costs: C4 512^3 SpMV 1425.5 us + dot 165.6 us vs 1643.6 us fused (ncu),
+  // 2.458 vs 2.497 ms per CG iteration (profiles/r02_c4_f32_split.txt).
+  // CSRK_FUSED_DOT_F32=1 keeps the fused launch for fp32.
   if (value_type == CSRK_F32) {
-    if (!m->vals32) return CSRK_OK;
+    const char *f = std::getenv("CSRK_FUSED_DOT_F32");
+    if (!m->vals32 || !(f && f[0] == '1')) return CSRK_OK;
     *fused = true;
     return launch_stream<float, 0, false, 4, true>(
         m, m->vals32, static_cast<const float *>(x), static_cast<float *>(y), stream, 0,

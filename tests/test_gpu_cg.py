@@ -164,6 +164,7 @@ def test_cg_fused_dot_matches_separate_dot(dtype, monkeypatch):
     b = torch.from_numpy(np.random.default_rng(4).uniform(-1, 1, n)).cuda()
     if dtype == "f32":
         b = b.float()
+        monkeypatch.setenv("CSRK_FUSED_DOT_F32", "1")  # fp32 runs unfused by default
     x_f, info_f = cg.cg(m, b, iters=40)
     x_f2, _ = cg.cg(m, b, iters=40)
     assert torch.equal(x_f, x_f2)
