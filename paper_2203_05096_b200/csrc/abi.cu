@@ -661,7 +661,7 @@ int csrk_matrix_plan(const csrk_matrix *m, int64_t out[10]) {
   out[4] = m->plan.n_tiles;
   out[5] = m->plan.group_aligned ? 1 : 0;
   out[6] = m->plan.gather_first;
-  out[7] = m->plan.ctas_per_sm ? m->plan.ctas_per_sm : auto_ctas(m->plan.row_var, 8);
+  out[7] = m->plan.ctas_per_sm ? m->plan.ctas_per_sm : auto_ctas(m->plan.row_var, 8, m->plan.n_long, m->plan.mean_short);
   out[8] = m->plan.cut_mode;
   out[9] = m->plan.n_long;
   return CSRK_OK;

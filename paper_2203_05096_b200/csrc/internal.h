@@ -42,9 +42,23 @@ constexpr int64_t kLongRow = 128;  // rows longer than this are summed a warp ea
 //    nonzero, so more tiles in flight);
 //  * the serial order over rows longer than 16 nonzeros gathers first
 //    (C3 +13 %); short rows keep the inline gathers (C2 -15 % otherwise).
-inline int auto_ctas(double row_var, int value_bytes) {
-  return row_var > 10.0 ? 2 : (value_bytes == 4 ? 4 : 3);
+//  * irregular rows without long rows whose lengths spread less than their
+//    mean squared (C5; the inline-gather class below): tiles of 1536, 2
+//    stages, 3 CTAs -- the same shared memory and carveout as 2 x 2 x 2048,
+//    one more tile in flight per SM (C5 f64 0.2066 -> 0.2037 ms, f32 0.1789
+//    -> 0.1717).  Wider spreads (power-law rows capped at 64 / 128, f64
+//    gather-first) keep 2048 x 2 x 2: 0.1356 vs 0.1394 ms
+//    (profiles/r02_c5_plan_confirm.jsonl).
+inline bool irregular_inline(double row_var, double mean_row, int64_t n_long) {
+  return row_var > 10.0 && n_long == 0 && row_var <= mean_row * mean_row;
 }
+inline int auto_ctas(double row_var, int value_bytes, int64_t n_long = 1,
+                     double mean_row = 0.0) {
+  if (row_var > 10.0) return irregular_inline(row_var, mean_row, n_long) ? 3 : 2;
+  return value_bytes == 4 ? 4 : 3;
+}
+// tile cost base of the auto plan (auto_tile_cost refines it per order)
+inline bool small_tiles(double row_var, int64_t n_long, double mean_row);
 #ifndef CSRK_OLD_AUTO
 // regular rows without long rows: 3-stage ring at tile 1536; otherwise the
 // round-1 plan (2 stages, tile 2048: auto_tile_cost below)
@@ -54,6 +68,9 @@ inline bool deep_ring(double, int64_t) { return false; }
 #endif
 inline int64_t auto_stages(double row_var, int64_t n_long) {
   return deep_ring(row_var, n_long) ? 3 : 2;
+}
+inline bool small_tiles(double row_var, int64_t n_long, double mean_row) {
+  return deep_ring(row_var, n_long) || irregular_inline(row_var, mean_row, n_long);
 }
 // Gather first in the serial order when rows are long (C3: 27-nonzero rows)
 // or their lengths spread wider than their mean (a thread per row then waits

@@ -1239,7 +1239,8 @@ int launch_stream(const csrk_matrix *m, const V *vals, const V *x, V *y,
   int cur_dev = 0;
   CSRK_CUDA_TRY(cudaGetDevice(&cur_dev));
   const int ctas = pl.ctas_per_sm > 0 ? pl.ctas_per_sm
-                                      : auto_ctas(pl.row_var, static_cast<int>(sizeof(V)));
+                                      : auto_ctas(pl.row_var, static_cast<int>(sizeof(V)),
+                                                  pl.n_long, pl.mean_short);
   const size_t extra =
       long_beside(m, NX == 0 ? CSRK_SERIAL : CSRK_STRIDED, NX) ? kBesideBlocks * kLongBlockSmem : 0;
   int per_sm = 0;
@@ -1777,7 +1778,7 @@ int prepare_plan(const csrk_matrix *cm, int value_type, int variant, int nx) {
   if (m->n_rows == 0) return CSRK_OK;
   if (!m->plan.row_stats) CSRK_TRY(ensure_plan(m, 0, 0, 0, m->stream));
   if (!m->plan.auto_tile) return CSRK_OK;
-  const bool deep = deep_ring(m->plan.row_var, m->plan.n_long);
+  const bool deep = small_tiles(m->plan.row_var, m->plan.n_long, m->plan.mean_short);
   const int64_t tc = auto_tile_cost(m->plan.mean_short, variant, nx,
                                     deep ? kDeepRingTileCost : kDefaultTileCost);
   const int64_t st = auto_stages(m->plan.row_var, m->plan.n_long);

@@ -12,6 +12,7 @@ import numpy as np
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 import bench  # noqa: E402
 import paper_2203_05096_b200 as ck  # noqa: E402
 from paper_2203_05096_b200.bench import spmv_bytes  # noqa: E402
@@ -20,7 +21,12 @@ from paper_2203_05096_b200.bench import spmv_bytes  # noqa: E402
 def main():
     cfg, tile, stages, ctas = sys.argv[1], int(sys.argv[2]), int(sys.argv[3]), int(sys.argv[4])
     f32 = "--fp32" in sys.argv
-    a, m, xp, params, _ = bench.build_matrix(cfg, lambda s: print(s, file=sys.stderr))
+    if cfg.startswith("PL"):  # power-law rows capped at int(cfg[2:]) (tools/powerlaw_probe.py)
+        from powerlaw_probe import build_powerlaw
+        a, m, _, params = build_powerlaw(2_000_000, int(cfg[2:]))
+        xp = np.random.default_rng(0).uniform(-1.0, 1.0, a.n_rows)
+    else:
+        a, m, xp, params, _ = bench.build_matrix(cfg, lambda s: print(s, file=sys.stderr))
     variant = "strided" if params.kernel_variant.value == "cuda35" else "serial"
     dims = params.block_dims
     dt = torch.float32 if f32 else torch.float64
