@@ -382,7 +382,7 @@ def run_ours(args, log):
                    "ssrs_target": params.ssrs, "srs_target": params.srs,
                    "n_sr": m.num_super_rows, "n_ssr": m.num_ssr,
                    "kernel": f"csrk_stream_kernel ({variant})",
-                   "plan": {k: v for k, v in m.device().plan().items()
+                   "plan": {k: v for k, v in m.device().plan(f32=f32).items()
                             if k in ("tile_cost", "stages", "n_tiles", "group_aligned",
                                      "gather_first", "ctas_per_sm", "n_long")},
                    "parallelism": "1 GPU",

@@ -114,6 +114,9 @@ int csrk_matrix_set_plan(csrk_matrix *m, int64_t tile_cost, int64_t cap,
  *       ctas_per_sm (the f64 value when auto), cut mode, n_long (rows
  *       longer than 128 nonzeros, summed by the long-row kernel) */
 int csrk_matrix_plan(const csrk_matrix *m, int64_t out[10]);
+/* CTAs per SM a launch with this value type uses (out[7] of
+ * csrk_matrix_plan is the f64 figure; fp32 runs 4 per SM on regular rows). */
+int csrk_matrix_plan_ctas(const csrk_matrix *m, int value_type, int64_t *ctas);
 /* Schedule of the streaming kernel (B200 tuning knobs with no reference
  * counterpart; results are bitwise identical under every setting).
  * gather: 0 = inline (each row gathers its x while summing), 1 = gather-first

@@ -49,6 +49,7 @@ _SIGNATURES = {
     "csrk_matrix_add_f32": ([P], C.c_int),
     "csrk_matrix_set_plan": ([P, I64, I64, I64], C.c_int),
     "csrk_matrix_plan": ([P, I64P], C.c_int),
+    "csrk_matrix_plan_ctas": ([P, C.c_int, I64P], C.c_int),
     "csrk_matrix_set_schedule": ([P, C.c_int, C.c_int], C.c_int),
     "csrk_matrix_set_cut_mode": ([P, C.c_int], C.c_int),
     "csrk_matrix_prepare": ([P, C.c_int, C.c_int, C.c_int], C.c_int),
@@ -321,12 +322,18 @@ class DeviceMatrix:
         """Build the tile plan a launch of this order would use (no launch)."""
         call("csrk_matrix_prepare", self.ptr, CSRK_F32 if f32 else CSRK_F64, variant, nx)
 
-    def plan(self) -> dict:
+    def plan(self, f32: bool = False) -> dict:
+        """The tile plan; ``ctas_per_sm`` is the figure a launch with the
+        given value type uses (fp32 runs more CTAs on regular rows)."""
         out = np.zeros(10, dtype=np.int64)
         call("csrk_matrix_plan", self.ptr, i64p(out))
         keys = ("tile_cost", "cap", "rcap", "stages", "n_tiles", "group_aligned",
                 "gather_first", "ctas_per_sm", "cut_mode", "n_long")
-        return {k: int(v) for k, v in zip(keys, out)}
+        d = {k: int(v) for k, v in zip(keys, out)}
+        c = np.zeros(1, dtype=np.int64)
+        call("csrk_matrix_plan_ctas", self.ptr, CSRK_F32 if f32 else CSRK_F64, i64p(c))
+        d["ctas_per_sm"] = int(c[0])
+        return d
 
     def stats(self):
         out = np.zeros(5, dtype=np.int64)

@@ -667,6 +667,17 @@ int csrk_matrix_plan(const csrk_matrix *m, int64_t out[10]) {
   return CSRK_OK;
 }
 
+int csrk_matrix_plan_ctas(const csrk_matrix *m, int value_type, int64_t *ctas) {
+  if (!m || !ctas || (value_type != CSRK_F64 && value_type != CSRK_F32)) {
+    set_error("invalid argument to csrk_matrix_plan_ctas");
+    return CSRK_EINVAL;
+  }
+  *ctas = m->plan.ctas_per_sm ? m->plan.ctas_per_sm
+                              : auto_ctas(m->plan.row_var, value_type == CSRK_F32 ? 4 : 8,
+                                          m->plan.n_long, m->plan.mean_short);
+  return CSRK_OK;
+}
+
 int csrk_matrix_set_cut_mode(csrk_matrix *m, int mode) {
   if (!m) {
     set_error("null argument");
